@@ -1,0 +1,169 @@
+/*
+ * fastmnmf.h -- C ABI of the B200-native FastMNMF update (libfastmnmf.so).
+ *
+ * Plain pointers and sizes only; every device pointer is a CUDA global-memory
+ * address, every `stream` a cudaStream_t passed as void*. Arrays are dense,
+ * row-major ("C order"), with the axis order of the reference's suffixed
+ * names: X_FTM (F,T,M) complex, xt_FTM (F,T,M) real,
+ * g_NFM (N,F,M), lam_NFT (N,F,T), W_NFK (N,F,K), H_NKT (N,K,T), Q_FMM (F,M,M)
+ * complex with ROW m OF Q_f = q_fm^H, V_FMMM (F,M,M,M) complex. Complex
+ * numbers are interleaved (re, im). The fused entry points carry a leading
+ * batch axis B (independent mixtures; BASELINE config 2).
+ *
+ * dtype: FM_F32 = complex64/float32 storage and arithmetic (fp64 for the
+ * log-likelihood accumulation and the M x M solves), FM_F64 =
+ * complex128/float64 throughout (the reference's only precision).
+ *
+ * Reference seam replaced (paths relative to /root/reference/pkg/src/fastsep):
+ * the reference has no C ABI; its operator seam is the Python module
+ * _kernels.py (backend picked at import, _kernels.py:16-31). Each fm_* per-op
+ * function below replaces one function of that seam (or of spatial.py /
+ * separate.py that wraps it), cited on its declaration. The fused
+ * fm_iterate* entry points replace one _DiagLoop.iterate call
+ * (separate.py:201-234).
+ *
+ * Return value: 0 on success, otherwise an FM_E* code; fm_last_error() gives
+ * a message. Numerical failures inside a kernel (the reference's
+ * SingularMatrixError, spatial.py:189-198 / separate.py:121-124) are not
+ * return codes: they are written to a device status word (see FM_STATUS_*)
+ * that the host reads when it synchronises.
+ */
+#ifndef FASTMNMF_H
+#define FASTMNMF_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FM_F32 0
+#define FM_F64 1
+
+#define FM_OK 0
+#define FM_EINVAL 1     /* bad sizes / dtype / unsupported M (1..16 supported) */
+#define FM_ECUDA 2      /* a CUDA launch or API call failed */
+
+/* Device status word (uint64, initialise to FM_STATUS_CLEAR). Kernels
+ * atomicMin an encoded key, so the first failure in (iteration, row m,
+ * frequency f) order wins -- the one the reference would raise first. */
+#define FM_STATUS_CLEAR 0xFFFFFFFFFFFFFFFFull
+#define FM_STATUS_NONPOS_NORM 1 /* spatial.py:194-198 "non-positive normalization" */
+#define FM_STATUS_SINGULAR_QV 2 /* spatial.py:189-192 zgesv LinAlgError */
+#define FM_STATUS_SINGULAR_Q 3  /* separate.py:121-124 inv(Q) LinAlgError */
+/* key = iteration<<44 | m<<24 | f<<2 | code  (f is the GLOBAL bin index). */
+
+/* ---- per-op entry points (the _kernels.py seam) -------------------------- */
+
+/* _kernels.fast_stats (_kernels.py:254-267; numba :208-251). Outputs that are
+ * not wanted may be NULL. phi1/phi2 (N,F,T); gnum/gden (N,F,M); *loglik_host
+ * receives the data term sum(-x~/y - log y) (synchronises the stream). */
+int fm_fast_stats(int dtype, int64_t F, int64_t T, int64_t M, int64_t N,
+                  const void* xt, const void* g, const void* lam, double floor,
+                  int want_gain, int want_phi, void* phi1, void* phi2, void* gnum,
+                  void* gden, double* loglik_host, void* stream);
+
+/* _kernels.mix_power (_kernels.py:325-331): y = max(sum_n lam g, floor). */
+int fm_mix_power(int dtype, int64_t N, int64_t F, int64_t T, int64_t M, const void* lam,
+                 const void* g, double floor, void* y, void* stream);
+
+/* _kernels.ip_weights (_kernels.py:296-302): V[f,m] = (1/T) sum_t x x^H / y. */
+int fm_ip_weights(int dtype, int64_t F, int64_t T, int64_t M, const void* X, const void* y,
+                  void* V, void* stream);
+
+/* _kernels.project_power (_kernels.py:353-359): xt = |Q x|^2. */
+int fm_project_power(int dtype, int64_t F, int64_t T, int64_t M, const void* Q,
+                     const void* X, void* xt, void* stream);
+
+/* spatial.update_diagonalizer (spatial.py:172-200), in place on Q.
+ * status: device uint64 (see FM_STATUS_*; iteration field 0). */
+int fm_update_diagonalizer(int dtype, int64_t F, int64_t T, int64_t M, void* Q,
+                           const void* X, const void* y, int sweeps, uint64_t* status,
+                           void* stream);
+
+/* np.linalg.slogdet(Q)[1] per bin (spatial.py:241, separate.py:238): (F) fp64. */
+int fm_logdet(int dtype, int64_t F, int64_t M, const void* Q, double* logdet, void* stream);
+
+/* separate.wiener_fast (separate.py:110-125): images (N,F,T,M) complex. */
+int fm_wiener_fast(int dtype, int64_t N, int64_t F, int64_t T, int64_t M, const void* lam,
+                   const void* Q, const void* g, const void* X, void* images,
+                   uint64_t* status, void* stream);
+
+/* ---- fused FastMNMF iteration (_DiagLoop, separate.py:175-243) ----------- */
+
+typedef struct fm_dims {
+  int64_t B;        /* independent mixtures (batch) */
+  int64_t F;        /* frequency bins held by this process */
+  int64_t T, M, N, K;
+  int64_t f_offset; /* global index of local bin 0 (frequency sharding) */
+  int32_t dtype;    /* FM_F32 | FM_F64 */
+  int32_t normalize;/* SeparatorConfig.normalize (separate.py:52) */
+  int32_t ip_sweeps;/* SeparatorConfig.ip_sweeps (separate.py:53) */
+  int32_t reserved;
+} fm_dims;
+
+typedef struct fm_state {
+  void* X;        /* (B,F,T,M) complex: scaled observation Xs (separate.py:293) */
+  void* xt;       /* (B,F,T,M) real: projected power (separate.py:183, :230) */
+  void* Q;        /* (B,F,M,M) complex */
+  void* g;        /* (B,N,F,M) real */
+  void* W;        /* (B,N,F,K) real */
+  void* H;        /* (B,N,K,T) real (replicated across frequency shards) */
+  void* floor;    /* (B) real: 1e-12 max|Xs|^2 (spatial.py:64-66) */
+  double* trace;  /* (n_iterations, B): loglik of the state after iteration i */
+  uint64_t* status; /* device status word */
+  void* work;     /* fm_workspace_bytes() bytes, 256-B aligned */
+} fm_state;
+
+/* Workspace: lambda (B,N,F,T), phi (B,2,N,F,T), H-statistic partials, bin
+ * partials of the log-likelihood, counters. */
+size_t fm_workspace_bytes(const fm_dims* d);
+
+/* NmfSource.lam (sources.py:184-187): lam (B,N,F,T) = W (B,N,F,K) H (B,N,K,T). */
+int fm_nmf_lambda(const fm_dims* d, const void* W, const void* H, void* lam, void* stream);
+
+/* Zero counters; compute lambda = W H and the projected power xt = |Q X|^2 and
+ * the first statistics pass of iteration 0 (separate.py:183, :186-193). */
+int fm_prologue(const fm_dims* d, const fm_state* s, void* stream);
+
+/* One full iteration (separate.py:201-234) on one process. Appends
+ * trace[i] (i = number of previous fm_iterate calls since fm_prologue) =
+ * data term + 2T sum_f log|det Q_f| of the state after this iteration. */
+int fm_iterate(const fm_dims* d, const fm_state* s, void* stream);
+
+/* Frequency-sharded iteration, split around the one exchange step: phase 0
+ * runs the W update and the H statistics of this shard and leaves the packed
+ * [num_H | den_H] (B,2,N,K,T) sums in *hstat (device, caller-sized); the
+ * caller all-reduces it (sum) across shards; phase 1 applies the H update
+ * from *hstat and runs the per-frequency rest of the iteration. */
+int fm_iterate_phase(const fm_dims* d, const fm_state* s, int phase, void* hstat,
+                     void* stream);
+
+/* fm_iterate with CUDA events recorded between its five launches on `stream`
+ * (synchronises): ms_host[0..4] = device ms of k_wupdate, k_hstats,
+ * k_hupdate, k_lambda, k_spatial. Used by bench.py for the roofline. */
+int fm_iterate_profiled(const fm_dims* d, const fm_state* s, float* ms_host, void* stream);
+
+/* n fm_iterate calls, optionally captured once into a CUDA graph that is
+ * replayed (launch-bound configs). */
+int fm_run(const fm_dims* d, const fm_state* s, int n_iterations, int use_graph,
+           void* stream);
+
+/* The observation prologue of run() (separate.py:284-293, spatial.py:64-66),
+ * split so a frequency-sharded caller can all-reduce in between:
+ * fm_observation_stats -> per mixture sum|X|^2 and max|X|^2 (fp64, host
+ * arrays of B); fm_scale_observation -> X /= scale[b] in place (device,
+ * scale given on the host, fp64). floor = 1e-12 max|Xs|^2 is then the
+ * max of a second fm_observation_stats call, exactly as power_floor does. */
+int fm_observation_stats(const fm_dims* d, const void* X, double* sumsq_host,
+                         double* maxsq_host, void* stream);
+int fm_scale_observation(const fm_dims* d, void* X, const double* scale_host, void* stream);
+
+const char* fm_last_error(void);
+int fm_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FASTMNMF_H */

@@ -1,0 +1,172 @@
+"""Generate tests/golden/*.npz by running the UNMODIFIED reference ``fastsep``.
+
+Run in the build container only (``/root/reference`` does not exist on the GPU
+box):
+
+    NUMBA_CACHE_DIR=/tmp/numba_cache PYTHONDONTWRITEBYTECODE=1 \
+        python oracle/make_golden.py
+
+It imports ``fastsep`` from ``/root/reference/pkg/src`` and drives it through
+its own public/kernel API:
+
+* ``kernels.npz``  -- seeded small inputs and the outputs of the reference
+  kernels ``_kernels.fast_stats`` / ``ip_weights`` / ``mix_power`` /
+  ``project_power``, ``spatial.update_diagonalizer``, ``normalize_gains``,
+  ``loglik_fast`` and ``separate.wiener_fast``;
+* ``run_*.npz``    -- ``fastsep.run(SeparatorConfig(method="fast-mnmf"), X)``
+  with the BASELINE init injected by the SURVEY §8(c) recipe (monkeypatched
+  ``_build_spatial`` / ``_build_source``), recording the likelihood trace,
+  final W/H/g/Q and the separated images (in full for small shapes, as a
+  strided sample plus norms for the larger ones).
+"""
+
+import os
+import sys
+import time
+
+os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache")
+os.environ.setdefault("PYTHONDONTWRITEBYTECODE", "1")
+sys.dont_write_bytecode = True
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, "/root/reference/pkg/src")
+sys.path.insert(0, REPO)
+
+import fastsep  # noqa: E402  (the reference)
+from fastsep import _kernels as K  # noqa: E402
+from fastsep import separate as S  # noqa: E402
+from fastsep import spatial as SP  # noqa: E402
+from fastsep import sources as SRC  # noqa: E402
+
+from paper_1903_03237_b200.synth import baseline_init, make_mixture  # noqa: E402
+
+OUT = os.path.join(REPO, "tests", "golden")
+
+
+def kernel_cases():
+    out = {}
+    rng = np.random.default_rng(20240811)  # reference conftest.py:53-55 seed
+    # fast_stats cases: test_kernels.py:28-34 shape and two extra shapes
+    for tag, (F, T, M, N) in {"a": (7, 30, 5, 2), "b": (4, 33, 8, 4), "c": (3, 40, 1, 3)}.items():
+        xt = rng.uniform(0.0, 3.0, (F, T, M))
+        g = rng.uniform(0.1, 2.0, (N, F, M))
+        lam = rng.uniform(0.1, 2.0, (N, F, T))
+        out[f"fs_{tag}_xt"], out[f"fs_{tag}_g"], out[f"fs_{tag}_lam"] = xt, g, lam
+        for floor in (0.0, 0.5):
+            for wg in (False, True):
+                for wp in (False, True):
+                    p1, p2, gn, gd, ll = K.fast_stats(xt, g, lam, floor, wg, wp)
+                    key = f"fs_{tag}_{floor}_{int(wg)}{int(wp)}"
+                    out[key + "_phi1"], out[key + "_phi2"] = p1, p2
+                    out[key + "_gnum"], out[key + "_gden"] = gn, gd
+                    out[key + "_ll"] = np.float64(ll)
+        out[f"fs_{tag}_mix"] = K.mix_power(lam, g, 0.5)
+    # ip_weights / project_power: test_kernels.py:52-67 shapes + M=16
+    for tag, (F, T, M) in {"a": (5, 40, 4), "b": (3, 17, 3), "c": (2, 64, 16), "d": (3, 20, 1)}.items():
+        X = rng.standard_normal((F, T, M)) + 1j * rng.standard_normal((F, T, M))
+        y = rng.uniform(0.2, 2.0, (F, T, M))
+        Q = rng.standard_normal((F, M, M)) + 1j * rng.standard_normal((F, M, M))
+        out[f"ip_{tag}_X"], out[f"ip_{tag}_y"], out[f"ip_{tag}_Q"] = X, y, Q
+        out[f"ip_{tag}_V"] = K.ip_weights(X, y)
+        out[f"ip_{tag}_xt"] = K.project_power(Q, X)
+        for sweeps in (1, 3):
+            Q0 = np.tile(np.eye(M, dtype=complex), (F, 1, 1)) + 0.1 * Q
+            out[f"ip_{tag}_Q0"] = Q0
+            out[f"ip_{tag}_Qnew{sweeps}"] = SP.update_diagonalizer(Q0, X, y, sweeps)
+        out[f"ip_{tag}_logdet"] = np.linalg.slogdet(Q)[1]
+    # normalize_gains / wiener_fast / loglik_fast
+    F, T, M, N = 6, 25, 4, 3
+    X = rng.standard_normal((F, T, M)) + 1j * rng.standard_normal((F, T, M))
+    Q = rng.standard_normal((F, M, M)) + 1j * rng.standard_normal((F, M, M)) + 2 * np.eye(M)
+    g = rng.uniform(0.1, 2.0, (N, F, M))
+    lam = rng.uniform(0.1, 2.0, (N, F, T))
+    lam[1, 2, 3:7] = 0.0
+    lam[:, 4, 10] = 0.0  # every source zero at one bin -> uniform 1/N gains
+    out.update(wf_X=X, wf_Q=Q, wf_g=g, wf_lam=lam)
+    out["wf_images"] = S.wiener_fast(lam, Q, g, X)
+    gn, c = SP.normalize_gains(g)
+    out["ng_g"], out["ng_c"] = gn, c
+    out["ll_fast"] = np.float64(SP.loglik_fast(X, Q, g, lam, 1e-3))
+    return out
+
+
+def run_injected(X, Q0, g0, W0, H0, n_iter, normalize=True, ip_sweeps=1, snap_every=0):
+    """fastsep.run with the BASELINE init injected."""
+    orig_sp, orig_src = S._build_spatial, S._build_source
+    S._build_spatial = lambda cfg, Xs: SP.DiagSpatial(Q0.copy(), g0.copy())
+    S._build_source = lambda cfg, Xs, rng: SRC.NmfSource(W0.copy(), H0.copy())
+    state = {}
+
+    def snap(it, loop):
+        state.update(W=loop.source.W_NFK.copy(), H=loop.source.H_NKT.copy(),
+                     g=loop.spatial.g_NFM.copy(), Q=loop.spatial.Q_FMM.copy(),
+                     floor=loop.floor)
+
+    try:
+        N, _, K_ = W0.shape
+        cfg = fastsep.SeparatorConfig(method="fast-mnmf", n_sources=N, n_basis=K_,
+                                      n_iterations=n_iter, seed=0, normalize=normalize,
+                                      ip_sweeps=ip_sweeps)
+        t0 = time.perf_counter()
+        res = fastsep.run(cfg, X, on_iteration=snap)
+        dt = time.perf_counter() - t0
+    finally:
+        S._build_spatial, S._build_source = orig_sp, orig_src
+    return res, state, dt
+
+
+def save_run(name, X, F, T, M, N, K_, seed, n_iter, full_images, round64=False, **kw):
+    Q0, g0, W0, H0 = baseline_init(F, T, M, N, K_, seed)
+    if round64:
+        X = X.astype(np.complex64).astype(np.complex128)
+    res, st, dt = run_injected(X, Q0, g0, W0, H0, n_iter, **kw)
+    d = dict(
+        shape=np.array([F, T, M, N, K_, seed, n_iter]),
+        X_abs_sum=np.float64(np.abs(X).sum()), X_sample=X[::13, ::11, :],
+        trace=res.likelihood_trace, W=st["W"], H=st["H"], g=st["g"], Q=st["Q"],
+        floor=np.float64(st["floor"]),
+        img_norm=np.linalg.norm(res.images_NFTM.reshape(N, -1), axis=1),
+    )
+    if full_images:
+        d["images"] = res.images_NFTM
+    else:
+        d["img_sample"] = res.images_NFTM[:, ::17, ::19, :]
+    if round64:
+        for k in ("W", "H", "g"):
+            d[k] = d[k].astype(np.float32)
+        d["Q"] = d["Q"].astype(np.complex64)
+        if "img_sample" in d:
+            d["img_sample"] = d["img_sample"].astype(np.complex64)
+    np.savez_compressed(os.path.join(OUT, name), **d)
+    print(f"{name}: {n_iter} it in {dt:.1f}s, LL {res.likelihood_trace[0]:.6f} -> "
+          f"{res.likelihood_trace[-1]:.6f}", flush=True)
+
+
+def main():
+    os.makedirs(OUT, exist_ok=True)
+    np.savez_compressed(os.path.join(OUT, "kernels.npz"), **kernel_cases())
+    print("kernels.npz written", flush=True)
+    # small end-to-end shapes (full images)
+    for name, (F, T, M, N, K_, it, kw) in {
+        "run_small_a.npz": (16, 40, 3, 2, 4, 10, {}),
+        "run_small_b.npz": (9, 48, 5, 3, 3, 8, {"normalize": False}),
+        "run_small_c.npz": (12, 36, 4, 2, 5, 6, {"ip_sweeps": 2}),
+        "run_small_d.npz": (5, 64, 8, 4, 6, 5, {}),
+    }.items():
+        X = make_mixture(F, T, M, N, K_, seed=3)
+        save_run(name, X, F, T, M, N, K_, 3, it, True, **kw)
+    # config 0: complex128, 50 iterations, seed 0
+    X0 = make_mixture(257, 128, 4, 2, 8, seed=0)
+    save_run("run_c0.npz", X0, 257, 128, 4, 2, 8, 0, 50, False)
+    # config 0 shape in complex64 mode (oracle fed the c64-rounded X)
+    save_run("run_c0_c64.npz", X0, 257, 128, 4, 2, 8, 0, 50, False, round64=True)
+    # config 1 shape, complex64-rounded X, 100 iterations
+    if "--with-c1" in sys.argv:
+        X1 = make_mixture(513, 1024, 8, 4, 16, seed=0)
+        save_run("run_c1_c64.npz", X1, 513, 1024, 8, 4, 16, 0, 100, False, round64=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,196 @@
+// fm_api.cu -- the extern "C" boundary declared in include/fastmnmf.h.
+#include <cstdarg>
+#include <mutex>
+
+#include "fm_impl.cuh"
+
+extern template struct fm::Impl<float>;
+extern template struct fm::Impl<double>;
+
+namespace fm {
+
+static thread_local char g_err[512] = "";
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+int validate_dims(const fm_dims* d) {
+  if (!d) { set_error("null dims"); return FM_EINVAL; }
+  if (d->dtype != FM_F32 && d->dtype != FM_F64) { set_error("dtype %d", d->dtype); return FM_EINVAL; }
+  if (d->B < 1 || d->F < 1 || d->T < 1) { set_error("empty problem B=%lld F=%lld T=%lld", (long long)d->B, (long long)d->F, (long long)d->T); return FM_EINVAL; }
+  if (d->M < 1 || d->M > 16) { set_error("M=%lld outside 1..16", (long long)d->M); return FM_EINVAL; }
+  if (d->N < 1 || d->N > NMAX) { set_error("N=%lld outside 1..%d", (long long)d->N, NMAX); return FM_EINVAL; }
+  if (d->K < 1 || d->K > 64) { set_error("K=%lld outside 1..64", (long long)d->K); return FM_EINVAL; }
+  if (d->ip_sweeps < 1) { set_error("ip_sweeps must be >= 1"); return FM_EINVAL; }
+  if (d->F > 65535 || d->B > 65535) { set_error("F and B must be <= 65535"); return FM_EINVAL; }
+  return FM_OK;
+}
+
+static int check_m(int64_t M) {
+  if (M < 1 || M > 16) { set_error("M=%lld outside 1..16", (long long)M); return FM_EINVAL; }
+  return FM_OK;
+}
+
+// One cached CUDA graph of a full iteration (launch-bound configs).
+struct GraphCache {
+  fm_dims d;
+  fm_state s;
+  cudaGraphExec_t exec = nullptr;
+  cudaStream_t cap = nullptr;
+  bool valid = false;
+};
+static GraphCache g_graph;
+static std::mutex g_graph_mu;
+
+}  // namespace fm
+
+using namespace fm;
+
+#define FM_BY_DTYPE(dt, CALL)                                      \
+  ((dt) == FM_F64 ? Impl<double>::CALL : ((dt) == FM_F32 ? Impl<float>::CALL \
+   : (set_error("dtype %d", (int)(dt)), FM_EINVAL)))
+
+extern "C" {
+
+const char* fm_last_error(void) { return g_err; }
+int fm_version(void) { return 1; }
+
+int fm_fast_stats(int dtype, int64_t F, int64_t T, int64_t M, int64_t N, const void* xt,
+                  const void* g, const void* lam, double floor, int want_gain, int want_phi,
+                  void* phi1, void* phi2, void* gnum, void* gden, double* loglik_host,
+                  void* stream) {
+  if (int rc = check_m(M)) return rc;
+  return FM_BY_DTYPE(dtype, fast_stats(F, T, M, N, xt, g, lam, floor, want_gain, want_phi, phi1,
+                                       phi2, gnum, gden, loglik_host, (cudaStream_t)stream));
+}
+
+int fm_mix_power(int dtype, int64_t N, int64_t F, int64_t T, int64_t M, const void* lam,
+                 const void* g, double floor, void* y, void* stream) {
+  return FM_BY_DTYPE(dtype, mix_power(N, F, T, M, lam, g, floor, y, (cudaStream_t)stream));
+}
+
+int fm_ip_weights(int dtype, int64_t F, int64_t T, int64_t M, const void* X, const void* y,
+                  void* V, void* stream) {
+  if (int rc = check_m(M)) return rc;
+  return FM_BY_DTYPE(dtype, ip_weights(F, T, M, X, y, V, (cudaStream_t)stream));
+}
+
+int fm_project_power(int dtype, int64_t F, int64_t T, int64_t M, const void* Q, const void* X,
+                     void* xt, void* stream) {
+  if (int rc = check_m(M)) return rc;
+  return FM_BY_DTYPE(dtype, project(F, T, M, Q, X, xt, (cudaStream_t)stream));
+}
+
+int fm_update_diagonalizer(int dtype, int64_t F, int64_t T, int64_t M, void* Q, const void* X,
+                           const void* y, int sweeps, uint64_t* status, void* stream) {
+  if (int rc = check_m(M)) return rc;
+  return FM_BY_DTYPE(dtype, update_diagonalizer(F, T, M, Q, X, y, sweeps, status,
+                                                (cudaStream_t)stream));
+}
+
+int fm_logdet(int dtype, int64_t F, int64_t M, const void* Q, double* logdet, void* stream) {
+  if (int rc = check_m(M)) return rc;
+  return FM_BY_DTYPE(dtype, logdet(F, M, Q, logdet, (cudaStream_t)stream));
+}
+
+int fm_wiener_fast(int dtype, int64_t N, int64_t F, int64_t T, int64_t M, const void* lam,
+                   const void* Q, const void* g, const void* X, void* images, uint64_t* status,
+                   void* stream) {
+  if (int rc = check_m(M)) return rc;
+  return FM_BY_DTYPE(dtype, wiener(N, F, T, M, lam, Q, g, X, images, status, (cudaStream_t)stream));
+}
+
+size_t fm_workspace_bytes(const fm_dims* d) {
+  if (validate_dims(d)) return 0;
+  return make_plan(d).total;
+}
+
+int fm_nmf_lambda(const fm_dims* d, const void* W, const void* H, void* lam, void* stream) {
+  if (int rc = validate_dims(d)) return rc;
+  if (d->dtype == FM_F64)
+    return Impl<double>::lambda(d, (const double*)W, (const double*)H, (double*)lam,
+                                (cudaStream_t)stream);
+  return Impl<float>::lambda(d, (const float*)W, (const float*)H, (float*)lam, (cudaStream_t)stream);
+}
+
+int fm_prologue(const fm_dims* d, const fm_state* s, void* stream) {
+  if (int rc = validate_dims(d)) return rc;
+  return FM_BY_DTYPE(d->dtype, prologue(d, s, (cudaStream_t)stream));
+}
+
+int fm_iterate(const fm_dims* d, const fm_state* s, void* stream) {
+  if (int rc = validate_dims(d)) return rc;
+  return FM_BY_DTYPE(d->dtype, iterate_phase(d, s, 2, nullptr, (cudaStream_t)stream));
+}
+
+int fm_iterate_phase(const fm_dims* d, const fm_state* s, int phase, void* hstat, void* stream) {
+  if (int rc = validate_dims(d)) return rc;
+  if (phase != 0 && phase != 1) { set_error("phase must be 0 or 1"); return FM_EINVAL; }
+  return FM_BY_DTYPE(d->dtype, iterate_phase(d, s, phase, hstat, (cudaStream_t)stream));
+}
+
+int fm_iterate_profiled(const fm_dims* d, const fm_state* s, float* ms_host, void* stream) {
+  if (int rc = validate_dims(d)) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaEvent_t ev[6];
+  for (int i = 0; i < 6; ++i) FM_CUDA(cudaEventCreate(&ev[i]));
+  int rc = d->dtype == FM_F64 ? Impl<double>::iterate_phase(d, s, 2, nullptr, st, ev)
+                              : Impl<float>::iterate_phase(d, s, 2, nullptr, st, ev);
+  if (rc == FM_OK) {
+    FM_CUDA(cudaEventSynchronize(ev[5]));
+    for (int i = 0; i < 5; ++i) FM_CUDA(cudaEventElapsedTime(&ms_host[i], ev[i], ev[i + 1]));
+  }
+  for (int i = 0; i < 6; ++i) cudaEventDestroy(ev[i]);
+  return rc;
+}
+
+int fm_run(const fm_dims* d, const fm_state* s, int n_iterations, int use_graph, void* stream) {
+  if (int rc = validate_dims(d)) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (!use_graph) {
+    for (int i = 0; i < n_iterations; ++i)
+      if (int rc = fm_iterate(d, s, stream)) return rc;
+    return FM_OK;
+  }
+  std::lock_guard<std::mutex> lk(g_graph_mu);
+  GraphCache& c = g_graph;
+  const bool same = c.valid && std::memcmp(&c.d, d, sizeof(fm_dims)) == 0 &&
+                    std::memcmp(&c.s, s, sizeof(fm_state)) == 0;
+  if (!same) {
+    if (c.exec) { cudaGraphExecDestroy(c.exec); c.exec = nullptr; }
+    c.valid = false;
+    // first call un-captured: sets kernel attributes outside the capture
+    if (!c.cap) FM_CUDA(cudaStreamCreateWithFlags(&c.cap, cudaStreamNonBlocking));
+    cudaGraph_t graph = nullptr;
+    FM_CUDA(cudaStreamBeginCapture(c.cap, cudaStreamCaptureModeThreadLocal));
+    int rc = fm_iterate(d, s, (void*)c.cap);
+    cudaError_t ce = cudaStreamEndCapture(c.cap, &graph);
+    if (rc) { if (graph) cudaGraphDestroy(graph); return rc; }
+    if (ce != cudaSuccess) { set_error("graph capture: %s", cudaGetErrorString(ce)); return FM_ECUDA; }
+    ce = cudaGraphInstantiate(&c.exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (ce != cudaSuccess) { set_error("graph instantiate: %s", cudaGetErrorString(ce)); return FM_ECUDA; }
+    c.d = *d;
+    c.s = *s;
+    c.valid = true;
+  }
+  for (int i = 0; i < n_iterations; ++i) FM_CUDA(cudaGraphLaunch(c.exec, st));
+  return FM_OK;
+}
+
+int fm_observation_stats(const fm_dims* d, const void* X, double* sumsq_host, double* maxsq_host,
+                         void* stream) {
+  if (int rc = validate_dims(d)) return rc;
+  return FM_BY_DTYPE(d->dtype, obs_stats(d, X, sumsq_host, maxsq_host, (cudaStream_t)stream));
+}
+
+int fm_scale_observation(const fm_dims* d, void* X, const double* scale_host, void* stream) {
+  if (int rc = validate_dims(d)) return rc;
+  return FM_BY_DTYPE(d->dtype, scale(d, X, scale_host, (cudaStream_t)stream));
+}
+
+}  // extern "C"

@@ -1,0 +1,416 @@
+// fm_impl.cuh -- host-side launch logic, templated on the real type.
+// Explicitly instantiated in fm_f32.cu / fm_f64.cu (parallel compilation);
+// fm_api.cu holds the extern "C" boundary (include/fastmnmf.h).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/fastmnmf.h"
+#include "fm_kernels.cuh"
+#include "fm_ops.cuh"
+
+namespace fm {
+
+void set_error(const char* fmt, ...);
+
+#define FM_CHECK_LAUNCH(what)                                                   \
+  do {                                                                          \
+    cudaError_t e_ = cudaGetLastError();                                        \
+    if (e_ != cudaSuccess) {                                                    \
+      set_error("%s: %s", what, cudaGetErrorString(e_));                         \
+      return FM_ECUDA;                                                          \
+    }                                                                           \
+  } while (0)
+
+#define FM_CUDA(call)                                                           \
+  do {                                                                          \
+    cudaError_t e_ = (call);                                                    \
+    if (e_ != cudaSuccess) {                                                    \
+      set_error("%s: %s", #call, cudaGetErrorString(e_));                        \
+      return FM_ECUDA;                                                          \
+    }                                                                           \
+  } while (0)
+
+// M dispatch (M = 1..16), compile-time channel count for the per-bin kernels.
+#define FM_DISPATCH_M(Mrt, ...)                                                \
+  switch (Mrt) {                                                                \
+    case 1: { constexpr int MM = 1; __VA_ARGS__; } break;                              \
+    case 2: { constexpr int MM = 2; __VA_ARGS__; } break;                              \
+    case 3: { constexpr int MM = 3; __VA_ARGS__; } break;                              \
+    case 4: { constexpr int MM = 4; __VA_ARGS__; } break;                              \
+    case 5: { constexpr int MM = 5; __VA_ARGS__; } break;                              \
+    case 6: { constexpr int MM = 6; __VA_ARGS__; } break;                              \
+    case 7: { constexpr int MM = 7; __VA_ARGS__; } break;                              \
+    case 8: { constexpr int MM = 8; __VA_ARGS__; } break;                              \
+    case 9: { constexpr int MM = 9; __VA_ARGS__; } break;                              \
+    case 10: { constexpr int MM = 10; __VA_ARGS__; } break;                            \
+    case 11: { constexpr int MM = 11; __VA_ARGS__; } break;                            \
+    case 12: { constexpr int MM = 12; __VA_ARGS__; } break;                            \
+    case 13: { constexpr int MM = 13; __VA_ARGS__; } break;                            \
+    case 14: { constexpr int MM = 14; __VA_ARGS__; } break;                            \
+    case 15: { constexpr int MM = 15; __VA_ARGS__; } break;                            \
+    case 16: { constexpr int MM = 16; __VA_ARGS__; } break;                            \
+    default: set_error("M=%d outside the supported 1..16", (int)(Mrt)); return FM_EINVAL; \
+  }
+
+#define FM_DISPATCH_KB(Krt, ...)                                               \
+  if ((Krt) <= 4) { constexpr int KB = 4; __VA_ARGS__; }                               \
+  else if ((Krt) <= 8) { constexpr int KB = 8; __VA_ARGS__; }                          \
+  else if ((Krt) <= 16) { constexpr int KB = 16; __VA_ARGS__; }                        \
+  else if ((Krt) <= 32) { constexpr int KB = 32; __VA_ARGS__; }                        \
+  else if ((Krt) <= 64) { constexpr int KB = 64; __VA_ARGS__; }                        \
+  else { set_error("K=%d outside the supported 1..64", (int)(Krt)); return FM_EINVAL; }
+
+inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+// Workspace plan for the fused iteration.
+struct Plan {
+  int G, TT, ntt, FC, FCH;
+  size_t off_lam, off_phi, off_part, off_llp, off_ldp, off_cnt, total;
+  size_t hstats_smem;
+};
+
+inline Plan make_plan(const fm_dims* d) {
+  Plan p;
+  const size_t rs = d->dtype == FM_F64 ? 8 : 4;
+  const long long B = d->B, F = d->F, T = d->T, M = d->M, N = d->N, K = d->K;
+  p.G = std::max<long long>(1, 8 / N);
+  p.TT = 32 * p.G;
+  p.ntt = (int)((T + p.TT - 1) / p.TT);
+  long long fc = (2 * 296 + B * p.ntt - 1) / (B * p.ntt);  // ~4 resident CTAs per SM
+  fc = std::max<long long>(1, std::min<long long>(fc, (F + 3) / 4));
+  long long fch = (F + fc - 1) / fc;
+  // shared-memory cap for the staged W/g rows (~96 KB)
+  const long long per_f = (N * K + N * M) * (long long)rs;
+  const long long fch_cap = std::max<long long>(1, (96 * 1024 - 2 * p.G * N * 32 * (long long)rs) / per_f);
+  fch = std::min(fch, fch_cap);
+  p.FCH = (int)fch;
+  p.FC = (int)((F + fch - 1) / fch);
+  p.hstats_smem = (size_t)(fch * per_f + 2 * p.G * N * 32 * rs);
+  size_t o = 0;
+  p.off_lam = o; o = align256(o + (size_t)B * N * F * T * rs);
+  p.off_phi = o; o = align256(o + (size_t)B * 2 * N * F * T * rs);
+  p.off_part = o; o = align256(o + (size_t)B * p.FC * 2 * N * K * T * rs);
+  p.off_llp = o; o = align256(o + (size_t)B * F * 8);
+  p.off_ldp = o; o = align256(o + (size_t)B * F * 8);
+  p.off_cnt = o; o = align256(o + 64);
+  p.total = o;
+  return p;
+}
+
+int validate_dims(const fm_dims* d);
+
+template <typename R> struct Impl {
+  using C = cplx<R>;
+
+  static int prologue(const fm_dims* d, const fm_state* s, cudaStream_t st);
+  static int iterate_phase(const fm_dims* d, const fm_state* s, int phase, void* hstat,
+                           cudaStream_t st, cudaEvent_t* ev = nullptr);
+  static int lambda(const fm_dims* d, const R* W, const R* H, R* lam, cudaStream_t st);
+  static int spatial(const fm_dims* d, const fm_state* s, int tail_only, int record,
+                     cudaStream_t st);
+
+  static int fast_stats(int64_t F, int64_t T, int64_t M, int64_t N, const void* xt,
+                        const void* g, const void* lam, double floor, int want_gain,
+                        int want_phi, void* phi1, void* phi2, void* gnum, void* gden,
+                        double* ll_host, cudaStream_t st);
+  static int mix_power(int64_t N, int64_t F, int64_t T, int64_t M, const void* lam,
+                       const void* g, double floor, void* y, cudaStream_t st);
+  static int ip_weights(int64_t F, int64_t T, int64_t M, const void* X, const void* y, void* V,
+                        cudaStream_t st);
+  static int project(int64_t F, int64_t T, int64_t M, const void* Q, const void* X, void* xt,
+                     cudaStream_t st);
+  static int update_diagonalizer(int64_t F, int64_t T, int64_t M, void* Q, const void* X,
+                                 const void* y, int sweeps, uint64_t* status, cudaStream_t st);
+  static int logdet(int64_t F, int64_t M, const void* Q, double* out, cudaStream_t st);
+  static int wiener(int64_t N, int64_t F, int64_t T, int64_t M, const void* lam, const void* Q,
+                    const void* g, const void* X, void* out, uint64_t* status, cudaStream_t st);
+  static int obs_stats(const fm_dims* d, const void* X, double* sumsq, double* maxsq,
+                       cudaStream_t st);
+  static int scale(const fm_dims* d, void* X, const double* scale_host, cudaStream_t st);
+};
+
+template <typename Kern>
+inline int ensure_smem(Kern k, size_t bytes) {
+  if (bytes > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e != cudaSuccess) {
+      set_error("cudaFuncSetAttribute(%zu B smem): %s", bytes, cudaGetErrorString(e));
+      return FM_ECUDA;
+    }
+  }
+  return FM_OK;
+}
+
+template <typename R>
+int Impl<R>::lambda(const fm_dims* d, const R* W, const R* H, R* lam, cudaStream_t st) {
+  dim3 grid((unsigned)((d->T + 63) / 64), (unsigned)((d->F + 63) / 64), (unsigned)(d->B * d->N));
+  k_lambda<R><<<grid, 256, 0, st>>>(W, H, lam, (int)d->F, (int)d->T, (int)d->K);
+  FM_CHECK_LAUNCH("k_lambda");
+  return FM_OK;
+}
+
+template <typename R>
+int Impl<R>::spatial(const fm_dims* d, const fm_state* s, int tail_only, int record,
+                     cudaStream_t st) {
+  const Plan p = make_plan(d);
+  unsigned char* w = reinterpret_cast<unsigned char*>(s->work);
+  SpArgs<R> a;
+  a.X = reinterpret_cast<const C*>(s->X);
+  a.xt = reinterpret_cast<R*>(s->xt);
+  a.Q = reinterpret_cast<C*>(s->Q);
+  a.g = reinterpret_cast<R*>(s->g);
+  a.W = reinterpret_cast<R*>(s->W);
+  a.lam = reinterpret_cast<const R*>(w + p.off_lam);
+  a.phi = reinterpret_cast<R*>(w + p.off_phi);
+  a.floorp = reinterpret_cast<const R*>(s->floor);
+  a.ll_part = reinterpret_cast<double*>(w + p.off_llp);
+  a.ld_part = reinterpret_cast<double*>(w + p.off_ldp);
+  a.trace = s->trace;
+  a.counter = reinterpret_cast<unsigned*>(w + p.off_cnt);
+  a.iter = a.counter + 1;
+  a.status = reinterpret_cast<unsigned long long*>(s->status);
+  a.B = (int)d->B; a.F = (int)d->F; a.T = (int)d->T; a.M = (int)d->M; a.N = (int)d->N;
+  a.K = (int)d->K;
+  a.f_offset = d->f_offset;
+  a.normalize = d->normalize;
+  a.ip_sweeps = d->ip_sweeps;
+  a.tail_only = tail_only;
+  a.record = record && s->trace != nullptr;
+  dim3 grid((unsigned)d->F, (unsigned)d->B);
+  FM_DISPATCH_M(d->M, {
+    const size_t sm = spatial_smem_bytes<R, MM>();
+    if (int rc = ensure_smem(k_spatial<R, MM>, sm)) return rc;
+    k_spatial<R, MM><<<grid, SpCfg<MM>::BS, sm, st>>>(a);
+    FM_CHECK_LAUNCH("k_spatial");
+  });
+  return FM_OK;
+}
+
+template <typename R>
+int Impl<R>::prologue(const fm_dims* d, const fm_state* s, cudaStream_t st) {
+  const Plan p = make_plan(d);
+  unsigned char* w = reinterpret_cast<unsigned char*>(s->work);
+  FM_CUDA(cudaMemsetAsync(w + p.off_cnt, 0, 64, st));
+  if (int rc = lambda(d, reinterpret_cast<const R*>(s->W), reinterpret_cast<const R*>(s->H),
+                      reinterpret_cast<R*>(w + p.off_lam), st))
+    return rc;
+  return spatial(d, s, /*tail_only=*/1, /*record=*/0, st);
+}
+
+template <typename R>
+int Impl<R>::iterate_phase(const fm_dims* d, const fm_state* s, int phase, void* hstat,
+                           cudaStream_t st, cudaEvent_t* ev) {
+#define FM_EV(i) \
+  if (ev) FM_CUDA(cudaEventRecord(ev[i], st));
+  const Plan p = make_plan(d);
+  unsigned char* w = reinterpret_cast<unsigned char*>(s->work);
+  R* lam = reinterpret_cast<R*>(w + p.off_lam);
+  R* phi = reinterpret_cast<R*>(w + p.off_phi);
+  R* part = reinterpret_cast<R*>(w + p.off_part);
+  R* W = reinterpret_cast<R*>(s->W);
+  R* H = reinterpret_cast<R*>(s->H);
+  const int N = (int)d->N, F = (int)d->F, T = (int)d->T, M = (int)d->M, K = (int)d->K;
+  const long long NKT = (long long)N * K * T;
+  const long long total = (long long)d->B * NKT;
+  const unsigned hblocks = (unsigned)((total + 255) / 256);
+  // phase 0 (or full): W MU, 2nd statistics pass + H-statistic partials
+  if (phase == 0 || phase == 2) {
+    FM_DISPATCH_KB(K, {
+      dim3 g1((unsigned)((F + 7) / 8), (unsigned)N, (unsigned)d->B);
+      FM_EV(0);
+      k_wupdate<R, KB><<<g1, 256, 0, st>>>(phi, H, W, N, F, T, K);
+      FM_CHECK_LAUNCH("k_wupdate");
+      if (int rc = ensure_smem(k_hstats<R, KB>, p.hstats_smem)) return rc;
+      dim3 g2((unsigned)p.ntt, (unsigned)p.FC, (unsigned)d->B);
+      FM_EV(1);
+      k_hstats<R, KB><<<g2, 32 * N * p.G, p.hstats_smem, st>>>(
+          W, H, reinterpret_cast<const R*>(s->g), reinterpret_cast<const R*>(s->xt),
+          reinterpret_cast<const R*>(s->floor), part, N, F, T, M, K, p.FCH, p.G);
+      FM_CHECK_LAUNCH("k_hstats");
+    });
+  }
+  if (phase == 0) {
+    k_hupdate<R><<<hblocks, 256, 0, st>>>(part, H, reinterpret_cast<R*>(hstat), p.FC, NKT, total, 1);
+    FM_CHECK_LAUNCH("k_hupdate(reduce)");
+    return FM_OK;
+  }
+  FM_EV(2);
+  if (phase == 1) {
+    k_hupdate<R><<<hblocks, 256, 0, st>>>(part, H, reinterpret_cast<R*>(hstat), p.FC, NKT, total, 2);
+  } else {
+    k_hupdate<R><<<hblocks, 256, 0, st>>>(part, H, nullptr, p.FC, NKT, total, 0);
+  }
+  FM_CHECK_LAUNCH("k_hupdate");
+  FM_EV(3);
+  if (int rc = lambda(d, W, H, lam, st)) return rc;
+  FM_EV(4);
+  if (int rc = spatial(d, s, /*tail_only=*/0, /*record=*/1, st)) return rc;
+  FM_EV(5);
+  return FM_OK;
+#undef FM_EV
+}
+
+// ---------------------------------------------------------------------------
+// per-op entry points
+// ---------------------------------------------------------------------------
+template <typename R>
+int Impl<R>::fast_stats(int64_t F, int64_t T, int64_t M, int64_t N, const void* xt,
+                        const void* g, const void* lam, double floor, int want_gain,
+                        int want_phi, void* phi1, void* phi2, void* gnum, void* gden,
+                        double* ll_host, cudaStream_t st) {
+  if (N > 8) { set_error("N=%lld outside 1..8", (long long)N); return FM_EINVAL; }
+  double* llp = nullptr;
+  FM_CUDA(cudaMallocAsync(&llp, sizeof(double) * std::max<int64_t>(F, 1), st));
+  int rc = FM_OK;
+  FM_DISPATCH_M(M, {
+    k_fast_stats<R, MM><<<(unsigned)F, 256, 0, st>>>(
+        reinterpret_cast<const R*>(xt), reinterpret_cast<const R*>(g),
+        reinterpret_cast<const R*>(lam), (R)floor, (int)N, (int)F, (int)T,
+        want_phi ? reinterpret_cast<R*>(phi1) : nullptr,
+        want_phi ? reinterpret_cast<R*>(phi2) : nullptr,
+        want_gain ? reinterpret_cast<R*>(gnum) : nullptr,
+        want_gain ? reinterpret_cast<R*>(gden) : nullptr, llp);
+  });
+  if (cudaGetLastError() != cudaSuccess) rc = FM_ECUDA;
+  std::vector<double> h((size_t)F);
+  if (rc == FM_OK && F > 0) {
+    FM_CUDA(cudaMemcpyAsync(h.data(), llp, sizeof(double) * F, cudaMemcpyDeviceToHost, st));
+  }
+  FM_CUDA(cudaFreeAsync(llp, st));
+  FM_CUDA(cudaStreamSynchronize(st));
+  if (rc != FM_OK) { set_error("k_fast_stats launch failed"); return rc; }
+  double s = 0.0;
+  for (int64_t f = 0; f < F; ++f) s += h[(size_t)f];
+  if (ll_host) *ll_host = s;
+  return FM_OK;
+}
+
+template <typename R>
+int Impl<R>::mix_power(int64_t N, int64_t F, int64_t T, int64_t M, const void* lam, const void* g,
+                       double floor, void* y, cudaStream_t st) {
+  const long long n = (long long)F * T;
+  if (n == 0) return FM_OK;
+  k_mix_power<R><<<(unsigned)((n + 255) / 256), 256, 0, st>>>(
+      reinterpret_cast<const R*>(lam), reinterpret_cast<const R*>(g), (R)floor, (int)N, (int)F,
+      (int)T, (int)M, reinterpret_cast<R*>(y));
+  FM_CHECK_LAUNCH("k_mix_power");
+  return FM_OK;
+}
+
+template <typename R>
+int Impl<R>::ip_weights(int64_t F, int64_t T, int64_t M, const void* X, const void* y, void* V,
+                        cudaStream_t st) {
+  if (F == 0) return FM_OK;
+  FM_DISPATCH_M(M, {
+    k_ip_weights<R, MM><<<(unsigned)F, 256, 0, st>>>(reinterpret_cast<const C*>(X),
+                                                      reinterpret_cast<const R*>(y), (int)T,
+                                                      reinterpret_cast<C*>(V));
+    FM_CHECK_LAUNCH("k_ip_weights");
+  });
+  return FM_OK;
+}
+
+template <typename R>
+int Impl<R>::project(int64_t F, int64_t T, int64_t M, const void* Q, const void* X, void* xt,
+                     cudaStream_t st) {
+  const long long n = (long long)F * T;
+  if (n == 0) return FM_OK;
+  FM_DISPATCH_M(M, {
+    k_project<R, MM><<<(unsigned)((n + 255) / 256), 256, 0, st>>>(
+        reinterpret_cast<const C*>(Q), reinterpret_cast<const C*>(X), (int)F, (int)T,
+        reinterpret_cast<R*>(xt));
+    FM_CHECK_LAUNCH("k_project");
+  });
+  return FM_OK;
+}
+
+template <typename R>
+int Impl<R>::update_diagonalizer(int64_t F, int64_t T, int64_t M, void* Q, const void* X,
+                                 const void* y, int sweeps, uint64_t* status, cudaStream_t st) {
+  if (F == 0) return FM_OK;
+  C* V = nullptr;
+  FM_CUDA(cudaMallocAsync(&V, sizeof(C) * F * M * M * M, st));
+  int rc = ip_weights(F, T, M, X, y, V, st);
+  if (rc == FM_OK) {
+    FM_DISPATCH_M(M, {
+      k_ipsolve<R, MM><<<(unsigned)F, 32, 0, st>>>(reinterpret_cast<C*>(Q), V, sweeps,
+                                                    reinterpret_cast<unsigned long long*>(status));
+      FM_CHECK_LAUNCH("k_ipsolve");
+    });
+  }
+  FM_CUDA(cudaFreeAsync(V, st));
+  return rc;
+}
+
+template <typename R>
+int Impl<R>::logdet(int64_t F, int64_t M, const void* Q, double* out, cudaStream_t st) {
+  if (F == 0) return FM_OK;
+  FM_DISPATCH_M(M, {
+    k_logdet<R, MM><<<(unsigned)F, 32, 0, st>>>(reinterpret_cast<const C*>(Q), out);
+    FM_CHECK_LAUNCH("k_logdet");
+  });
+  return FM_OK;
+}
+
+template <typename R>
+int Impl<R>::wiener(int64_t N, int64_t F, int64_t T, int64_t M, const void* lam, const void* Q,
+                    const void* g, const void* X, void* out, uint64_t* status, cudaStream_t st) {
+  if (N > 8) { set_error("N=%lld outside 1..8", (long long)N); return FM_EINVAL; }
+  if (F == 0) return FM_OK;
+  FM_DISPATCH_M(M, {
+    k_wiener<R, MM><<<(unsigned)F, 256, 0, st>>>(
+        reinterpret_cast<const R*>(lam), reinterpret_cast<const C*>(Q),
+        reinterpret_cast<const R*>(g), reinterpret_cast<const C*>(X), (int)N, (int)F, (int)T,
+        reinterpret_cast<C*>(out), reinterpret_cast<unsigned long long*>(status));
+    FM_CHECK_LAUNCH("k_wiener");
+  });
+  return FM_OK;
+}
+
+template <typename R>
+int Impl<R>::obs_stats(const fm_dims* d, const void* X, double* sumsq, double* maxsq,
+                       cudaStream_t st) {
+  const long long per_b = d->F * d->T * d->M;
+  const unsigned nblk = (unsigned)std::max<long long>(1, std::min<long long>(256, (per_b + 4095) / 4096));
+  double* buf = nullptr;
+  FM_CUDA(cudaMallocAsync(&buf, sizeof(double) * 2 * nblk * d->B, st));
+  k_obs_stats<R><<<dim3(nblk, (unsigned)d->B), 256, 0, st>>>(reinterpret_cast<const C*>(X), per_b,
+                                                             buf, buf + (size_t)nblk * d->B);
+  FM_CHECK_LAUNCH("k_obs_stats");
+  std::vector<double> h((size_t)2 * nblk * d->B);
+  FM_CUDA(cudaMemcpyAsync(h.data(), buf, sizeof(double) * h.size(), cudaMemcpyDeviceToHost, st));
+  FM_CUDA(cudaFreeAsync(buf, st));
+  FM_CUDA(cudaStreamSynchronize(st));
+  for (long long b = 0; b < d->B; ++b) {
+    double s = 0.0, m = 0.0;
+    for (unsigned i = 0; i < nblk; ++i) {
+      s += h[(size_t)b * nblk + i];
+      m = std::max(m, h[(size_t)nblk * d->B + (size_t)b * nblk + i]);
+    }
+    if (sumsq) sumsq[b] = s;
+    if (maxsq) maxsq[b] = m;
+  }
+  return FM_OK;
+}
+
+template <typename R>
+int Impl<R>::scale(const fm_dims* d, void* X, const double* scale_host, cudaStream_t st) {
+  const long long per_b = d->F * d->T * d->M;
+  double* sc = nullptr;
+  FM_CUDA(cudaMallocAsync(&sc, sizeof(double) * d->B, st));
+  FM_CUDA(cudaMemcpyAsync(sc, scale_host, sizeof(double) * d->B, cudaMemcpyHostToDevice, st));
+  const long long n = per_b * d->B;
+  k_scale<R><<<(unsigned)((n + 255) / 256), 256, 0, st>>>(reinterpret_cast<C*>(X), per_b, sc, (int)d->B);
+  FM_CHECK_LAUNCH("k_scale");
+  FM_CUDA(cudaFreeAsync(sc, st));
+  FM_CUDA(cudaStreamSynchronize(st));
+  return FM_OK;
+}
+
+}  // namespace fm

@@ -1,0 +1,150 @@
+// fm_linalg.cuh -- warp-level M x M complex dense linear algebra in fp64.
+//
+// The reference solves the IP row system with numpy.linalg.solve (LAPACK zgesv:
+// partial-pivot LU, zgetrf, then zgetrs) at spatial.py:188, takes log|det Q|
+// with numpy.linalg.slogdet (zgetrf, separate.py:238 / spatial.py:241) and
+// inverts Q with numpy.linalg.inv (zgesv against I, separate.py:122). These
+// routines restate that arithmetic for one M x M system per warp (M <= 16),
+// matrices in shared memory, fp64 in both precision modes.
+#pragma once
+#include "fm_common.cuh"
+
+namespace fm {
+
+#define FM_FULL 0xffffffffu
+
+// Partial-pivot LU of the M x M block of A (row stride LD) by one warp, with
+// the same row operations applied to columns [M, ncol) (right-hand sides).
+// Pivot = first index of max |re|+|im| (izamax in zgetf2); multipliers are
+// a * (1/pivot) (zgetf2's reciprocal scaling); the RHS update order is the
+// column-oriented one of ztrsm('L','L','N','U'). Returns false on an exactly
+// zero pivot (zgetrf info > 0 -> numpy LinAlgError "Singular matrix").
+// If logabs != nullptr, *logabs (lane 0) = sum_k log|u_kk| (slogdet).
+template <int M>
+__device__ bool warp_lu(double2* A, int LD, int ncol, int lane, double* logabs) {
+  double la = 0.0;
+  for (int k = 0; k < M; ++k) {
+    double v = -1.0;
+    int idx = lane;
+    if (lane >= k && lane < M) v = cabs1(A[lane * LD + k]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      double ov = __shfl_xor_sync(FM_FULL, v, o);
+      int oi = __shfl_xor_sync(FM_FULL, idx, o);
+      if (ov > v || (ov == v && oi < idx)) {
+        v = ov;
+        idx = oi;
+      }
+    }
+    if (!(v > 0.0)) {  // zero (or NaN) pivot column
+      if (logabs) *logabs = -INFINITY;
+      return false;
+    }
+    if (idx != k) {
+      for (int c = lane; c < ncol; c += 32) {
+        double2 t = A[k * LD + c];
+        A[k * LD + c] = A[idx * LD + c];
+        A[idx * LD + c] = t;
+      }
+    }
+    __syncwarp();
+    const double2 piv = A[k * LD + k];
+    la += log(hypot(piv.x, piv.y));
+    const double2 rp = cdiv(make_double2(1.0, 0.0), piv);
+    if (lane > k && lane < M) {
+      const double2 l = cmul(A[lane * LD + k], rp);
+      A[lane * LD + k] = l;
+      for (int c = k + 1; c < ncol; ++c) A[lane * LD + c] = csub(A[lane * LD + c], cmul(l, A[k * LD + c]));
+    }
+    __syncwarp();
+  }
+  if (logabs) *logabs = la;
+  return true;
+}
+
+// Back substitution U x = b for the single right-hand side in column M
+// (ztrsm('L','U','N','N') order); x written to smem x[0..M).
+template <int M>
+__device__ void warp_backsub1(const double2* A, int LD, int lane, double2* x) {
+  double2 b = make_double2(0.0, 0.0);
+  if (lane < M) b = A[lane * LD + M];
+  for (int k = M - 1; k >= 0; --k) {
+    double2 xk = make_double2(0.0, 0.0);
+    if (lane == k) xk = cdiv(b, A[k * LD + k]);
+    xk.x = __shfl_sync(FM_FULL, xk.x, k);
+    xk.y = __shfl_sync(FM_FULL, xk.y, k);
+    if (lane < k) b = csub(b, cmul(xk, A[lane * LD + k]));
+    if (lane == k) x[k] = xk;
+  }
+  __syncwarp();
+}
+
+// Back substitution for the M right-hand sides in columns [M, 2M): lane j
+// solves column j sequentially. Result overwrites those columns.
+template <int M>
+__device__ void warp_backsubM(double2* A, int LD, int lane) {
+  if (lane < M) {
+    const int c = M + lane;
+    for (int k = M - 1; k >= 0; --k) {
+      double2 xk = cdiv(A[k * LD + c], A[k * LD + k]);
+      A[k * LD + c] = xk;
+      for (int i = 0; i < k; ++i) A[i * LD + c] = csub(A[i * LD + c], cmul(xk, A[i * LD + k]));
+    }
+  }
+  __syncwarp();
+}
+
+// One IP sweep set (spatial.py:181-199) for one frequency bin, by one warp.
+// Qd: M x M (row m = q_m^H), fp64, updated in place row by row (Gauss-Seidel:
+// row m's system uses rows < m already updated, spatial.py:183-188).
+// V: M x M x M weighted covariances (any complex type), V[(m*M+i)*M+j].
+// A: scratch M x (M+1); x: scratch M. Returns 0 or an FM_STATUS code and the
+// failing row in *bad_m.
+template <int M, typename CV>
+__device__ int warp_ip_update(double2* Qd, const CV* V, double2* A, double2* x, int sweeps,
+                              int lane, int* bad_m) {
+  constexpr int LD = M + 1;
+  for (int sw = 0; sw < sweeps; ++sw) {
+    for (int m = 0; m < M; ++m) {
+      const CV* Vm = V + (size_t)m * M * M;
+      // A = Q_f V_fm ; rhs = e_m  (spatial.py:184-188)
+      for (int e = lane; e < M * M; e += 32) {
+        const int r = e / M, c = e % M;
+        double2 s = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int k = 0; k < M; ++k) s = cadd(s, cmul(Qd[r * M + k], to_d2(Vm[k * M + c])));
+        A[r * LD + c] = s;
+      }
+      if (lane < M) A[lane * LD + M] = make_double2(lane == m ? 1.0 : 0.0, 0.0);
+      __syncwarp();
+      if (!warp_lu<M>(A, LD, M + 1, lane, nullptr)) {
+        *bad_m = m;
+        return 2;  // FM_STATUS_SINGULAR_QV
+      }
+      warp_backsub1<M>(A, LD, lane, x);
+      // norm = Re(q^H V q)  (spatial.py:193)
+      double part = 0.0;
+      if (lane < M) {
+        double2 s = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int j = 0; j < M; ++j) s = cadd(s, cmul(to_d2(Vm[lane * M + j]), x[j]));
+        const double2 xi = x[lane];
+        part = xi.x * s.x + xi.y * s.y;  // Re(conj(x_i) s_i)
+      }
+      const double norm = warp_sum(part);
+      if (!(norm > 0.0) || !isfinite(norm)) {  // spatial.py:194-198
+        *bad_m = m;
+        return 1;  // FM_STATUS_NONPOS_NORM
+      }
+      const double sn = sqrt(norm);
+      if (lane < M) {  // Q[m, :] = conj(q / sqrt(norm))  (spatial.py:199)
+        const double2 xv = x[lane];
+        Qd[m * M + lane] = make_double2(xv.x / sn, -(xv.y / sn));
+      }
+      __syncwarp();
+    }
+  }
+  return 0;
+}
+
+}  // namespace fm

@@ -1,0 +1,431 @@
+"""FastMNMF separator API on B200 -- drop-in for ``fastsep.separate``
+(``pkg/src/fastsep/separate.py``) on its hot path (``method="fast-mnmf"``).
+
+The parameter layout, config fields, result type, trace semantics and error
+behaviour follow the reference; the iteration itself runs as five sm_100a
+kernel launches per pass over device-resident state (libfastmnmf.so,
+``fm_iterate``), optionally replayed from one captured CUDA graph.
+"""
+
+import ctypes
+import time
+from dataclasses import dataclass, field, replace
+
+import numpy as np
+
+from . import _lib
+from . import kernels as K
+from .errors import InvalidInputError, NumericalBreakdownError, SingularMatrixError
+
+METHODS = ("fca", "mnmf", "mnmf-dp", "fast-fca", "fast-mnmf", "fast-mnmf-dp")  # separate.py:39
+FAST_METHODS = ("fast-fca", "fast-mnmf", "fast-mnmf-dp")
+DP_METHODS = ("mnmf-dp", "fast-mnmf-dp")
+SUPPORTED_METHODS = ("fast-mnmf",)  # the hot path this backend provides
+PRECISIONS = ("complex128", "complex64")
+
+
+@dataclass
+class MetropolisConfig:
+    """Kept for config compatibility (sources.py:38-49); unused by fast-mnmf."""
+
+    proposal_var: float = 1e-4
+    inner_steps: int = 30
+
+    def __post_init__(self):
+        if self.proposal_var <= 0:
+            raise InvalidInputError("proposal_var must be positive")
+        if self.inner_steps < 1:
+            raise InvalidInputError("inner_steps must be >= 1")
+
+
+@dataclass
+class SeparatorConfig:
+    """separate.py:44-71, plus the B200 execution fields ``precision``,
+    ``use_graph`` and ``device``."""
+
+    method: str = "fast-mnmf"
+    n_sources: int = 2
+    n_basis: int = 16
+    n_iterations: int = 100
+    seed: int = 0
+    spatial_init: str = "auto"  # auto | circular | observed
+    normalize: bool = True
+    ip_sweeps: int = 1
+    metropolis: MetropolisConfig = field(default_factory=MetropolisConfig)
+    metropolis_enabled: bool = True
+    decoder: object = None
+    record_likelihood: bool = True
+    precision: str = "complex128"
+    use_graph: bool = True
+    device: str = "cuda"
+
+    def validate(self):  # separate.py:59-71
+        if self.method not in METHODS:
+            raise InvalidInputError(f"unknown method {self.method!r}")
+        if self.n_sources < 1:
+            raise InvalidInputError("n_sources must be >= 1")
+        if self.method in DP_METHODS and self.n_sources < 2:
+            raise InvalidInputError("deep-prior methods need n_sources >= 2")
+        if self.n_iterations < 1:
+            raise InvalidInputError("n_iterations must be >= 1")
+        if self.n_basis < 1:
+            raise InvalidInputError("n_basis must be >= 1")
+        if self.spatial_init not in ("auto", "circular", "observed"):
+            raise InvalidInputError(f"unknown spatial_init {self.spatial_init!r}")
+        if self.precision not in PRECISIONS:
+            raise InvalidInputError(f"unknown precision {self.precision!r}")
+        if self.ip_sweeps < 1:
+            raise InvalidInputError("ip_sweeps must be >= 1")
+
+
+@dataclass
+class SeparationResult:  # separate.py:74-80
+    images_NFTM: np.ndarray
+    likelihood_trace: np.ndarray
+    time_trace: np.ndarray
+    method: str
+    config: SeparatorConfig
+
+
+def _torch():
+    import torch
+
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_1903_03237_b200 needs a CUDA device (no CPU fallback)")
+    return torch
+
+
+def wiener_fast(lam_NFT, Q_FMM, g_NFM, X_FTM):
+    """Diagonalized-domain Wiener filter (separate.py:110-125) on the device."""
+    return K.wiener_fast(lam_NFT, Q_FMM, g_NFM, X_FTM)
+
+
+# ---------------------------------------------------------------------------
+# device-resident loop state
+# ---------------------------------------------------------------------------
+
+class _SpatialView:
+    """``loop.spatial`` surface (DiagSpatial, spatial.py:47-56): host copies."""
+
+    def __init__(self, loop, b):
+        self._loop, self._b = loop, b
+
+    @property
+    def Q_FMM(self):
+        return self._loop.Q[self._b].cpu().numpy().astype(np.complex128)
+
+    @property
+    def g_NFM(self):
+        return self._loop.g[self._b].cpu().numpy().astype(np.float64)
+
+    @property
+    def n_sources(self):
+        return self._loop.N
+
+
+class _SourceView:
+    """``loop.source`` surface (NmfSource, sources.py:167-204): host copies."""
+
+    mu_steps = ("W", "H")
+
+    def __init__(self, loop, b):
+        self._loop, self._b = loop, b
+
+    @property
+    def W_NFK(self):
+        return self._loop.W[self._b].cpu().numpy().astype(np.float64)
+
+    @property
+    def H_NKT(self):
+        return self._loop.H[self._b].cpu().numpy().astype(np.float64)
+
+    def lam(self):
+        return self._loop.lam_device()[self._b].cpu().numpy().astype(np.float64)
+
+
+class DeviceLoop:
+    """The _DiagLoop (separate.py:175-243) over a batch of B mixtures held in
+    HBM. ``X`` is the SCALED observation (B,F,T,M) on the device.
+
+    Frequency sharding: ``f_offset`` is the global index of local bin 0 and
+    ``hstat_allreduce`` (a callable on the packed (B,2,N,K,T) H statistics)
+    is invoked between the two phases of every iteration.
+    """
+
+    def __init__(self, X, Q, g, W, H, floor, normalize=True, ip_sweeps=1, n_trace=1,
+                 f_offset=0, hstat_allreduce=None):
+        torch = _torch()
+        self.torch = torch
+        self.X = X
+        self.real = torch.float32 if X.dtype == torch.complex64 else torch.float64
+        self.B, self.F, self.T, self.M = X.shape
+        self.N, self.K = W.shape[1], W.shape[3]
+        dev = X.device
+        self.Q = Q.to(dev, X.dtype).resolve_conj().contiguous()
+        self.g = g.to(dev, self.real).contiguous()
+        self.W = W.to(dev, self.real).contiguous()
+        self.H = H.to(dev, self.real).contiguous()
+        self.floor = floor.to(dev, self.real).contiguous()
+        self.xt = torch.empty((self.B, self.F, self.T, self.M), device=dev, dtype=self.real)
+        self.n_trace = max(1, int(n_trace))
+        self.trace = torch.zeros((self.n_trace, self.B), device=dev, dtype=torch.float64)
+        self.status = torch.full((1,), -1, dtype=torch.int64, device=dev)
+        self.dims = _lib.FmDims(self.B, self.F, self.T, self.M, self.N, self.K, int(f_offset),
+                                _lib.FM_F32 if self.real == torch.float32 else _lib.FM_F64,
+                                int(bool(normalize)), int(ip_sweeps), 0)
+        lib = _lib.load()
+        nbytes = lib.fm_workspace_bytes(ctypes.byref(self.dims))
+        if nbytes == 0:
+            raise InvalidInputError(f"unsupported problem: {lib.fm_last_error().decode()}")
+        self.work = torch.empty((nbytes,), dtype=torch.uint8, device=dev)
+        self.state = _lib.FmState(*[_lib.ptr(t).value for t in (
+            self.X, self.xt, self.Q, self.g, self.W, self.H, self.floor, self.trace,
+            self.status, self.work)])
+        self.hstat_allreduce = hstat_allreduce
+        self.hstat = (torch.empty((self.B, 2, self.N, self.K, self.T), device=dev, dtype=self.real)
+                      if hstat_allreduce is not None else None)
+        self.iterations_done = 0
+        self.spatial = _SpatialView(self, 0)
+        self.source = _SourceView(self, 0)
+
+    # reference-facing attributes of _DiagLoop
+    @property
+    def xt_FTM(self):
+        return self.xt[0]
+
+    def lam_device(self):
+        """lambda = W H of the current state (sources.py:184-187), (B,N,F,T)."""
+        torch = self.torch
+        lam = torch.empty((self.B, self.N, self.F, self.T), device=self.X.device, dtype=self.real)
+        lib = _lib.load()
+        _lib.check(lib.fm_nmf_lambda(ctypes.byref(self.dims), _lib.ptr(self.W), _lib.ptr(self.H),
+                                     _lib.ptr(lam), _lib.stream_ptr()), "fm_nmf_lambda")
+        return lam
+
+    def prologue(self):
+        lib = _lib.load()
+        _lib.check(lib.fm_prologue(ctypes.byref(self.dims), ctypes.byref(self.state),
+                                   _lib.stream_ptr()), "fm_prologue")
+
+    def run(self, n, use_graph=False):
+        lib = _lib.load()
+        if self.iterations_done + n > self.n_trace:
+            raise InvalidInputError("trace buffer too small for the requested iterations")
+        if self.hstat_allreduce is None:
+            _lib.check(lib.fm_run(ctypes.byref(self.dims), ctypes.byref(self.state), int(n),
+                                  int(bool(use_graph)), _lib.stream_ptr()), "fm_run")
+        else:
+            for _ in range(n):
+                _lib.check(lib.fm_iterate_phase(ctypes.byref(self.dims), ctypes.byref(self.state),
+                                                0, _lib.ptr(self.hstat), _lib.stream_ptr()),
+                           "fm_iterate_phase(0)")
+                self.hstat_allreduce(self.hstat)
+                _lib.check(lib.fm_iterate_phase(ctypes.byref(self.dims), ctypes.byref(self.state),
+                                                1, _lib.ptr(self.hstat), _lib.stream_ptr()),
+                           "fm_iterate_phase(1)")
+        self.iterations_done += n
+
+    def status_error(self):
+        """The first numerical failure as the reference's exception, or None."""
+        s = K.decode_status(self.status.item())
+        if s is None:
+            return None
+        code, it, m, f = s
+        return SingularMatrixError(f"iteration {it}: {K.status_message(code, m, f)}")
+
+    def images(self, scale):
+        """separate.py:240-243 + the scale-back of :323, per mixture."""
+        lam = self.lam_device()
+        out = []
+        for b in range(self.B):
+            img = K.wiener_fast(lam[b], self.Q[b], self.g[b], self.X[b])
+            out.append(img * float(scale[b]))
+        return out
+
+
+# ---------------------------------------------------------------------------
+# initialisation (separate.py:246-264)
+# ---------------------------------------------------------------------------
+
+def default_init(cfg, Xs, rng):
+    """Reference default init: circular spatial init (spatial.py:109-121) and
+    NmfSource.random (sources.py:177-182) drawn from the run's rng.
+
+    The spatial part (time-averaged SCM, PSD clamp and descending Hermitian
+    eigendecomposition, linalg.py:23-33, 85-94) runs on the device through
+    torch.linalg.eigh (cuSOLVER); see DESIGN.md §8(f) for the planned native
+    batched-Jacobi kernel.
+    """
+    torch = _torch()
+    F, T, M = Xs.shape
+    N = cfg.n_sources
+    Xd = Xs.to(torch.complex128)
+    init = cfg.spatial_init
+    if init == "auto":
+        init = "observed" if cfg.method in DP_METHODS else "circular"
+    G1 = torch.einsum("fti,ftj->fij", Xd, Xd.conj()) / T  # spatial.py:93
+    G1 = 0.5 * (G1 + G1.conj().transpose(-1, -2))  # clamp_psd (linalg.py:85-94)
+    w, v = torch.linalg.eigh(G1)
+    w = torch.maximum(w, 1e-12 * torch.clamp(w.max(dim=-1, keepdim=True).values, min=0.0))
+    G1 = (v * w[..., None, :].to(v.dtype)) @ v.conj().transpose(-1, -2)
+    w, U = torch.linalg.eigh(G1)  # hermitian_eig: descending (linalg.py:23-33)
+    w, U = w.flip(-1), U.flip(-1)
+    Q = U.conj_physical().transpose(-1, -2).contiguous()
+    if init == "circular":  # spatial.py:109-121
+        g = torch.full((N, F, M), 1e-2, dtype=torch.float64, device=Xd.device)
+        for m in range(M):
+            g[m % N, :, m] = 1.0
+    else:  # "observed": init_spatial diagonalizable (spatial.py:100-105)
+        g = torch.ones((N, F, M), dtype=torch.float64, device=Xd.device)
+        g[0] = torch.maximum(w, w.max(dim=-1, keepdim=True).values * 1e-12)
+    Wn = rng.uniform(0.1, 1.1, (N, F, cfg.n_basis))  # sources.py:180-181
+    Hn = rng.uniform(0.1, 1.1, (N, cfg.n_basis, T))
+    return Q, g, torch.from_numpy(Wn), torch.from_numpy(Hn)
+
+
+# ---------------------------------------------------------------------------
+# run
+# ---------------------------------------------------------------------------
+
+def _check_method(cfg):
+    if cfg.method not in SUPPORTED_METHODS:
+        raise InvalidInputError(
+            f"method {cfg.method!r} is outside this backend's hot path; "
+            f"supported: {SUPPORTED_METHODS}")
+
+
+def _prepare_observation(X, cfg, torch):
+    """separate.py:284-293 + spatial.py:64-66 on the device: returns
+    (Xs device (B,F,T,M), scale (B,) np, floor (B,) tensor)."""
+    cdt = torch.complex64 if cfg.precision == "complex64" else torch.complex128
+    if isinstance(X, torch.Tensor):
+        Xd = X.to(device=cfg.device, dtype=cdt).contiguous()
+    else:
+        Xn = np.asarray(X)
+        if not np.all(np.isfinite(Xn)):
+            raise InvalidInputError("observation contains non-finite values")
+        Xd = torch.from_numpy(np.ascontiguousarray(Xn.astype(np.complex128))).to(cfg.device, cdt)
+    if Xd.dim() == 3:
+        Xd = Xd.unsqueeze(0)
+    B, F, T, M = Xd.shape
+    dims = _lib.FmDims(B, F, T, M, 1, 1, 0,
+                       _lib.FM_F32 if cdt == torch.complex64 else _lib.FM_F64, 1, 1, 0)
+    lib = _lib.load()
+    sumsq = (ctypes.c_double * B)()
+    maxsq = (ctypes.c_double * B)()
+    _lib.check(lib.fm_observation_stats(ctypes.byref(dims), _lib.ptr(Xd), sumsq, maxsq,
+                                        _lib.stream_ptr()), "fm_observation_stats")
+    power = np.array(sumsq[:]) / float(F * T * M)
+    if not np.all(np.isfinite(power)):
+        raise InvalidInputError("observation contains non-finite values")
+    if np.any(power == 0.0):
+        raise InvalidInputError("observation is identically zero")
+    scale = np.sqrt(power)
+    sc = (ctypes.c_double * B)(*scale.tolist())
+    _lib.check(lib.fm_scale_observation(ctypes.byref(dims), _lib.ptr(Xd), sc, _lib.stream_ptr()),
+               "fm_scale_observation")
+    _lib.check(lib.fm_observation_stats(ctypes.byref(dims), _lib.ptr(Xd), sumsq, maxsq,
+                                        _lib.stream_ptr()), "fm_observation_stats")
+    floor = torch.tensor([1e-12 * v for v in maxsq[:]], dtype=torch.float64)  # spatial.py:64-66
+    return Xd, scale, floor.to(cfg.device)
+
+
+def _as_batch(a, torch, B):
+    t = a if isinstance(a, torch.Tensor) else torch.from_numpy(np.asarray(a))
+    if t.dim() == 3:
+        t = t.unsqueeze(0).expand(B, *t.shape)
+    return t
+
+
+def run(cfg: SeparatorConfig, X_FTM, on_iteration=None, init=None) -> SeparationResult:
+    """fastsep.run (separate.py:276-330) for method="fast-mnmf".
+
+    ``init`` optionally injects the initial (Q_FMM, g_NFM, W_NFK, H_NKT) in
+    the scaled domain -- where the reference's _build_spatial/_build_source
+    place theirs; by default the reference's own init is used.
+    """
+    cfg.validate()
+    _check_method(cfg)
+    torch = _torch()
+    if not isinstance(X_FTM, torch.Tensor):
+        Xn = np.asarray(X_FTM)
+        if Xn.ndim != 3:
+            raise InvalidInputError(f"observation must have shape (F, T, M), got {Xn.shape}")
+    elif X_FTM.dim() != 3:
+        raise InvalidInputError(f"observation must have shape (F, T, M), got {tuple(X_FTM.shape)}")
+    Xs, scale, floor = _prepare_observation(X_FTM, cfg, torch)
+    rng = np.random.default_rng(cfg.seed)  # separate.py:295
+    if init is None:
+        Q0, g0, W0, H0 = default_init(cfg, Xs[0], rng)
+    else:
+        Q0, g0, W0, H0 = init
+    loop = DeviceLoop(Xs, _as_batch(Q0, torch, 1), _as_batch(g0, torch, 1),
+                      _as_batch(W0, torch, 1), _as_batch(H0, torch, 1), floor,
+                      cfg.normalize, cfg.ip_sweeps, n_trace=cfg.n_iterations)
+    loop.X_FTM = Xs[0]
+    loop.floor_value = float(floor[0])
+    loop.prologue()
+    time_trace = []
+    start = torch.cuda.Event(enable_timing=True)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(cfg.n_iterations)]
+    start.record()
+    for it in range(cfg.n_iterations):
+        loop.run(1, use_graph=cfg.use_graph)
+        ev[it].record()
+        if on_iteration is not None:
+            torch.cuda.synchronize()
+            err = loop.status_error()
+            if err is not None:
+                raise err
+            on_iteration(it, loop)
+    torch.cuda.synchronize()
+    err = loop.status_error()
+    if err is not None:
+        raise err
+    prev = start
+    for e in ev:  # per-iteration device time (separate.py:307-312 analogue)
+        time_trace.append(prev.elapsed_time(e) / 1e3)
+        prev = e
+    ll = loop.trace[:, 0].cpu().numpy().copy() if cfg.record_likelihood else np.zeros(0)
+    images = loop.images(scale)[0].cpu().numpy().astype(np.complex128)
+    res = SeparationResult(images_NFTM=images, likelihood_trace=np.asarray(ll),
+                           time_trace=np.asarray(time_trace), method=cfg.method,
+                           config=replace(cfg))
+    res.loop = loop
+    return res
+
+
+@dataclass
+class BatchSeparationResult:
+    """run_batch output: per-mixture results of B independent runs."""
+
+    images_BNFTM: object
+    likelihood_trace: np.ndarray  # (B, n_iterations)
+    seconds: float
+    config: SeparatorConfig
+    loop: object = None
+
+
+def run_batch(cfg: SeparatorConfig, X_BFTM, init, want_images=True) -> BatchSeparationResult:
+    """B independent fast-mnmf runs in lock-step on one device (BASELINE
+    config 2); equal to B separate ``run`` calls."""
+    cfg.validate()
+    _check_method(cfg)
+    torch = _torch()
+    Xs, scale, floor = _prepare_observation(X_BFTM, cfg, torch)
+    Q0, g0, W0, H0 = init
+    B = Xs.shape[0]
+    loop = DeviceLoop(Xs, _as_batch(Q0, torch, B), _as_batch(g0, torch, B),
+                      _as_batch(W0, torch, B), _as_batch(H0, torch, B), floor,
+                      cfg.normalize, cfg.ip_sweeps, n_trace=cfg.n_iterations)
+    loop.prologue()
+    t0 = time.perf_counter()
+    loop.run(cfg.n_iterations, use_graph=cfg.use_graph)
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    err = loop.status_error()
+    if err is not None:
+        raise err
+    imgs = torch.stack(loop.images(scale)) if want_images else None
+    return BatchSeparationResult(images_BNFTM=imgs, likelihood_trace=loop.trace.cpu().numpy().T,
+                                 seconds=dt, config=replace(cfg), loop=loop)
