@@ -136,15 +136,15 @@ int fm_iterate_phase(const fm_dims* d, const fm_state* s, int phase, void* hstat
 int fm_iterate_profiled(const fm_dims* d, const fm_state* s, float* ms_host, void* stream) {
   if (int rc = validate_dims(d)) return rc;
   cudaStream_t st = (cudaStream_t)stream;
-  cudaEvent_t ev[6];
-  for (int i = 0; i < 6; ++i) FM_CUDA(cudaEventCreate(&ev[i]));
+  cudaEvent_t ev[8];
+  for (int i = 0; i < 8; ++i) FM_CUDA(cudaEventCreate(&ev[i]));
   int rc = d->dtype == FM_F64 ? Impl<double>::iterate_phase(d, s, 2, nullptr, st, ev)
                               : Impl<float>::iterate_phase(d, s, 2, nullptr, st, ev);
   if (rc == FM_OK) {
-    FM_CUDA(cudaEventSynchronize(ev[5]));
-    for (int i = 0; i < 5; ++i) FM_CUDA(cudaEventElapsedTime(&ms_host[i], ev[i], ev[i + 1]));
+    FM_CUDA(cudaEventSynchronize(ev[7]));
+    for (int i = 0; i < 7; ++i) FM_CUDA(cudaEventElapsedTime(&ms_host[i], ev[i], ev[i + 1]));
   }
-  for (int i = 0; i < 6; ++i) cudaEventDestroy(ev[i]);
+  for (int i = 0; i < 8; ++i) cudaEventDestroy(ev[i]);
   return rc;
 }
 

@@ -7,6 +7,8 @@
 
 namespace fm {
 
+constexpr int NMAX = 8;  // sources per mixture supported by the fused kernels
+
 // Real type traits: storage/arithmetic type R, its complex pair C, TINY
 // (np.finfo(float).tiny in the reference, sources.py:24; FLT_MIN in the
 // complex64 mode, SURVEY §8(a) exact-numerics checklist).
@@ -62,6 +64,9 @@ template <> __device__ __forceinline__ double rsqrt_r<double>(double x) { return
 __device__ __forceinline__ float log_r(float x) { return logf(x); }
 __device__ __forceinline__ double log_r(double x) { return log(x); }
 __device__ __forceinline__ float sqrt_r(float x) { return sqrtf(x); }
+// log for the likelihood data term only (reported, never fed back): MUFU-based in fp32
+__device__ __forceinline__ float log_fast(float x) { return __logf(x); }
+__device__ __forceinline__ double log_fast(double x) { return log(x); }
 __device__ __forceinline__ double sqrt_r(double x) { return sqrt(x); }
 
 // Multiplicative-update factor sqrt(num / max(den, TINY))  (sources.py:194, :198;

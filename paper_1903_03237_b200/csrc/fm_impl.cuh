@@ -70,35 +70,32 @@ inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 // Workspace plan for the fused iteration.
 struct Plan {
-  int G, TT, ntt, FC, FCH;
-  size_t off_lam, off_phi, off_part, off_llp, off_ldp, off_cnt, total;
-  size_t hstats_smem;
+  int TS, FS, nft, ntt;  // split counts of k_wstats / k_hstats, their tile counts
+  size_t off_lam, off_phi, off_part, off_llp, off_ldp, off_cs, off_cnt, off_tiles, total;
 };
 
 inline Plan make_plan(const fm_dims* d) {
   Plan p;
   const size_t rs = d->dtype == FM_F64 ? 8 : 4;
-  const long long B = d->B, F = d->F, T = d->T, M = d->M, N = d->N, K = d->K;
-  p.G = std::max<long long>(1, 8 / N);
-  p.TT = 32 * p.G;
-  p.ntt = (int)((T + p.TT - 1) / p.TT);
-  long long fc = (2 * 296 + B * p.ntt - 1) / (B * p.ntt);  // ~4 resident CTAs per SM
-  fc = std::max<long long>(1, std::min<long long>(fc, (F + 3) / 4));
-  long long fch = (F + fc - 1) / fc;
-  // shared-memory cap for the staged W/g rows (~96 KB)
-  const long long per_f = (N * K + N * M) * (long long)rs;
-  const long long fch_cap = std::max<long long>(1, (96 * 1024 - 2 * p.G * N * 32 * (long long)rs) / per_f);
-  fch = std::min(fch, fch_cap);
-  p.FCH = (int)fch;
-  p.FC = (int)((F + fch - 1) / fch);
-  p.hstats_smem = (size_t)(fch * per_f + 2 * p.G * N * 32 * rs);
+  const long long B = d->B, F = d->F, T = d->T, N = d->N, K = d->K;
+  const long long target = 2 * 148;  // >= 2 CTAs per SM
+  p.nft = (int)((F + 31) / 32);
+  p.ntt = (int)((T + 63) / 64);
+  long long ts = (target + B * N * p.nft - 1) / (B * N * p.nft);
+  p.TS = (int)std::max<long long>(1, std::min<long long>(ts, (T + 63) / 64));
+  long long fs = (target + B * N * p.ntt - 1) / (B * N * p.ntt);
+  p.FS = (int)std::max<long long>(1, std::min<long long>(fs, (F + 31) / 32));
+  const size_t partw = (size_t)B * N * p.TS * 2 * F * K;
+  const size_t parth = (size_t)B * N * p.FS * 2 * K * T;
   size_t o = 0;
   p.off_lam = o; o = align256(o + (size_t)B * N * F * T * rs);
   p.off_phi = o; o = align256(o + (size_t)B * 2 * N * F * T * rs);
-  p.off_part = o; o = align256(o + (size_t)B * p.FC * 2 * N * K * T * rs);
+  p.off_part = o; o = align256(o + std::max(partw, parth) * rs);
   p.off_llp = o; o = align256(o + (size_t)B * F * 8);
   p.off_ldp = o; o = align256(o + (size_t)B * F * 8);
+  p.off_cs = o; o = align256(o + (size_t)B * F * NMAX * rs);
   p.off_cnt = o; o = align256(o + 64);
+  p.off_tiles = o; o = align256(o + sizeof(unsigned) * (size_t)B * N * (p.nft + p.ntt));
   p.total = o;
   return p;
 }
@@ -110,10 +107,10 @@ template <typename R> struct Impl {
 
   static int prologue(const fm_dims* d, const fm_state* s, cudaStream_t st);
   static int iterate_phase(const fm_dims* d, const fm_state* s, int phase, void* hstat,
-                           cudaStream_t st, cudaEvent_t* ev = nullptr);
+                           cudaStream_t st, cudaEvent_t* ev = nullptr);  // ev: 8 events
   static int lambda(const fm_dims* d, const R* W, const R* H, R* lam, cudaStream_t st);
-  static int spatial(const fm_dims* d, const fm_state* s, int tail_only, int record,
-                     cudaStream_t st);
+  static int front(const fm_dims* d, const fm_state* s, cudaStream_t st);
+  static int back(const fm_dims* d, const fm_state* s, int tail_only, int record, cudaStream_t st);
 
   static int fast_stats(int64_t F, int64_t T, int64_t M, int64_t N, const void* xt,
                         const void* g, const void* lam, double floor, int want_gain,
@@ -156,38 +153,60 @@ int Impl<R>::lambda(const fm_dims* d, const R* W, const R* H, R* lam, cudaStream
 }
 
 template <typename R>
-int Impl<R>::spatial(const fm_dims* d, const fm_state* s, int tail_only, int record,
-                     cudaStream_t st) {
+int Impl<R>::front(const fm_dims* d, const fm_state* s, cudaStream_t st) {
   const Plan p = make_plan(d);
   unsigned char* w = reinterpret_cast<unsigned char*>(s->work);
-  SpArgs<R> a;
+  FrontArgs<R> a;
   a.X = reinterpret_cast<const C*>(s->X);
-  a.xt = reinterpret_cast<R*>(s->xt);
+  a.xt = reinterpret_cast<const R*>(s->xt);
   a.Q = reinterpret_cast<C*>(s->Q);
   a.g = reinterpret_cast<R*>(s->g);
   a.W = reinterpret_cast<R*>(s->W);
   a.lam = reinterpret_cast<const R*>(w + p.off_lam);
-  a.phi = reinterpret_cast<R*>(w + p.off_phi);
   a.floorp = reinterpret_cast<const R*>(s->floor);
-  a.ll_part = reinterpret_cast<double*>(w + p.off_llp);
+  a.cs_out = reinterpret_cast<R*>(w + p.off_cs);
   a.ld_part = reinterpret_cast<double*>(w + p.off_ldp);
-  a.trace = s->trace;
-  a.counter = reinterpret_cast<unsigned*>(w + p.off_cnt);
-  a.iter = a.counter + 1;
+  a.iter = reinterpret_cast<const unsigned*>(w + p.off_cnt) + 1;
   a.status = reinterpret_cast<unsigned long long*>(s->status);
-  a.B = (int)d->B; a.F = (int)d->F; a.T = (int)d->T; a.M = (int)d->M; a.N = (int)d->N;
-  a.K = (int)d->K;
+  a.F = (int)d->F; a.T = (int)d->T; a.N = (int)d->N; a.K = (int)d->K;
   a.f_offset = d->f_offset;
   a.normalize = d->normalize;
   a.ip_sweeps = d->ip_sweeps;
-  a.tail_only = tail_only;
+  dim3 grid((unsigned)d->F, (unsigned)d->B);
+  FM_DISPATCH_M(d->M, {
+    const size_t sm = FrontSmem<R, MM>::bytes;
+    if (int rc = ensure_smem(k_front<R, MM>, sm)) return rc;
+    k_front<R, MM><<<grid, FrCfg<MM>::BS, sm, st>>>(a);
+    FM_CHECK_LAUNCH("k_front");
+  });
+  return FM_OK;
+}
+
+template <typename R>
+int Impl<R>::back(const fm_dims* d, const fm_state* s, int tail_only, int record,
+                  cudaStream_t st) {
+  const Plan p = make_plan(d);
+  unsigned char* w = reinterpret_cast<unsigned char*>(s->work);
+  BackArgs<R> a;
+  a.X = reinterpret_cast<const C*>(s->X);
+  a.xt = reinterpret_cast<R*>(s->xt);
+  a.Q = reinterpret_cast<const C*>(s->Q);
+  a.g = reinterpret_cast<const R*>(s->g);
+  a.lam = reinterpret_cast<const R*>(w + p.off_lam);
+  a.cs = tail_only ? nullptr : reinterpret_cast<const R*>(w + p.off_cs);
+  a.phi = reinterpret_cast<R*>(w + p.off_phi);
+  a.floorp = reinterpret_cast<const R*>(s->floor);
+  a.ll_part = reinterpret_cast<double*>(w + p.off_llp);
+  a.ld_part = reinterpret_cast<const double*>(w + p.off_ldp);
+  a.trace = s->trace;
+  a.counter = reinterpret_cast<unsigned*>(w + p.off_cnt);
+  a.iter = a.counter + 1;
+  a.B = (int)d->B; a.F = (int)d->F; a.T = (int)d->T; a.N = (int)d->N;
   a.record = record && s->trace != nullptr;
   dim3 grid((unsigned)d->F, (unsigned)d->B);
   FM_DISPATCH_M(d->M, {
-    const size_t sm = spatial_smem_bytes<R, MM>();
-    if (int rc = ensure_smem(k_spatial<R, MM>, sm)) return rc;
-    k_spatial<R, MM><<<grid, SpCfg<MM>::BS, sm, st>>>(a);
-    FM_CHECK_LAUNCH("k_spatial");
+    k_back<R, MM><<<grid, 256, 0, st>>>(a);
+    FM_CHECK_LAUNCH("k_back");
   });
   return FM_OK;
 }
@@ -196,11 +215,11 @@ template <typename R>
 int Impl<R>::prologue(const fm_dims* d, const fm_state* s, cudaStream_t st) {
   const Plan p = make_plan(d);
   unsigned char* w = reinterpret_cast<unsigned char*>(s->work);
-  FM_CUDA(cudaMemsetAsync(w + p.off_cnt, 0, 64, st));
+  FM_CUDA(cudaMemsetAsync(w + p.off_cnt, 0, p.total - p.off_cnt, st));
   if (int rc = lambda(d, reinterpret_cast<const R*>(s->W), reinterpret_cast<const R*>(s->H),
                       reinterpret_cast<R*>(w + p.off_lam), st))
     return rc;
-  return spatial(d, s, /*tail_only=*/1, /*record=*/0, st);
+  return back(d, s, /*tail_only=*/1, /*record=*/0, st);
 }
 
 template <typename R>
@@ -213,45 +232,57 @@ int Impl<R>::iterate_phase(const fm_dims* d, const fm_state* s, int phase, void*
   R* lam = reinterpret_cast<R*>(w + p.off_lam);
   R* phi = reinterpret_cast<R*>(w + p.off_phi);
   R* part = reinterpret_cast<R*>(w + p.off_part);
+  unsigned* wcnt = reinterpret_cast<unsigned*>(w + p.off_tiles);
+  unsigned* hcnt = wcnt + (size_t)d->B * d->N * p.nft;
   R* W = reinterpret_cast<R*>(s->W);
   R* H = reinterpret_cast<R*>(s->H);
-  const int N = (int)d->N, F = (int)d->F, T = (int)d->T, M = (int)d->M, K = (int)d->K;
-  const long long NKT = (long long)N * K * T;
-  const long long total = (long long)d->B * NKT;
-  const unsigned hblocks = (unsigned)((total + 255) / 256);
-  // phase 0 (or full): W MU, 2nd statistics pass + H-statistic partials
+  const int N = (int)d->N, F = (int)d->F, T = (int)d->T, K = (int)d->K;
+  const unsigned BN = (unsigned)(d->B * d->N);
   if (phase == 0 || phase == 2) {
+    // W step (separate.py:214-216 with step "W"): statistics from the phi of the
+    // previous pass, MU, then the refresh with the new W (lambda + phi)
     FM_DISPATCH_KB(K, {
-      dim3 g1((unsigned)((F + 7) / 8), (unsigned)N, (unsigned)d->B);
       FM_EV(0);
-      k_wupdate<R, KB><<<g1, 256, 0, st>>>(phi, H, W, N, F, T, K);
-      FM_CHECK_LAUNCH("k_wupdate");
-      if (int rc = ensure_smem(k_hstats<R, KB>, p.hstats_smem)) return rc;
-      dim3 g2((unsigned)p.ntt, (unsigned)p.FC, (unsigned)d->B);
-      FM_EV(1);
-      k_hstats<R, KB><<<g2, 32 * N * p.G, p.hstats_smem, st>>>(
-          W, H, reinterpret_cast<const R*>(s->g), reinterpret_cast<const R*>(s->xt),
-          reinterpret_cast<const R*>(s->floor), part, N, F, T, M, K, p.FCH, p.G);
+      const size_t smw = WsCfg<R, KB>::bytes;
+      if (int rc = ensure_smem(k_wstats<R, KB>, smw)) return rc;
+      k_wstats<R, KB><<<dim3((unsigned)p.nft, (unsigned)p.TS, BN), 256, smw, st>>>(
+          phi, H, W, part, wcnt, N, F, T, K, p.TS);
+      FM_CHECK_LAUNCH("k_wstats");
+    });
+    FM_EV(1);
+    if (int rc = lambda(d, W, H, lam, st)) return rc;
+    FM_EV(2);
+    FM_DISPATCH_M(d->M, {
+      k_phi<R, MM><<<dim3((unsigned)((T + 255) / 256), (unsigned)F, (unsigned)d->B), 256, 0, st>>>(
+          lam, reinterpret_cast<const R*>(s->xt), reinterpret_cast<const R*>(s->g),
+          reinterpret_cast<const R*>(s->floor), phi, N, F, T);
+      FM_CHECK_LAUNCH("k_phi");
+    });
+    // H step (separate.py:214-216 with step "H")
+    FM_EV(3);
+    FM_DISPATCH_KB(K, {
+      const size_t smh = HsCfg<R, KB>::bytes;
+      if (int rc = ensure_smem(k_hstats<R, KB>, smh)) return rc;
+      k_hstats<R, KB><<<dim3((unsigned)p.ntt, (unsigned)p.FS, BN), 256, smh, st>>>(
+          phi, W, H, part, hcnt, reinterpret_cast<R*>(hstat), N, F, T, K, p.FS,
+          phase == 0 ? 1 : 0);
       FM_CHECK_LAUNCH("k_hstats");
     });
   }
-  if (phase == 0) {
-    k_hupdate<R><<<hblocks, 256, 0, st>>>(part, H, reinterpret_cast<R*>(hstat), p.FC, NKT, total, 1);
-    FM_CHECK_LAUNCH("k_hupdate(reduce)");
-    return FM_OK;
-  }
-  FM_EV(2);
+  if (phase == 0) return FM_OK;
   if (phase == 1) {
-    k_hupdate<R><<<hblocks, 256, 0, st>>>(part, H, reinterpret_cast<R*>(hstat), p.FC, NKT, total, 2);
-  } else {
-    k_hupdate<R><<<hblocks, 256, 0, st>>>(part, H, nullptr, p.FC, NKT, total, 0);
+    const long long NKT = (long long)N * K * T, total = (long long)d->B * NKT;
+    k_hupdate<R><<<(unsigned)((total + 255) / 256), 256, 0, st>>>(
+        part, H, reinterpret_cast<R*>(hstat), 1, NKT, total, 2);
+    FM_CHECK_LAUNCH("k_hupdate");
   }
-  FM_CHECK_LAUNCH("k_hupdate");
-  FM_EV(3);
-  if (int rc = lambda(d, W, H, lam, st)) return rc;
   FM_EV(4);
-  if (int rc = spatial(d, s, /*tail_only=*/0, /*record=*/1, st)) return rc;
+  if (int rc = lambda(d, W, H, lam, st)) return rc;
   FM_EV(5);
+  if (int rc = front(d, s, st)) return rc;
+  FM_EV(6);
+  if (int rc = back(d, s, /*tail_only=*/0, /*record=*/1, st)) return rc;
+  FM_EV(7);
   return FM_OK;
 #undef FM_EV
 }

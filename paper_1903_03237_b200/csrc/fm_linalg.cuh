@@ -148,3 +148,102 @@ __device__ int warp_ip_update(double2* Qd, const CV* V, double2* A, double2* x, 
 }
 
 }  // namespace fm
+
+namespace fm {
+
+// In-place Gauss-Jordan inverse of one M x M Hermitian positive-definite
+// matrix (row-major in smem) by one warp, entry-parallel, no pivoting (HPD
+// pivots are the positive Schur-complement diagonals). Returns false if a
+// pivot is not positive/finite (rank-deficient V_fm: the reference's
+// "non-positive normalization", spatial.py:194-198).
+template <int M>
+__device__ bool warp_inv_hpd(double2* A, int lane) {
+  constexpr int NE = (M * M + 31) / 32;
+  for (int k = 0; k < M; ++k) {
+    const double2 p = A[k * M + k];
+    if (!(p.x > 0.0) || !isfinite(p.x)) return false;
+    const double2 rp = cdiv(make_double2(1.0, 0.0), p);
+    double2 nv[NE];
+#pragma unroll
+    for (int r = 0; r < NE; ++r) {
+      const int e = lane + 32 * r;
+      if (e < M * M) {
+        const int i = e / M, j = e % M;
+        const double2 aik = A[i * M + k], akj = A[k * M + j];
+        if (i == k && j == k) nv[r] = rp;
+        else if (i == k) nv[r] = cmul(akj, rp);
+        else if (j == k) nv[r] = make_double2(-(aik.x * rp.x - aik.y * rp.y), -(aik.x * rp.y + aik.y * rp.x));
+        else nv[r] = csub(A[e], cmul(aik, cmul(akj, rp)));
+      }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int r = 0; r < NE; ++r) {
+      const int e = lane + 32 * r;
+      if (e < M * M) A[e] = nv[r];
+    }
+    __syncwarp();
+  }
+  return true;
+}
+
+// Gauss-Jordan with partial pivoting (izamax-style first max |re|+|im|) on
+// the augmented [Q | I] (M x 2M, row-major) by one warp; on success the
+// right half holds Q^-1 and *logabs = sum_k log|pivot_k| = log|det Q|
+// (the LU pivots; slogdet, separate.py:238).
+template <int M>
+__device__ bool warp_inv_pivot(double2* A, int lane, double* logabs) {
+  constexpr int W2 = 2 * M;
+  constexpr int NE = (M * W2 + 31) / 32;
+  double la = 0.0;
+  for (int k = 0; k < M; ++k) {
+    double v = -1.0;
+    int idx = lane;
+    if (lane >= k && lane < M) v = cabs1(A[lane * W2 + k]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(FM_FULL, v, o);
+      const int oi = __shfl_xor_sync(FM_FULL, idx, o);
+      if (ov > v || (ov == v && oi < idx)) {
+        v = ov;
+        idx = oi;
+      }
+    }
+    if (!(v > 0.0)) {
+      *logabs = -INFINITY;
+      return false;
+    }
+    if (idx != k) {
+      for (int c = lane; c < W2; c += 32) {
+        const double2 t = A[k * W2 + c];
+        A[k * W2 + c] = A[idx * W2 + c];
+        A[idx * W2 + c] = t;
+      }
+    }
+    __syncwarp();
+    const double2 piv = A[k * W2 + k];
+    la += log(hypot(piv.x, piv.y));
+    const double2 rp = cdiv(make_double2(1.0, 0.0), piv);
+    double2 nv[NE];
+#pragma unroll
+    for (int r = 0; r < NE; ++r) {
+      const int e = lane + 32 * r;
+      if (e < M * W2) {
+        const int i = e / W2, j = e % W2;
+        const double2 akj = cmul(A[k * W2 + j], rp);
+        nv[r] = (i == k) ? akj : csub(A[e], cmul(A[i * W2 + k], akj));
+      }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int r = 0; r < NE; ++r) {
+      const int e = lane + 32 * r;
+      if (e < M * W2) A[e] = nv[r];
+    }
+    __syncwarp();
+  }
+  *logabs = la;
+  return true;
+}
+
+}  // namespace fm

@@ -1,0 +1,386 @@
+// fm_nmf.cuh -- the NMF source-model part of the FastMNMF iteration as
+// register-blocked SIMT contractions (sources.py:167-204).
+//
+//   k_wstats  num/den_W = phi{1,2} H^T  (sum over T; sources.py:192-193),
+//             split over T across CTAs; the last CTA of each F-tile reduces
+//             the partials in fixed order and applies the W MU
+//             (sources.py:194).
+//   k_phi     statistics pass (separate.py:186-193; _kernels.py:226-243):
+//             phi1 = sum_m g x~/y^2, phi2 = sum_m g/y from lambda, x~, g.
+//   k_hstats  num/den_H = W^T phi{1,2}  (sum over F; sources.py:196-197),
+//             split over F across CTAs; the last CTA of each T-tile reduces
+//             in fixed order and applies the H MU (sources.py:198) -- or,
+//             frequency-sharded, writes the sums for the NCCL all-reduce.
+//
+// Both contractions stage their operands in shared memory with the
+// reduction index contiguous, and every thread owns a 4 x 4 (x2: numerator
+// and denominator) output block: 3 LDS.128 per 32 FMA.
+#pragma once
+#include "fm_common.cuh"
+
+namespace fm {
+
+__device__ __forceinline__ void lds4(const float* p, float (&v)[4]) {
+  const float4 q = *reinterpret_cast<const float4*>(p);
+  v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
+}
+__device__ __forceinline__ void lds4(const double* p, double (&v)[4]) {
+  const double2 a = *reinterpret_cast<const double2*>(p);
+  const double2 b = *reinterpret_cast<const double2*>(p + 2);
+  v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
+}
+
+// ---------------------------------------------------------------------------
+// W statistics + W MU. Tile: 32 f x KB k per CTA, T split in TS parts.
+// grid (ceil(F/32), TS, B*N), block 256.
+// Partials: part (B*N, TS, 2, F, K); counters: (B*N, ceil(F/32)).
+// ---------------------------------------------------------------------------
+template <typename R, int KB> struct WsCfg {
+  static constexpr int FT = 32;                          // f per CTA
+  static constexpr int TCH = sizeof(R) == 4 ? 64 : 32;   // t per staged chunk
+  static constexpr int LD = TCH + 4;                     // padded row
+  static constexpr int NTH = (FT / 4) * (KB / 4);        // threads per slice
+  static constexpr int S = 256 / NTH;                    // reduction slices per CTA
+  static constexpr int STAGE = (2 * FT + KB) * LD;       // staged operands (elements)
+  static constexpr int RED = 2 * FT * KB;                // slice reduction
+  static constexpr size_t bytes = sizeof(R) * (STAGE > RED ? STAGE : RED);
+};
+
+template <typename R, int KB>
+__global__ void __launch_bounds__(256) k_wstats(const R* __restrict__ phi, const R* __restrict__ H,
+                                                R* __restrict__ W, R* __restrict__ part,
+                                                unsigned* __restrict__ counters, int N, int F,
+                                                int T, int K, int TS) {
+  using Cf = WsCfg<R, KB>;
+  constexpr int FT = Cf::FT, TCH = Cf::TCH, LD = Cf::LD, NTH = Cf::NTH, S = Cf::S;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  R* p1s = reinterpret_cast<R*>(smraw);
+  R* p2s = p1s + FT * LD;
+  R* hs = p2s + FT * LD;
+  __shared__ int is_last;
+  const int bn = blockIdx.z, ts = blockIdx.y, ftile = blockIdx.x;
+  const int f0 = ftile * FT;
+  const int tid = threadIdx.x;
+  const int slot = tid % NTH, s = tid / NTH;
+  const int fg = slot % (FT / 4), kg = slot / (FT / 4);
+  const size_t FTs = (size_t)F * T;
+  const int b = bn / N, n = bn % N;
+  const R* P1 = phi + ((size_t)b * 2 * N + n) * FTs;
+  const R* P2 = P1 + (size_t)N * FTs;
+  const R* Hn = H + (size_t)bn * K * T;
+  // T range of this split (multiples of 4 keep the quads aligned)
+  const int tper = ((T + TS - 1) / TS + 3) & ~3;
+  const int ta = ts * tper, tb = min(T, ta + tper);
+  R a1[4][4], a2[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) a1[i][j] = a2[i][j] = 0;
+  for (int t0 = ta; t0 < tb; t0 += TCH) {
+    // stage phi1/phi2 rows (FT x TCH) and H rows (KB x TCH); t contiguous
+    for (int e = tid; e < FT * TCH; e += 256) {
+      const int fl = e / TCH, tl = e % TCH;
+      const int f = f0 + fl, t = t0 + tl;
+      const bool v = f < F && t < tb;
+      p1s[fl * LD + tl] = v ? P1[(size_t)f * T + t] : R(0);
+      p2s[fl * LD + tl] = v ? P2[(size_t)f * T + t] : R(0);
+    }
+    for (int e = tid; e < KB * TCH; e += 256) {
+      const int kl = e / TCH, tl = e % TCH;
+      const int t = t0 + tl;
+      hs[kl * LD + tl] = (kl < K && t < tb) ? Hn[(size_t)kl * T + t] : R(0);
+    }
+    __syncthreads();
+    if (s < S) {
+      for (int tq = s * 4; tq < TCH; tq += 4 * S) {
+        R x1[4][4], x2[4][4], h[4][4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          lds4(p1s + (fg + 8 * i) * LD + tq, x1[i]);
+          lds4(p2s + (fg + 8 * i) * LD + tq, x2[i]);
+          lds4(hs + (kg + (KB / 4) * i) * LD + tq, h[i]);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              a1[i][j] += x1[i][u] * h[j][u];
+              a2[i][j] += x2[i][u] * h[j][u];
+            }
+      }
+    }
+    __syncthreads();
+  }
+  // fixed-order reduction over the S slices (staging area reused)
+  R* red = p1s;
+  R* red2 = p1s + FT * KB;
+  for (int ss = 0; ss < S; ++ss) {
+    if (s == ss) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int idx = (fg + 8 * i) * KB + kg + (KB / 4) * j;
+          if (ss == 0) {
+            red[idx] = a1[i][j];
+            red2[idx] = a2[i][j];
+          } else {
+            red[idx] += a1[i][j];
+            red2[idx] += a2[i][j];
+          }
+        }
+    }
+    __syncthreads();
+  }
+  // write this split's partial, then the last split of the tile reduces + MU
+  R* pb = part + ((size_t)bn * TS + ts) * 2 * (size_t)F * K;
+  for (int e = tid; e < FT * KB; e += 256) {
+    const int fl = e / KB, k = e % KB, f = f0 + fl;
+    if (f < F && k < K) {
+      pb[(size_t)f * K + k] = red[e];
+      pb[(size_t)F * K + (size_t)f * K + k] = red2[e];
+    }
+  }
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) {
+    unsigned* c = counters + (size_t)bn * gridDim.x + ftile;
+    const unsigned prev = atomicAdd(c, 1u);
+    is_last = prev == (unsigned)TS - 1;
+    if (is_last) *c = 0u;
+  }
+  __syncthreads();
+  if (!is_last) return;
+  __threadfence();
+  R* Wn = W + (size_t)bn * F * K;
+  for (int e = tid; e < FT * KB; e += 256) {
+    const int fl = e / KB, k = e % KB, f = f0 + fl;
+    if (f < F && k < K) {
+      R sn = 0, sd = 0;
+      for (int q = 0; q < TS; ++q) {
+        const R* pq = part + ((size_t)bn * TS + q) * 2 * (size_t)F * K;
+        sn += __ldcg(pq + (size_t)f * K + k);
+        sd += __ldcg(pq + (size_t)F * K + (size_t)f * K + k);
+      }
+      Wn[(size_t)f * K + k] *= mu_factor(sn, sd);  // sources.py:194
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// H statistics + H MU. Tile: KB k x 64 t per CTA, F split in FS parts.
+// grid (ceil(T/64), FS, B*N), block 256.
+// Partials: part (B*N, FS, 2, K, T); counters (B*N, ceil(T/64)).
+// mode 0: apply the MU; mode 1: write the (num, den) sums to hout
+// (B, 2, N, K, T) for the cross-shard all-reduce.
+// ---------------------------------------------------------------------------
+template <typename R, int KB> struct HsCfg {
+  static constexpr int TT = 64;                          // t per CTA
+  static constexpr int FCH = sizeof(R) == 4 ? 32 : 16;   // f per staged chunk
+  static constexpr int NTH = (KB / 4) * (TT / 4);        // threads per slice
+  static constexpr int S = 256 / NTH;                    // reduction slices
+  static constexpr int LDW = KB + 4, LDP = TT + 4;
+  static constexpr int STAGE = FCH * LDW + 2 * FCH * LDP;
+  static constexpr int RED = 2 * KB * TT;
+  static constexpr size_t bytes = sizeof(R) * (STAGE > RED ? STAGE : RED);
+};
+
+template <typename R, int KB>
+__global__ void __launch_bounds__(256) k_hstats(const R* __restrict__ phi, const R* __restrict__ W,
+                                                R* __restrict__ H, R* __restrict__ part,
+                                                unsigned* __restrict__ counters,
+                                                R* __restrict__ hout, int N, int F, int T, int K,
+                                                int FS, int mode) {
+  using Cf = HsCfg<R, KB>;
+  constexpr int TT = Cf::TT, FCH = Cf::FCH, NTH = Cf::NTH, S = Cf::S;
+  constexpr int LDW = Cf::LDW, LDP = Cf::LDP;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  R* ws = reinterpret_cast<R*>(smraw);
+  R* p1s = ws + FCH * LDW;
+  R* p2s = p1s + FCH * LDP;
+  __shared__ int is_last;
+  const int bn = blockIdx.z, fs = blockIdx.y, ttile = blockIdx.x;
+  const int t0 = ttile * TT;
+  const int tid = threadIdx.x;
+  const int slot = tid % NTH, s = tid / NTH;
+  const int tg = slot % (TT / 4), kg = slot / (TT / 4);
+  const size_t FTs = (size_t)F * T;
+  const int b = bn / N, n = bn % N;
+  const R* P1 = phi + ((size_t)b * 2 * N + n) * FTs;
+  const R* P2 = P1 + (size_t)N * FTs;
+  const R* Wn = W + (size_t)bn * F * K;
+  const int fper = (F + FS - 1) / FS;
+  const int fa = fs * fper, fb = min(F, fa + fper);
+  R a1[4][4], a2[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) a1[i][j] = a2[i][j] = 0;
+  for (int c0 = fa; c0 < fb; c0 += FCH) {
+    for (int e = tid; e < FCH * KB; e += 256) {
+      const int fl = e / KB, k = e % KB, f = c0 + fl;
+      ws[fl * LDW + k] = (f < fb && k < K) ? Wn[(size_t)f * K + k] : R(0);
+    }
+    for (int e = tid; e < FCH * TT; e += 256) {
+      const int fl = e / TT, tl = e % TT, f = c0 + fl, t = t0 + tl;
+      const bool v = f < fb && t < T;
+      p1s[fl * LDP + tl] = v ? P1[(size_t)f * T + t] : R(0);
+      p2s[fl * LDP + tl] = v ? P2[(size_t)f * T + t] : R(0);
+    }
+    __syncthreads();
+    if (s < S) {
+      const int fe = min(FCH, fb - c0);
+      for (int fl = s; fl < fe; fl += S) {
+        R w[4], x1[4], x2[4];
+        lds4(ws + fl * LDW + kg * 4, w);
+        lds4(p1s + fl * LDP + tg * 4, x1);
+        lds4(p2s + fl * LDP + tg * 4, x2);
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            a1[i][j] += w[i] * x1[j];
+            a2[i][j] += w[i] * x2[j];
+          }
+      }
+    }
+    __syncthreads();
+  }
+  // fixed-order slice reduction into smem (KB x TT each; staging area reused)
+  R* red = ws;
+  R* red2 = ws + KB * TT;
+  for (int ss = 0; ss < S; ++ss) {
+    if (s == ss) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int idx = (kg * 4 + i) * TT + tg * 4 + j;
+          if (ss == 0) {
+            red[idx] = a1[i][j];
+            red2[idx] = a2[i][j];
+          } else {
+            red[idx] += a1[i][j];
+            red2[idx] += a2[i][j];
+          }
+        }
+    }
+    __syncthreads();
+  }
+  R* pb = part + ((size_t)bn * FS + fs) * 2 * (size_t)K * T;
+  for (int e = tid; e < KB * TT; e += 256) {
+    const int k = e / TT, tl = e % TT, t = t0 + tl;
+    if (k < K && t < T) {
+      pb[(size_t)k * T + t] = red[e];
+      pb[(size_t)K * T + (size_t)k * T + t] = red2[e];
+    }
+  }
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) {
+    unsigned* c = counters + (size_t)bn * gridDim.x + ttile;
+    const unsigned prev = atomicAdd(c, 1u);
+    is_last = prev == (unsigned)FS - 1;
+    if (is_last) *c = 0u;
+  }
+  __syncthreads();
+  if (!is_last) return;
+  __threadfence();
+  R* Hn = H + (size_t)bn * K * T;
+  for (int e = tid; e < KB * TT; e += 256) {
+    const int k = e / TT, tl = e % TT, t = t0 + tl;
+    if (k < K && t < T) {
+      R sn = 0, sd = 0;
+      for (int q = 0; q < FS; ++q) {
+        const R* pq = part + ((size_t)bn * FS + q) * 2 * (size_t)K * T;
+        sn += __ldcg(pq + (size_t)k * T + t);
+        sd += __ldcg(pq + (size_t)K * T + (size_t)k * T + t);
+      }
+      if (mode == 0) {
+        Hn[(size_t)k * T + t] *= mu_factor(sn, sd);  // sources.py:198
+      } else {
+        const size_t NKT = (size_t)N * K * T;
+        hout[(size_t)b * 2 * NKT + (size_t)n * K * T + (size_t)k * T + t] = sn;
+        hout[(size_t)b * 2 * NKT + NKT + (size_t)n * K * T + (size_t)k * T + t] = sd;
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Statistics pass at one (f, t): phi1[n] = sum_m g x~/y^2, phi2[n] = sum_m g/y,
+// and the data term sum_m (-x~/y - log y)  (_kernels.py:226-243).
+// Loops over sources exit early (uniform branch) instead of predicating.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ float rcp_r(float y) { return __frcp_rn(y); }
+__device__ __forceinline__ double rcp_r(double y) { return 1.0 / y; }
+
+template <typename R, int M>
+__device__ __forceinline__ void model_power(const R (&l)[NMAX], const R* gs, int N, R fl,
+                                            R (&iy)[M], R (&y)[M]) {
+#pragma unroll
+  for (int m = 0; m < M; ++m) y[m] = 0;
+#pragma unroll
+  for (int n = 0; n < NMAX; ++n) {
+    if (n >= N) break;
+    R g[M];
+    RowIO<R, M>::load(gs + n * M, g);
+#pragma unroll
+    for (int m = 0; m < M; ++m) y[m] += l[n] * g[m];
+  }
+#pragma unroll
+  for (int m = 0; m < M; ++m) {
+    y[m] = floor_max(y[m], fl);
+    iy[m] = rcp_r(y[m]);
+  }
+}
+
+template <typename R, int M>
+__device__ __forceinline__ void phi_point(const R (&xtv)[M], const R (&iy)[M], const R* gs, int N,
+                                          R* phi, size_t FT, size_t off) {
+  R r[M];
+#pragma unroll
+  for (int m = 0; m < M; ++m) r[m] = xtv[m] * iy[m] * iy[m];
+#pragma unroll
+  for (int n = 0; n < NMAX; ++n) {
+    if (n >= N) break;
+    R g[M];
+    RowIO<R, M>::load(gs + n * M, g);
+    R p1 = 0, p2 = 0;
+#pragma unroll
+    for (int m = 0; m < M; ++m) {
+      p1 += g[m] * r[m];
+      p2 += g[m] * iy[m];
+    }
+    phi[(size_t)n * FT + off] = p1;
+    phi[(size_t)(N + n) * FT + off] = p2;
+  }
+}
+
+// refresh after the W step (separate.py:215): grid (ceil(T/256), F, B), block 256
+template <typename R, int M>
+__global__ void __launch_bounds__(256) k_phi(const R* __restrict__ lam, const R* __restrict__ xt,
+                                             const R* __restrict__ g, const R* __restrict__ floorp,
+                                             R* __restrict__ phi, int N, int F, int T) {
+  __shared__ __align__(16) R gs[NMAX * M];
+  const int f = blockIdx.y, b = blockIdx.z, tid = threadIdx.x;
+  const int t = blockIdx.x * 256 + tid;
+  const size_t FT = (size_t)F * T;
+  for (int e = tid; e < N * M; e += 256)
+    gs[e] = g[(size_t)b * N * F * M + (size_t)(e / M) * F * M + (size_t)f * M + (e % M)];
+  __syncthreads();
+  if (t >= T) return;
+  const R fl = floorp[b];
+  const R* lb = lam + (size_t)b * N * FT + (size_t)f * T + t;
+  R l[NMAX];
+#pragma unroll
+  for (int n = 0; n < NMAX; ++n) l[n] = n < N ? lb[(size_t)n * FT] : R(0);
+  R xtv[M], iy[M], y[M];
+  RowIO<R, M>::load(xt + (((size_t)b * F + f) * T + t) * M, xtv);
+  model_power<R, M>(l, gs, N, fl, iy, y);
+  phi_point<R, M>(xtv, iy, gs, N, phi + (size_t)b * 2 * N * FT, FT, (size_t)f * T + t);
+}
+
+}  // namespace fm
