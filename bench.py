@@ -297,11 +297,12 @@ def main():
     iters_per_s = iters / (ms_per_step / 1e3)
 
     # ---- roofline of the dominant kernel: per-kernel CUDA events on the launch stream
-    names = ["k_wstats", "k_lambda(W)", "k_phi", "k_hstats", "k_lambda(H)", "k_front", "k_back"]
-    acc = np.zeros(7)
+    names = ["k_wstats", "k_lambda(W)", "k_phi", "k_hstats", "k_lambda(H)", "k_front", "k_ip",
+             "k_back"]
+    acc = np.zeros(8)
     nprof = 10
     if not sharded_f:
-        ms = (ctypes.c_float * 7)()
+        ms = (ctypes.c_float * 8)()
         for _ in range(nprof):
             _lib.check(lib.fm_iterate_profiled(ctypes.byref(loop.dims), ctypes.byref(loop.state), ms,
                                                _lib.stream_ptr()), "fm_iterate_profiled")
@@ -320,6 +321,7 @@ def main():
         "k_phi": ftm * rs + 3 * N * (ftm // M) * rs,       # read xt, lambda; write phi
         "k_lambda(W)": N * (ftm // M) * rs,                # write lambda
         "k_lambda(H)": N * (ftm // M) * rs,
+        "k_ip": 0,
     }[names[dom]]
     hbm, peak_kind = peaks()
     achieved = alg / (acc[dom] / 1e3) / 1e9 if acc[dom] > 0 else None
@@ -357,7 +359,7 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline and args.config in ("c1", "c0"):
         cpu = cpu_baseline_sample(cfg)
 
-    launches = args.steps * (2 + 7 * iters)
+    launches = args.steps * (2 + 8 * iters)
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,

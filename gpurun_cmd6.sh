@@ -1,0 +1,9 @@
+timeout 900 python -m pytest tests -m gpu -q --timeout 600 -x > gpurun_out/pytest_gpu.log 2>&1; echo rc=$? >> gpurun_out/pytest_gpu.log
+timeout 600 python bench.py --no-cpu-baseline > gpurun_out/bench_c1.json 2> gpurun_out/bench_c1.err
+timeout 600 python bench.py --config c2 --steps 3 --warmup 3 --no-e2e > gpurun_out/bench_c2.json 2> gpurun_out/bench_c2.err
+timeout 600 python bench.py --config c3 --steps 2 --warmup 3 --iters 20 --no-e2e > gpurun_out/bench_c3.json 2> gpurun_out/bench_c3.err
+ARGS="--steps 1 --warmup 3 --iters 5 --no-e2e --no-cpu-baseline"
+timeout 300 python bench.py $ARGS > gpurun_out/plain6.log 2>&1 && \
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -s 60 -c 70 --csv --log-file gpurun_out/launches_c1_v4.csv python bench.py $ARGS > gpurun_out/ncu6a.log 2>&1 && \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_front|k_back|k_lambda|k_wstats|k_hstats|k_phi" -s 20 -c 7 -o gpurun_out/prof_c1_v4 python bench.py $ARGS > gpurun_out/ncu6b.log 2>&1
+echo done

@@ -54,6 +54,11 @@ __device__ __forceinline__ double2 cdiv(double2 a, double2 b) {
   }
 }
 __device__ __forceinline__ double cabs1(double2 a) { return fabs(a.x) + fabs(a.y); }
+// 1/p as conj(p)/|p|^2: one fp64 division (pivots here are well scaled)
+__device__ __forceinline__ double2 crcp(double2 p) {
+  const double inv = 1.0 / (p.x * p.x + p.y * p.y);
+  return make_double2(p.x * inv, -p.y * inv);
+}
 __device__ __forceinline__ double2 to_d2(float2 a) { return make_double2(a.x, a.y); }
 __device__ __forceinline__ double2 to_d2(double2 a) { return a; }
 

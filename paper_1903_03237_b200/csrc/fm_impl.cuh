@@ -17,6 +17,8 @@
 namespace fm {
 
 void set_error(const char* fmt, ...);
+// device buffer for k_front phase stamps (fm_debug_front_timing); null = off
+extern long long* g_front_timing;
 
 #define FM_CHECK_LAUNCH(what)                                                   \
   do {                                                                          \
@@ -71,7 +73,7 @@ inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 // Workspace plan for the fused iteration.
 struct Plan {
   int TS, FS, nft, ntt;  // split counts of k_wstats / k_hstats, their tile counts
-  size_t off_lam, off_phi, off_part, off_llp, off_ldp, off_cs, off_cnt, off_tiles, total;
+  size_t off_lam, off_phi, off_part, off_llp, off_ldp, off_cs, off_V, off_cnt, off_tiles, total;
 };
 
 inline Plan make_plan(const fm_dims* d) {
@@ -94,6 +96,7 @@ inline Plan make_plan(const fm_dims* d) {
   p.off_llp = o; o = align256(o + (size_t)B * F * 8);
   p.off_ldp = o; o = align256(o + (size_t)B * F * 8);
   p.off_cs = o; o = align256(o + (size_t)B * F * NMAX * rs);
+  p.off_V = o; o = align256(o + (size_t)B * F * d->M * d->M * d->M * sizeof(double2));
   p.off_cnt = o; o = align256(o + 64);
   p.off_tiles = o; o = align256(o + sizeof(unsigned) * (size_t)B * N * (p.nft + p.ntt));
   p.total = o;
@@ -107,9 +110,10 @@ template <typename R> struct Impl {
 
   static int prologue(const fm_dims* d, const fm_state* s, cudaStream_t st);
   static int iterate_phase(const fm_dims* d, const fm_state* s, int phase, void* hstat,
-                           cudaStream_t st, cudaEvent_t* ev = nullptr);  // ev: 8 events
+                           cudaStream_t st, cudaEvent_t* ev = nullptr);  // ev: 9 events
   static int lambda(const fm_dims* d, const R* W, const R* H, R* lam, cudaStream_t st);
   static int front(const fm_dims* d, const fm_state* s, cudaStream_t st);
+  static int ip(const fm_dims* d, const fm_state* s, cudaStream_t st);
   static int back(const fm_dims* d, const fm_state* s, int tail_only, int record, cudaStream_t st);
 
   static int fast_stats(int64_t F, int64_t T, int64_t M, int64_t N, const void* xt,
@@ -164,20 +168,42 @@ int Impl<R>::front(const fm_dims* d, const fm_state* s, cudaStream_t st) {
   a.W = reinterpret_cast<R*>(s->W);
   a.lam = reinterpret_cast<const R*>(w + p.off_lam);
   a.floorp = reinterpret_cast<const R*>(s->floor);
-  a.cs_out = reinterpret_cast<R*>(w + p.off_cs);
-  a.ld_part = reinterpret_cast<double*>(w + p.off_ldp);
-  a.iter = reinterpret_cast<const unsigned*>(w + p.off_cnt) + 1;
-  a.status = reinterpret_cast<unsigned long long*>(s->status);
+  a.V = reinterpret_cast<double2*>(w + p.off_V);
   a.F = (int)d->F; a.T = (int)d->T; a.N = (int)d->N; a.K = (int)d->K;
-  a.f_offset = d->f_offset;
-  a.normalize = d->normalize;
-  a.ip_sweeps = d->ip_sweeps;
+  a.timing = g_front_timing;
   dim3 grid((unsigned)d->F, (unsigned)d->B);
   FM_DISPATCH_M(d->M, {
     const size_t sm = FrontSmem<R, MM>::bytes;
     if (int rc = ensure_smem(k_front<R, MM>, sm)) return rc;
     k_front<R, MM><<<grid, FrCfg<MM>::BS, sm, st>>>(a);
     FM_CHECK_LAUNCH("k_front");
+  });
+  return FM_OK;
+}
+
+template <typename R>
+int Impl<R>::ip(const fm_dims* d, const fm_state* s, cudaStream_t st) {
+  const Plan p = make_plan(d);
+  unsigned char* w = reinterpret_cast<unsigned char*>(s->work);
+  IpArgs<R> a;
+  a.V = reinterpret_cast<const double2*>(w + p.off_V);
+  a.Q = reinterpret_cast<C*>(s->Q);
+  a.g = reinterpret_cast<R*>(s->g);
+  a.W = reinterpret_cast<R*>(s->W);
+  a.cs_out = reinterpret_cast<R*>(w + p.off_cs);
+  a.ld_part = reinterpret_cast<double*>(w + p.off_ldp);
+  a.iter = reinterpret_cast<const unsigned*>(w + p.off_cnt) + 1;
+  a.status = reinterpret_cast<unsigned long long*>(s->status);
+  a.F = (int)d->F; a.N = (int)d->N; a.K = (int)d->K;
+  a.f_offset = d->f_offset;
+  a.normalize = d->normalize;
+  a.ip_sweeps = d->ip_sweeps;
+  dim3 grid((unsigned)d->F, (unsigned)d->B);
+  FM_DISPATCH_M(d->M, {
+    const size_t sm = IpSmem<R, MM>::bytes;
+    if (int rc = ensure_smem(k_ip<R, MM>, sm)) return rc;
+    k_ip<R, MM><<<grid, IpCfg<MM>::BS, sm, st>>>(a);
+    FM_CHECK_LAUNCH("k_ip");
   });
   return FM_OK;
 }
@@ -281,8 +307,10 @@ int Impl<R>::iterate_phase(const fm_dims* d, const fm_state* s, int phase, void*
   FM_EV(5);
   if (int rc = front(d, s, st)) return rc;
   FM_EV(6);
-  if (int rc = back(d, s, /*tail_only=*/0, /*record=*/1, st)) return rc;
+  if (int rc = ip(d, s, st)) return rc;
   FM_EV(7);
+  if (int rc = back(d, s, /*tail_only=*/0, /*record=*/1, st)) return rc;
+  FM_EV(8);
   return FM_OK;
 #undef FM_EV
 }

@@ -31,14 +31,16 @@ namespace fm {
 template <typename R>
 __global__ void __launch_bounds__(256) k_lambda(const R* __restrict__ W, const R* __restrict__ H,
                                                 R* __restrict__ lam, int F, int T, int K) {
-  __shared__ R Ws[32][64 + 4];
-  __shared__ R Hs[32][64 + 4];
+  __shared__ __align__(16) R Ws[32][64 + 4];
+  __shared__ __align__(16) R Hs[32][64 + 4];
   const int bn = blockIdx.z;
   const int t0 = blockIdx.x * 64, f0 = blockIdx.y * 64;
   const R* Wb = W + (size_t)bn * F * K;
   const R* Hb = H + (size_t)bn * K * T;
   R* Lb = lam + (size_t)bn * F * T;
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  // 16-B vector paths need 4-element alignment of rows (fp32 only)
+  const bool vec = sizeof(R) == 4 && (K % 4) == 0 && (T % 4) == 0;
   R acc[4][4];
 #pragma unroll
   for (int i = 0; i < 4; ++i)
@@ -46,15 +48,29 @@ __global__ void __launch_bounds__(256) k_lambda(const R* __restrict__ W, const R
     for (int j = 0; j < 4; ++j) acc[i][j] = 0;
   for (int k0 = 0; k0 < K; k0 += 32) {
     const int kc = min(32, K - k0);
-    for (int e = threadIdx.x; e < 64 * 32; e += 256) {
-      // W tile: 64 f rows x 32 k (k contiguous in memory) -> Ws[k][f]
-      const int fl = e / 32, kl = e % 32;
-      const int f = f0 + fl, k = k0 + kl;
-      Ws[kl][fl] = (f < F && kl < kc) ? Wb[(size_t)f * K + k] : R(0);
-      // H tile: 32 k rows x 64 t (t contiguous) -> Hs[k][t]
-      const int kh = e / 64, th = e % 64;
-      const int t = t0 + th;
-      Hs[kh][th] = (kh < kc && t < T) ? Hb[(size_t)(k0 + kh) * T + t] : R(0);
+    if (vec) {
+      const int kq = kc / 4;  // float4 per W row segment
+      for (int e = threadIdx.x; e < 64 * kq; e += 256) {
+        const int fl = e / kq, q = e % kq, f = f0 + fl;
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (f < F) v = *reinterpret_cast<const float4*>(reinterpret_cast<const float*>(Wb) + (size_t)f * K + k0 + 4 * q);
+        Ws[4 * q][fl] = v.x; Ws[4 * q + 1][fl] = v.y; Ws[4 * q + 2][fl] = v.z; Ws[4 * q + 3][fl] = v.w;
+      }
+      for (int e = threadIdx.x; e < kc * 16; e += 256) {
+        const int kh = e / 16, q = e % 16, t = t0 + 4 * q;
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (t < T) v = *reinterpret_cast<const float4*>(reinterpret_cast<const float*>(Hb) + (size_t)(k0 + kh) * T + t);
+        *reinterpret_cast<float4*>(&Hs[kh][4 * q]) = v;
+      }
+    } else {
+      for (int e = threadIdx.x; e < 64 * kc; e += 256) {
+        const int fl = e / kc, kl = e % kc, f = f0 + fl;
+        Ws[kl][fl] = f < F ? Wb[(size_t)f * K + k0 + kl] : R(0);
+      }
+      for (int e = threadIdx.x; e < kc * 64; e += 256) {
+        const int kh = e / 64, th = e % 64, t = t0 + th;
+        Hs[kh][th] = t < T ? Hb[(size_t)(k0 + kh) * T + t] : R(0);
+      }
     }
     __syncthreads();
     for (int k = 0; k < kc; ++k) {
@@ -70,14 +86,19 @@ __global__ void __launch_bounds__(256) k_lambda(const R* __restrict__ W, const R
     }
     __syncthreads();
   }
+  const int tb = t0 + tx * 4;
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const int f = f0 + ty * 4 + i;
     if (f >= F) continue;
+    R* o = Lb + (size_t)f * T + tb;
+    if (vec && tb + 3 < T) {
+      *reinterpret_cast<float4*>(reinterpret_cast<float*>(o)) =
+          make_float4((float)acc[i][0], (float)acc[i][1], (float)acc[i][2], (float)acc[i][3]);
+    } else {
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int t = t0 + tx * 4 + j;
-      if (t < T) Lb[(size_t)f * T + t] = acc[i][j];
+      for (int j = 0; j < 4; ++j)
+        if (tb + j < T) o[j] = acc[i][j];
     }
   }
 }

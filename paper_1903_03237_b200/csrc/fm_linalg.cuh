@@ -162,7 +162,7 @@ __device__ bool warp_inv_hpd(double2* A, int lane) {
   for (int k = 0; k < M; ++k) {
     const double2 p = A[k * M + k];
     if (!(p.x > 0.0) || !isfinite(p.x)) return false;
-    const double2 rp = cdiv(make_double2(1.0, 0.0), p);
+    const double2 rp = crcp(p);
     double2 nv[NE];
 #pragma unroll
     for (int r = 0; r < NE; ++r) {
@@ -222,8 +222,8 @@ __device__ bool warp_inv_pivot(double2* A, int lane, double* logabs) {
     }
     __syncwarp();
     const double2 piv = A[k * W2 + k];
-    la += log(hypot(piv.x, piv.y));
-    const double2 rp = cdiv(make_double2(1.0, 0.0), piv);
+    la += 0.5 * log(piv.x * piv.x + piv.y * piv.y);
+    const double2 rp = crcp(piv);
     double2 nv[NE];
 #pragma unroll
     for (int r = 0; r < NE; ++r) {

@@ -30,6 +30,17 @@ __device__ __forceinline__ void lds4(const double* p, double (&v)[4]) {
   v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
 }
 
+// cp.async (LDGSTS) 16-byte copies with zero-fill, for double-buffered staging
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  const int n = valid ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gmem), "r"(n));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int NPEND> __device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(NPEND));
+}
+
 // ---------------------------------------------------------------------------
 // W statistics + W MU. Tile: 32 f x KB k per CTA, T split in TS parts.
 // grid (ceil(F/32), TS, B*N), block 256.
@@ -43,7 +54,7 @@ template <typename R, int KB> struct WsCfg {
   static constexpr int S = 256 / NTH;                    // reduction slices per CTA
   static constexpr int STAGE = (2 * FT + KB) * LD;       // staged operands (elements)
   static constexpr int RED = 2 * FT * KB;                // slice reduction
-  static constexpr size_t bytes = sizeof(R) * (STAGE > RED ? STAGE : RED);
+  static constexpr size_t bytes = sizeof(R) * (2 * STAGE > RED ? 2 * STAGE : RED);
 };
 
 template <typename R, int KB>
@@ -54,9 +65,7 @@ __global__ void __launch_bounds__(256) k_wstats(const R* __restrict__ phi, const
   using Cf = WsCfg<R, KB>;
   constexpr int FT = Cf::FT, TCH = Cf::TCH, LD = Cf::LD, NTH = Cf::NTH, S = Cf::S;
   extern __shared__ __align__(16) unsigned char smraw[];
-  R* p1s = reinterpret_cast<R*>(smraw);
-  R* p2s = p1s + FT * LD;
-  R* hs = p2s + FT * LD;
+  R* stage0 = reinterpret_cast<R*>(smraw);
   __shared__ int is_last;
   const int bn = blockIdx.z, ts = blockIdx.y, ftile = blockIdx.x;
   const int f0 = ftile * FT;
@@ -71,26 +80,61 @@ __global__ void __launch_bounds__(256) k_wstats(const R* __restrict__ phi, const
   // T range of this split (multiples of 4 keep the quads aligned)
   const int tper = ((T + TS - 1) / TS + 3) & ~3;
   const int ta = ts * tper, tb = min(T, ta + tper);
+  const bool async = sizeof(R) == 4 && (T % 4) == 0;
+  auto stage = [&](int st) { return stage0 + st * Cf::STAGE; };
+  // stage phi1/phi2 rows (FT x TCH) and H rows (KB x TCH) of chunk t0; t contiguous
+  auto load = [&](int st, int t0) {
+    R* p1s = stage(st);
+    R* p2s = p1s + FT * LD;
+    R* hs = p2s + FT * LD;
+    if (async) {
+      constexpr int Q = TCH / 4;
+      for (int e = tid; e < FT * Q; e += 256) {
+        const int fl = e / Q, q = e % Q, f = f0 + fl, t = t0 + 4 * q;
+        const bool v = f < F && t < tb;
+        const size_t off = v ? (size_t)f * T + t : 0;
+        cp_async16(p1s + fl * LD + 4 * q, P1 + off, v);
+        cp_async16(p2s + fl * LD + 4 * q, P2 + off, v);
+      }
+      for (int e = tid; e < KB * Q; e += 256) {
+        const int kl = e / Q, q = e % Q, t = t0 + 4 * q;
+        const bool v = kl < K && t < tb;
+        cp_async16(hs + kl * LD + 4 * q, Hn + (v ? (size_t)kl * T + t : 0), v);
+      }
+    } else {
+      for (int e = tid; e < FT * TCH; e += 256) {
+        const int fl = e / TCH, tl = e % TCH;
+        const int f = f0 + fl, t = t0 + tl;
+        const bool v = f < F && t < tb;
+        p1s[fl * LD + tl] = v ? P1[(size_t)f * T + t] : R(0);
+        p2s[fl * LD + tl] = v ? P2[(size_t)f * T + t] : R(0);
+      }
+      for (int e = tid; e < KB * TCH; e += 256) {
+        const int kl = e / TCH, tl = e % TCH;
+        const int t = t0 + tl;
+        hs[kl * LD + tl] = (kl < K && t < tb) ? Hn[(size_t)kl * T + t] : R(0);
+      }
+    }
+    cp_async_commit();
+  };
   R a1[4][4], a2[4][4];
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j) a1[i][j] = a2[i][j] = 0;
-  for (int t0 = ta; t0 < tb; t0 += TCH) {
-    // stage phi1/phi2 rows (FT x TCH) and H rows (KB x TCH); t contiguous
-    for (int e = tid; e < FT * TCH; e += 256) {
-      const int fl = e / TCH, tl = e % TCH;
-      const int f = f0 + fl, t = t0 + tl;
-      const bool v = f < F && t < tb;
-      p1s[fl * LD + tl] = v ? P1[(size_t)f * T + t] : R(0);
-      p2s[fl * LD + tl] = v ? P2[(size_t)f * T + t] : R(0);
-    }
-    for (int e = tid; e < KB * TCH; e += 256) {
-      const int kl = e / TCH, tl = e % TCH;
-      const int t = t0 + tl;
-      hs[kl * LD + tl] = (kl < K && t < tb) ? Hn[(size_t)kl * T + t] : R(0);
+  int st = 0;
+  if (ta < tb) load(0, ta);
+  for (int t0 = ta; t0 < tb; t0 += TCH, st ^= 1) {
+    if (t0 + TCH < tb) {
+      load(st ^ 1, t0 + TCH);  // next chunk in flight during this one
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
     }
     __syncthreads();
+    const R* p1s = stage(st);
+    const R* p2s = p1s + FT * LD;
+    const R* hs = p2s + FT * LD;
     if (s < S) {
       for (int tq = s * 4; tq < TCH; tq += 4 * S) {
         R x1[4][4], x2[4][4], h[4][4];
@@ -114,8 +158,8 @@ __global__ void __launch_bounds__(256) k_wstats(const R* __restrict__ phi, const
     __syncthreads();
   }
   // fixed-order reduction over the S slices (staging area reused)
-  R* red = p1s;
-  R* red2 = p1s + FT * KB;
+  R* red = stage0;
+  R* red2 = stage0 + FT * KB;
   for (int ss = 0; ss < S; ++ss) {
     if (s == ss) {
 #pragma unroll
@@ -184,7 +228,7 @@ template <typename R, int KB> struct HsCfg {
   static constexpr int LDW = KB + 4, LDP = TT + 4;
   static constexpr int STAGE = FCH * LDW + 2 * FCH * LDP;
   static constexpr int RED = 2 * KB * TT;
-  static constexpr size_t bytes = sizeof(R) * (STAGE > RED ? STAGE : RED);
+  static constexpr size_t bytes = sizeof(R) * (2 * STAGE > RED ? 2 * STAGE : RED);
 };
 
 template <typename R, int KB>
@@ -197,9 +241,7 @@ __global__ void __launch_bounds__(256) k_hstats(const R* __restrict__ phi, const
   constexpr int TT = Cf::TT, FCH = Cf::FCH, NTH = Cf::NTH, S = Cf::S;
   constexpr int LDW = Cf::LDW, LDP = Cf::LDP;
   extern __shared__ __align__(16) unsigned char smraw[];
-  R* ws = reinterpret_cast<R*>(smraw);
-  R* p1s = ws + FCH * LDW;
-  R* p2s = p1s + FCH * LDP;
+  R* stage0 = reinterpret_cast<R*>(smraw);
   __shared__ int is_last;
   const int bn = blockIdx.z, fs = blockIdx.y, ttile = blockIdx.x;
   const int t0 = ttile * TT;
@@ -213,23 +255,53 @@ __global__ void __launch_bounds__(256) k_hstats(const R* __restrict__ phi, const
   const R* Wn = W + (size_t)bn * F * K;
   const int fper = (F + FS - 1) / FS;
   const int fa = fs * fper, fb = min(F, fa + fper);
+  const bool async = sizeof(R) == 4 && (T % 4) == 0;
+  auto stage = [&](int st) { return stage0 + st * Cf::STAGE; };
+  auto load = [&](int st, int c0) {
+    R* ws = stage(st);
+    R* p1s = ws + FCH * LDW;
+    R* p2s = p1s + FCH * LDP;
+    for (int e = tid; e < FCH * KB; e += 256) {
+      const int fl = e / KB, k = e % KB, f = c0 + fl;
+      ws[fl * LDW + k] = (f < fb && k < K) ? Wn[(size_t)f * K + k] : R(0);
+    }
+    if (async) {
+      constexpr int Q = TT / 4;
+      for (int e = tid; e < FCH * Q; e += 256) {
+        const int fl = e / Q, q = e % Q, f = c0 + fl, t = t0 + 4 * q;
+        const bool v = f < fb && t < T;
+        const size_t off = v ? (size_t)f * T + t : 0;
+        cp_async16(p1s + fl * LDP + 4 * q, P1 + off, v);
+        cp_async16(p2s + fl * LDP + 4 * q, P2 + off, v);
+      }
+    } else {
+      for (int e = tid; e < FCH * TT; e += 256) {
+        const int fl = e / TT, tl = e % TT, f = c0 + fl, t = t0 + tl;
+        const bool v = f < fb && t < T;
+        p1s[fl * LDP + tl] = v ? P1[(size_t)f * T + t] : R(0);
+        p2s[fl * LDP + tl] = v ? P2[(size_t)f * T + t] : R(0);
+      }
+    }
+    cp_async_commit();
+  };
   R a1[4][4], a2[4][4];
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j) a1[i][j] = a2[i][j] = 0;
-  for (int c0 = fa; c0 < fb; c0 += FCH) {
-    for (int e = tid; e < FCH * KB; e += 256) {
-      const int fl = e / KB, k = e % KB, f = c0 + fl;
-      ws[fl * LDW + k] = (f < fb && k < K) ? Wn[(size_t)f * K + k] : R(0);
-    }
-    for (int e = tid; e < FCH * TT; e += 256) {
-      const int fl = e / TT, tl = e % TT, f = c0 + fl, t = t0 + tl;
-      const bool v = f < fb && t < T;
-      p1s[fl * LDP + tl] = v ? P1[(size_t)f * T + t] : R(0);
-      p2s[fl * LDP + tl] = v ? P2[(size_t)f * T + t] : R(0);
+  int st = 0;
+  if (fa < fb) load(0, fa);
+  for (int c0 = fa; c0 < fb; c0 += FCH, st ^= 1) {
+    if (c0 + FCH < fb) {
+      load(st ^ 1, c0 + FCH);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
     }
     __syncthreads();
+    const R* ws = stage(st);
+    const R* p1s = ws + FCH * LDW;
+    const R* p2s = p1s + FCH * LDP;
     if (s < S) {
       const int fe = min(FCH, fb - c0);
       for (int fl = s; fl < fe; fl += S) {
@@ -249,8 +321,8 @@ __global__ void __launch_bounds__(256) k_hstats(const R* __restrict__ phi, const
     __syncthreads();
   }
   // fixed-order slice reduction into smem (KB x TT each; staging area reused)
-  R* red = ws;
-  R* red2 = ws + KB * TT;
+  R* red = stage0;
+  R* red2 = stage0 + KB * TT;
   for (int ss = 0; ss < S; ++ss) {
     if (s == ss) {
 #pragma unroll
@@ -314,7 +386,13 @@ __global__ void __launch_bounds__(256) k_hstats(const R* __restrict__ phi, const
 // and the data term sum_m (-x~/y - log y)  (_kernels.py:226-243).
 // Loops over sources exit early (uniform branch) instead of predicating.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ float rcp_r(float y) { return __frcp_rn(y); }
+// 1/y: MUFU.RCP (rcp.approx, <= 1 ulp) in fp32 -- the IEEE __frcp_rn sequence
+// with its slow path cost ~50 instructions per call in the streaming loops
+__device__ __forceinline__ float rcp_r(float y) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(y));
+  return r;
+}
 __device__ __forceinline__ double rcp_r(double y) { return 1.0 / y; }
 
 template <typename R, int M>

@@ -59,13 +59,9 @@ template <typename R> struct FrontArgs {
   R* W;
   const R* lam;
   const R* floorp;
-  R* cs_out;        // (B, F, NMAX) gain-normalisation factors folded into W
-  double* ld_part;  // (B, F) log|det Q_f|
-  const unsigned* iter;
-  unsigned long long* status;
+  double2* V;       // (B, F, M, M, M) weighted covariances for k_ip
   int F, T, N, K;
-  long long f_offset;
-  int normalize, ip_sweeps;
+  long long* timing;  // optional (F, 8) clock64 stamps per phase (profiling builds/tools)
 };
 
 template <typename R, int M> struct FrontSmem {
@@ -95,25 +91,15 @@ template <typename R, int M> struct FrontSmem {
 };
 
 template <typename R, int M>
-__global__ void __launch_bounds__(FrCfg<M>::BS, (M <= 8 ? 3 : 1)) k_front(FrontArgs<R> a) {
+__global__ void __launch_bounds__(FrCfg<M>::BS, (M <= 8 ? 2 : 1)) k_front(FrontArgs<R> a) {
   using C = cplx<R>;
   using L = FrontSmem<R, M>;
   constexpr int BS = FrCfg<M>::BS, TC = FrCfg<M>::TC, P = FrCfg<M>::P, S2 = FrCfg<M>::S2;
   constexpr int NW = BS / 32;
   extern __shared__ __align__(16) unsigned char sm[];
   R* gs = reinterpret_cast<R*>(sm + L::o_gs);
-  R* cs = reinterpret_cast<R*>(sm + L::o_cs);
-  double* rown = reinterpret_cast<double*>(sm + L::o_rown);
   int* pairs = reinterpret_cast<int*>(sm + L::o_pairs);
   R* redw = reinterpret_cast<R*>(sm + L::o_redw);
-  double* misc = reinterpret_cast<double*>(sm + L::o_misc);
-  int* vfail = reinterpret_cast<int*>(misc + 8);
-  int* flags = vfail + M;
-  double2* Qd = reinterpret_cast<double2*>(sm + L::o_Qd);
-  double2* Ai = reinterpret_cast<double2*>(sm + L::o_Ai);
-  double2* ub = reinterpret_cast<double2*>(sm + L::o_vec);
-  double2* qb = ub + M;
-  double2* sk = qb + M;
   unsigned char* un = sm + L::o_union;
   R* lamc = reinterpret_cast<R*>(un + L::s_lam);
   R* iys = reinterpret_cast<R*>(un + L::s_iy);
@@ -128,16 +114,14 @@ __global__ void __launch_bounds__(FrCfg<M>::BS, (M <= 8 ? 3 : 1)) k_front(FrontA
   const C* X = a.X + ((size_t)b * F + f) * T * M;
   const R* xt = a.xt + ((size_t)b * F + f) * T * M;
   const R* lam = a.lam + (size_t)b * N * FT + (size_t)f * T;
-  C* Qg = a.Q + ((size_t)b * F + f) * M * M;
   R* gg = a.g + (size_t)b * N * F * M + (size_t)f * M;
-  R* Wg = a.W + (size_t)b * N * F * K + (size_t)f * K;
   const R fl = a.floorp[b];
-  const unsigned it = *a.iter;
-  const long long fglob = a.f_offset + f;
+  long long* tstamp = (a.timing && b == 0) ? a.timing + (size_t)f * 8 : nullptr;
+#define FM_STAMP(i) \
+  if (tstamp && tid == 0) tstamp[i] = clock64();
+  FM_STAMP(0);
 
   for (int e = tid; e < N * M; e += BS) gs[e] = gg[(size_t)(e / M) * F * M + (e % M)];
-  for (int e = tid; e < M * M; e += BS) Qd[e] = to_d2(Qg[e]);
-  if (tid < NMAX) cs[tid] = R(1);
   if (tid == 0) {
     int p = 0;
     for (int i = 0; i < M; ++i)
@@ -146,7 +130,6 @@ __global__ void __launch_bounds__(FrCfg<M>::BS, (M <= 8 ? 3 : 1)) k_front(FrontA
         pairs[2 * p + 1] = j;
         ++p;
       }
-    flags[0] = 0;
   }
   __syncthreads();
 
@@ -159,20 +142,34 @@ __global__ void __launch_bounds__(FrCfg<M>::BS, (M <= 8 ? 3 : 1)) k_front(FrontA
     R num[M], den[M];
 #pragma unroll
     for (int m = 0; m < M; ++m) num[m] = den[m] = 0;
+    // register prefetch of the next chunk's lambda and x~ (one t per thread)
+    R lp[NMAX], xp[M];
+    auto fetchA1 = [&](int t0) {
+      const int t = t0 + tid;
+      const int tc = t < T ? t : T - 1;
+#pragma unroll
+      for (int n = 0; n < NMAX; ++n) {
+        lp[n] = R(0);
+        if (n >= N) break;
+        lp[n] = lam[(size_t)n * FT + tc];
+      }
+      RowIO<R, M>::load(xt + (size_t)tc * M, xp);
+    };
+    if (tid < TC) fetchA1(0);
     for (int t0 = 0; t0 < T; t0 += TC) {
-      for (int tl = tid; tl < TC; tl += BS) {
-        const int t = t0 + tl;
-        const int tc = t < T ? t : T - 1;
-        R l[NMAX];
+      if (tid < TC) {
+        const int tl = tid, t = t0 + tl;
+        R l[NMAX], x[M];
+#pragma unroll
+        for (int n = 0; n < NMAX; ++n) l[n] = t < T ? lp[n] : R(0);
+#pragma unroll
+        for (int m = 0; m < M; ++m) x[m] = xp[m];
+        if (t0 + TC < T) fetchA1(t0 + TC);
 #pragma unroll
         for (int n = 0; n < NMAX; ++n) {
-          l[n] = R(0);
           if (n >= N) break;
-          l[n] = t < T ? lam[(size_t)n * FT + tc] : R(0);
           lamc[n * (TC + 1) + tl] = l[n];
         }
-        R x[M];
-        RowIO<R, M>::load(xt + (size_t)tc * M, x);
         R iy[M], y[M], xr[M];
         model_power<R, M>(l, gs, N, fl, iy, y);
 #pragma unroll
@@ -224,6 +221,7 @@ __global__ void __launch_bounds__(FrCfg<M>::BS, (M <= 8 ? 3 : 1)) k_front(FrontA
     __syncthreads();
   }
 
+  FM_STAMP(1);
   // ---- A2: V_fm accumulation ------------------------------------------------
   {
     const int p = tid % P, s2 = tid / P;
@@ -232,37 +230,62 @@ __global__ void __launch_bounds__(FrCfg<M>::BS, (M <= 8 ? 3 : 1)) k_front(FrontA
     C v[M];  // (re, im) of V[m][pi][pj]
 #pragma unroll
     for (int m = 0; m < M; ++m) v[m] = cmake<C>(0.0, 0.0);
-    for (int t0 = 0; t0 < T; t0 += TC) {
-      for (int tl = tid; tl < TC; tl += BS) {
-        const int t = t0 + tl;
-        const int tc = t < T ? t : T - 1;
-        R l[NMAX];
+    R lp[NMAX];
+    C xp[M];
+    auto fetchA2 = [&](int t0) {
+      const int t = t0 + tid;
+      const int tc = t < T ? t : T - 1;
 #pragma unroll
-        for (int n = 0; n < NMAX; ++n) {
-          l[n] = R(0);
-          if (n >= N) break;
-          l[n] = lam[(size_t)n * FT + tc];
-        }
+      for (int n = 0; n < NMAX; ++n) {
+        lp[n] = R(0);
+        if (n >= N) break;
+        lp[n] = lam[(size_t)n * FT + tc];
+      }
+      CRowIO<R, M>::load(X + (size_t)tc * M, xp);
+    };
+    if (tid < TC) fetchA2(0);
+    for (int t0 = 0; t0 < T; t0 += TC) {
+      if (tid < TC) {
+        const int tl = tid, t = t0 + tl;
+        R l[NMAX];
+        C xv[M];
+#pragma unroll
+        for (int n = 0; n < NMAX; ++n) l[n] = lp[n];
+#pragma unroll
+        for (int m = 0; m < M; ++m) xv[m] = t < T ? xp[m] : cmake<C>(0.0, 0.0);
+        if (t0 + TC < T) fetchA2(t0 + TC);
         R iy[M], y[M];
         model_power<R, M>(l, gs, N, fl, iy, y);
 #pragma unroll
         for (int m = 0; m < M; ++m)
           if (t >= T) iy[m] = R(0);
         RowIO<R, M>::store(iys + tl * M, iy);
-        C xv[M];
-        if (t < T) {
-          CRowIO<R, M>::load(X + (size_t)t * M, xv);
-        } else {
-#pragma unroll
-          for (int m = 0; m < M; ++m) xv[m] = cmake<C>(0.0, 0.0);
-        }
         CRowIO<R, M>::store(Xc + tl * M, xv);
       }
       __syncthreads();
       if (act) {
-        for (int tl = s2; tl < TC; tl += S2) {
+        // two t per trip: both rows' loads are in flight before the FMAs
+        int tl = s2;
+        for (; tl + S2 < TC; tl += 2 * S2) {
+          const C xi0 = Xc[tl * M + pi], xj0 = Xc[tl * M + pj];
+          const C xi1 = Xc[(tl + S2) * M + pi], xj1 = Xc[(tl + S2) * M + pj];
+          R iy0[M], iy1[M];
+          RowIO<R, M>::load(iys + tl * M, iy0);
+          RowIO<R, M>::load(iys + (tl + S2) * M, iy1);
+          C p0, p1;  // x_i conj(x_j)
+          p0.x = xi0.x * xj0.x + xi0.y * xj0.y;
+          p0.y = xi0.y * xj0.x - xi0.x * xj0.y;
+          p1.x = xi1.x * xj1.x + xi1.y * xj1.y;
+          p1.y = xi1.y * xj1.x - xi1.x * xj1.y;
+#pragma unroll
+          for (int m = 0; m < M; ++m) {
+            v[m] = fma2(cmake<C>(iy0[m], iy0[m]), p0, v[m]);
+            v[m] = fma2(cmake<C>(iy1[m], iy1[m]), p1, v[m]);
+          }
+        }
+        if (tl < TC) {
           const C xi = Xc[tl * M + pi], xj = Xc[tl * M + pj];
-          C pr;  // x_i conj(x_j)
+          C pr;
           pr.x = xi.x * xj.x + xi.y * xj.y;
           pr.y = xi.y * xj.x - xi.x * xj.y;
           R iy[M];
@@ -297,6 +320,87 @@ __global__ void __launch_bounds__(FrCfg<M>::BS, (M <= 8 ? 3 : 1)) k_front(FrontA
     __syncthreads();
   }
 
+  // publish the updated gains and V_f (fp64) for k_ip
+  {
+    double2* Vg = a.V + ((size_t)b * F + f) * M * M * M;
+    for (int e = tid; e < M * M * M; e += BS) Vg[e] = Vd[e];
+    for (int e = tid; e < N * M; e += BS) gg[(size_t)(e / M) * F * M + (e % M)] = gs[e];
+  }
+  FM_STAMP(2);
+#undef FM_STAMP
+}
+
+// ---------------------------------------------------------------------------
+// k_ip: iterative projection + normalisations, one small CTA per (f, b):
+// warp 0 inverts [Q | I] (pivoted Gauss-Jordan; also log|det Q|) while warps
+// 1.. invert the HPD V_fm in parallel; warp 0 then runs the M sequential row
+// updates (one mat-vec each); all threads normalise and fold into W.
+// ---------------------------------------------------------------------------
+template <typename R> struct IpArgs {
+  const double2* V;  // (B, F, M, M, M) from k_front
+  cplx<R>* Q;
+  R* g;
+  R* W;
+  R* cs_out;
+  double* ld_part;
+  const unsigned* iter;
+  unsigned long long* status;
+  int F, N, K;
+  long long f_offset;
+  int normalize, ip_sweeps;
+};
+
+template <int M> struct IpCfg {
+  static constexpr int NW = (M < 8 ? M : 8) + 1;  // warp 0 + HPD-inversion warps
+  static constexpr int BS = 32 * NW;
+};
+
+template <typename R, int M> struct IpSmem {
+  static constexpr size_t al(size_t x) { return (x + 15) & ~size_t(15); }
+  static constexpr size_t o_Vd = 0;
+  static constexpr size_t o_Qd = o_Vd + al(sizeof(double2) * M * M * M);
+  static constexpr size_t o_Ai = o_Qd + al(sizeof(double2) * M * M);
+  static constexpr size_t o_vec = o_Ai + al(sizeof(double2) * M * 2 * M);
+  static constexpr size_t o_gs = o_vec + al(sizeof(double2) * 3 * M);
+  static constexpr size_t o_cs = o_gs + al(sizeof(R) * NMAX * M);
+  static constexpr size_t o_rown = o_cs + al(sizeof(R) * NMAX);
+  static constexpr size_t o_misc = o_rown + al(sizeof(double) * M);
+  static constexpr size_t bytes = o_misc + al(sizeof(double) * 8 + sizeof(int) * (M + 8));
+};
+
+template <typename R, int M>
+__global__ void __launch_bounds__(IpCfg<M>::BS) k_ip(IpArgs<R> a) {
+  using C = cplx<R>;
+  using L = IpSmem<R, M>;
+  constexpr int NW = IpCfg<M>::NW, BS = IpCfg<M>::BS;
+  extern __shared__ __align__(16) unsigned char sm[];
+  double2* Vd = reinterpret_cast<double2*>(sm + L::o_Vd);
+  double2* Qd = reinterpret_cast<double2*>(sm + L::o_Qd);
+  double2* Ai = reinterpret_cast<double2*>(sm + L::o_Ai);
+  double2* ub = reinterpret_cast<double2*>(sm + L::o_vec);
+  double2* qb = ub + M;
+  double2* sk = qb + M;
+  R* gs = reinterpret_cast<R*>(sm + L::o_gs);
+  R* cs = reinterpret_cast<R*>(sm + L::o_cs);
+  double* rown = reinterpret_cast<double*>(sm + L::o_rown);
+  double* misc = reinterpret_cast<double*>(sm + L::o_misc);
+  int* vfail = reinterpret_cast<int*>(misc + 8);
+  int* flags = vfail + M;
+  const int f = blockIdx.x, b = blockIdx.y;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int N = a.N, F = a.F, K = a.K;
+  C* Qg = a.Q + ((size_t)b * F + f) * M * M;
+  R* gg = a.g + (size_t)b * N * F * M + (size_t)f * M;
+  R* Wg = a.W + (size_t)b * N * F * K + (size_t)f * K;
+  const unsigned it = *a.iter;
+  const long long fglob = a.f_offset + f;
+  const double2* Vg = a.V + ((size_t)b * F + f) * M * M * M;
+  for (int e = tid; e < M * M * M; e += BS) Vd[e] = Vg[e];
+  for (int e = tid; e < M * M; e += BS) Qd[e] = to_d2(Qg[e]);
+  for (int e = tid; e < N * M; e += BS) gs[e] = gg[(size_t)(e / M) * F * M + (e % M)];
+  if (tid < NMAX) cs[tid] = R(1);
+  if (tid == 0) flags[0] = flags[1] = 0;
+  __syncthreads();
   // ---- A3: iterative projection (spatial.py:181-199) -------------------------
   {
     if (warp == 0) {
@@ -313,13 +417,13 @@ __global__ void __launch_bounds__(FrCfg<M>::BS, (M <= 8 ? 3 : 1)) k_front(FrontA
         flags[0] = ok ? 0 : 1;
       }
     }
-    for (int m = warp; m < M; m += NW) {
+    for (int m = warp - 1; warp > 0 && m < M; m += NW - 1) {
       const bool ok = warp_inv_hpd<M>(Vd + (size_t)m * M * M, lane);
       if (lane == 0) vfail[m] = ok ? 0 : 1;
     }
     __syncthreads();
     if (warp == 0) {
-      double ldet = misc[0];
+      double ldet = misc[0], nprod = 1.0;
       int code = flags[0] ? 2 : 0, bad_m = 0;  // singular Q -> singular Q V at m = 0
       for (int sw = 0; sw < a.ip_sweeps && code == 0; ++sw) {
         for (int m = 0; m < M; ++m) {
@@ -345,19 +449,19 @@ __global__ void __launch_bounds__(FrCfg<M>::BS, (M <= 8 ? 3 : 1)) k_front(FrontA
             bad_m = m;
             break;
           }
-          const double sn = sqrt(nrm);
+          const double isn = rsqrt(nrm);  // 1 / sqrt(norm)
           if (lane < M) {  // new row r = conj(q / sqrt(norm))  (spatial.py:199)
-            const double2 r = make_double2(q.x / sn, -(q.y / sn));
+            const double2 r = make_double2(q.x * isn, -(q.y * isn));
             qb[lane] = r;
             Qd[m * M + lane] = r;
           }
           __syncwarp();
-          if (lane < M) {  // s = r Q^-1 - e_m^T
+          if (lane < M) {  // s = (r Q^-1 - e_m^T) / sqrt(norm)
             double2 s = make_double2(0.0, 0.0);
 #pragma unroll
             for (int j = 0; j < M; ++j) s = cadd(s, cmul(qb[j], Ai[j * 2 * M + M + lane]));
             if (lane == m) s.x -= 1.0;
-            sk[lane] = make_double2(s.x / sn, s.y / sn);
+            sk[lane] = make_double2(s.x * isn, s.y * isn);
           }
           __syncwarp();
           for (int e = lane; e < M * M; e += 32) {  // Q^-1 -= u s / sqrt(norm)
@@ -365,7 +469,11 @@ __global__ void __launch_bounds__(FrCfg<M>::BS, (M <= 8 ? 3 : 1)) k_front(FrontA
             double2* d = Ai + i * 2 * M + M + k;
             *d = csub(*d, cmul(ub[i], sk[k]));
           }
-          ldet += 0.5 * log(nrm);
+          nprod *= nrm;  // log|det Q| += log sqrt(norm) (determinant lemma)
+          if (nprod > 1e150 || nprod < 1e-150) {
+            ldet += 0.5 * log(nprod);
+            nprod = 1.0;
+          }
           __syncwarp();
         }
       }
@@ -374,7 +482,7 @@ __global__ void __launch_bounds__(FrCfg<M>::BS, (M <= 8 ? 3 : 1)) k_front(FrontA
           report_status(a.status, it, bad_m, fglob, code);
           flags[1] = 1;
         }
-        misc[1] = ldet;
+        misc[1] = ldet + 0.5 * log(nprod);
       }
     }
     __syncthreads();
@@ -429,6 +537,7 @@ __global__ void __launch_bounds__(FrCfg<M>::BS, (M <= 8 ? 3 : 1)) k_front(FrontA
   if (tid == 0) a.ld_part[(size_t)b * F + f] = misc[1];
 }
 
+
 // ---------------------------------------------------------------------------
 template <typename R> struct BackArgs {
   const cplx<R>* X;
@@ -449,7 +558,7 @@ template <typename R> struct BackArgs {
 };
 
 template <typename R, int M>
-__global__ void __launch_bounds__(256, 3) k_back(BackArgs<R> a) {
+__global__ void __launch_bounds__(256, 2) k_back(BackArgs<R> a) {
   using C = cplx<R>;
   __shared__ C Qr[M * M];
   __shared__ __align__(16) R gs[NMAX * M];
@@ -471,19 +580,30 @@ __global__ void __launch_bounds__(256, 3) k_back(BackArgs<R> a) {
   if (tid < NMAX) cs[tid] = a.cs ? a.cs[((size_t)b * F + f) * NMAX + tid] : R(1);
   __syncthreads();
   double ll = 0.0;
+  // register prefetch of the next step's x row and lambda values
+  C xp[M];
+  R lp[NMAX];
+  auto fetch = [&](int t) {
+    CRowIO<R, M>::load(X + (size_t)t * M, xp);
+#pragma unroll
+    for (int n = 0; n < NMAX; ++n) {
+      lp[n] = R(0);
+      if (n >= N) break;
+      lp[n] = lam[(size_t)n * FT + t];
+    }
+  };
+  if (tid < T) fetch(tid);
   for (int t = tid; t < T; t += 256) {
     // compiler barrier: re-read the (broadcast) shared-memory parameters each
     // step instead of hoisting M*M + N*M of them into registers
     asm volatile("" ::: "memory");
     C xv[M];
-    CRowIO<R, M>::load(X + (size_t)t * M, xv);
     R l[NMAX];
 #pragma unroll
-    for (int n = 0; n < NMAX; ++n) {
-      l[n] = R(0);
-      if (n >= N) break;
-      l[n] = lam[(size_t)n * FT + t] * cs[n];
-    }
+    for (int m = 0; m < M; ++m) xv[m] = xp[m];
+#pragma unroll
+    for (int n = 0; n < NMAX; ++n) l[n] = lp[n] * cs[n];
+    if (t + 256 < T) fetch(t + 256);
     R xtv[M];
 #pragma unroll
     for (int i = 0; i < M; ++i) {
