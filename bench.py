@@ -297,12 +297,12 @@ def main():
     iters_per_s = iters / (ms_per_step / 1e3)
 
     # ---- roofline of the dominant kernel: per-kernel CUDA events on the launch stream
-    names = ["k_wstats", "k_lambda(W)", "k_phi", "k_hstats", "k_lambda(H)", "k_front", "k_ip",
-             "k_back"]
-    acc = np.zeros(8)
+    names = ["k_wstats", "k_lambda(W)", "k_phi", "k_hstats", "k_lambda(H)", "k_gain", "k_vacc",
+             "k_ip", "k_back"]
+    acc = np.zeros(9)
     nprof = 10
     if not sharded_f:
-        ms = (ctypes.c_float * 8)()
+        ms = (ctypes.c_float * 9)()
         for _ in range(nprof):
             _lib.check(lib.fm_iterate_profiled(ctypes.byref(loop.dims), ctypes.byref(loop.state), ms,
                                                _lib.stream_ptr()), "fm_iterate_profiled")
@@ -314,8 +314,9 @@ def main():
     ftm = F * T * M * Bl if not sharded_f else (loop.F * T * M)
     # algorithmic bytes per launch
     alg = {
-        "k_front": ftm * (rs + 2 * rs),                    # read xt (gain stats), read X (V)
-        "k_back": ftm * (2 * rs + rs),                     # read X, write xt
+        "k_gain": ftm * rs + N * (ftm // M) * rs,          # read xt, lambda
+        "k_vacc": ftm * 2 * rs + N * (ftm // M) * rs,      # read X, lambda
+        "k_back": ftm * (2 * rs + rs) + 3 * N * (ftm // M) * rs,  # read X, lambda; write xt, phi
         "k_hstats": 2 * N * (ftm // M) * rs,               # read phi1, phi2
         "k_wstats": 2 * N * (ftm // M) * rs,               # read phi1, phi2
         "k_phi": ftm * rs + 3 * N * (ftm // M) * rs,       # read xt, lambda; write phi
@@ -359,7 +360,7 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline and args.config in ("c1", "c0"):
         cpu = cpu_baseline_sample(cfg)
 
-    launches = args.steps * (2 + 8 * iters)
+    launches = args.steps * (2 + (10 if cfg['B'] == 1 else 11) * iters)
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,

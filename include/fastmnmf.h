@@ -127,7 +127,7 @@ int fm_nmf_lambda(const fm_dims* d, const void* W, const void* H, void* lam, voi
  * the first statistics pass of iteration 0 (separate.py:183, :186-193). */
 int fm_prologue(const fm_dims* d, const fm_state* s, void* stream);
 
-/* One full iteration (separate.py:201-234) on one process: eight launches. Appends
+/* One full iteration (separate.py:201-234) on one process: nine launches. Appends
  * trace[i] (i = number of previous fm_iterate calls since fm_prologue) =
  * data term + 2T sum_f log|det Q_f| of the state after this iteration. */
 int fm_iterate(const fm_dims* d, const fm_state* s, void* stream);
@@ -140,9 +140,10 @@ int fm_iterate(const fm_dims* d, const fm_state* s, void* stream);
 int fm_iterate_phase(const fm_dims* d, const fm_state* s, int phase, void* hstat,
                      void* stream);
 
-/* fm_iterate with CUDA events recorded between its eight launches on `stream`
- * (synchronises): ms_host[0..7] = device ms of k_wstats, k_lambda, k_phi,
- * k_hstats, k_lambda, k_front, k_ip, k_back. Used by bench.py for the roofline. */
+/* fm_iterate with CUDA events recorded between its nine launches on `stream`
+ * (synchronises): ms_host[0..8] = device ms of k_wstats, k_lambda, k_phi,
+ * k_hstats, k_lambda, k_gain, k_vacc, k_ip, k_back. Used by bench.py for the
+ * per-kernel roofline. */
 int fm_iterate_profiled(const fm_dims* d, const fm_state* s, float* ms_host, void* stream);
 
 /* n fm_iterate calls, optionally captured once into a CUDA graph that is
@@ -159,10 +160,6 @@ int fm_run(const fm_dims* d, const fm_state* s, int n_iterations, int use_graph,
 int fm_observation_stats(const fm_dims* d, const void* X, double* sumsq_host,
                          double* maxsq_host, void* stream);
 int fm_scale_observation(const fm_dims* d, void* X, const double* scale_host, void* stream);
-
-/* Profiling hook: k_front phase clock64() stamps (F x 8 int64 device buffer,
- * mixture 0) or NULL to disable. Used by tools/phase_timing.py. */
-int fm_debug_front_timing(long long* buf);
 
 const char* fm_last_error(void);
 int fm_version(void);

@@ -10,7 +10,7 @@ extern template struct fm::Impl<double>;
 namespace fm {
 
 static thread_local char g_err[512] = "";
-long long* g_front_timing = nullptr;
+
 
 void set_error(const char* fmt, ...) {
   va_list ap;
@@ -58,15 +58,8 @@ using namespace fm;
 extern "C" {
 
 const char* fm_last_error(void) { return g_err; }
-
-/* Profiling hook (not part of the drop-in surface): when buf != NULL, k_front
- * writes clock64() stamps at its phase boundaries for mixture 0 into buf
- * (F x 8 int64, device). Pass NULL to switch off. */
-int fm_debug_front_timing(long long* buf) {
-  g_front_timing = buf;
-  return FM_OK;
-}
 int fm_version(void) { return 1; }
+
 
 int fm_fast_stats(int dtype, int64_t F, int64_t T, int64_t M, int64_t N, const void* xt,
                   const void* g, const void* lam, double floor, int want_gain, int want_phi,
@@ -145,15 +138,15 @@ int fm_iterate_phase(const fm_dims* d, const fm_state* s, int phase, void* hstat
 int fm_iterate_profiled(const fm_dims* d, const fm_state* s, float* ms_host, void* stream) {
   if (int rc = validate_dims(d)) return rc;
   cudaStream_t st = (cudaStream_t)stream;
-  cudaEvent_t ev[9];
-  for (int i = 0; i < 9; ++i) FM_CUDA(cudaEventCreate(&ev[i]));
+  cudaEvent_t ev[10];
+  for (int i = 0; i < 10; ++i) FM_CUDA(cudaEventCreate(&ev[i]));
   int rc = d->dtype == FM_F64 ? Impl<double>::iterate_phase(d, s, 2, nullptr, st, ev)
                               : Impl<float>::iterate_phase(d, s, 2, nullptr, st, ev);
   if (rc == FM_OK) {
-    FM_CUDA(cudaEventSynchronize(ev[8]));
-    for (int i = 0; i < 8; ++i) FM_CUDA(cudaEventElapsedTime(&ms_host[i], ev[i], ev[i + 1]));
+    FM_CUDA(cudaEventSynchronize(ev[9]));
+    for (int i = 0; i < 9; ++i) FM_CUDA(cudaEventElapsedTime(&ms_host[i], ev[i], ev[i + 1]));
   }
-  for (int i = 0; i < 9; ++i) cudaEventDestroy(ev[i]);
+  for (int i = 0; i < 10; ++i) cudaEventDestroy(ev[i]);
   return rc;
 }
 

@@ -54,9 +54,24 @@ __device__ __forceinline__ double2 cdiv(double2 a, double2 b) {
   }
 }
 __device__ __forceinline__ double cabs1(double2 a) { return fabs(a.x) + fabs(a.y); }
-// 1/p as conj(p)/|p|^2: one fp64 division (pivots here are well scaled)
+// fp64 1/x and 1/sqrt(x) from the fp32 MUFU estimate + two Newton steps
+// (error 1e-7 -> 1e-14 -> ~1 ulp); x must be a normal fp32-range value,
+// which holds for the pivots and norms they are used on.
+__device__ __forceinline__ double drcp(double x) {
+  double r = (double)__frcp_rn((float)x);
+  r = r * fma(-x, r, 2.0);
+  r = r * fma(-x, r, 2.0);
+  return r;
+}
+__device__ __forceinline__ double drsqrt(double x) {
+  double r = (double)rsqrtf((float)x);
+  r = r * fma(-0.5 * x * r, r, 1.5);
+  r = r * fma(-0.5 * x * r, r, 1.5);
+  return r;
+}
+// 1/p as conj(p)/|p|^2
 __device__ __forceinline__ double2 crcp(double2 p) {
-  const double inv = 1.0 / (p.x * p.x + p.y * p.y);
+  const double inv = drcp(p.x * p.x + p.y * p.y);
   return make_double2(p.x * inv, -p.y * inv);
 }
 __device__ __forceinline__ double2 to_d2(float2 a) { return make_double2(a.x, a.y); }

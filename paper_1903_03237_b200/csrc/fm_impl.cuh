@@ -17,8 +17,7 @@
 namespace fm {
 
 void set_error(const char* fmt, ...);
-// device buffer for k_front phase stamps (fm_debug_front_timing); null = off
-extern long long* g_front_timing;
+
 
 #define FM_CHECK_LAUNCH(what)                                                   \
   do {                                                                          \
@@ -73,7 +72,7 @@ inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 // Workspace plan for the fused iteration.
 struct Plan {
   int TS, FS, nft, ntt;  // split counts of k_wstats / k_hstats, their tile counts
-  size_t off_lam, off_phi, off_part, off_llp, off_ldp, off_cs, off_V, off_cnt, off_tiles, total;
+  size_t off_lam, off_phi, off_part, off_llp, off_ldp, off_cs, off_V, off_cnt, off_tiles, off_fcnt, total;
 };
 
 inline Plan make_plan(const fm_dims* d) {
@@ -89,16 +88,20 @@ inline Plan make_plan(const fm_dims* d) {
   p.FS = (int)std::max<long long>(1, std::min<long long>(fs, (F + 31) / 32));
   const size_t partw = (size_t)B * N * p.TS * 2 * F * K;
   const size_t parth = (size_t)B * N * p.FS * 2 * K * T;
+  const long long M = d->M, tiles64 = (T + 63) / 64;  // k_gain/k_vacc tiles >= 64 frames
+  const size_t partg = (size_t)B * F * tiles64 * N * 2 * M;
+  const size_t partv = (size_t)B * F * tiles64 * M * (M * (M + 1) / 2) * 2;
   size_t o = 0;
   p.off_lam = o; o = align256(o + (size_t)B * N * F * T * rs);
   p.off_phi = o; o = align256(o + (size_t)B * 2 * N * F * T * rs);
-  p.off_part = o; o = align256(o + std::max(partw, parth) * rs);
-  p.off_llp = o; o = align256(o + (size_t)B * F * 8);
+  p.off_part = o; o = align256(o + std::max(std::max(partw, parth), std::max(partg, partv)) * rs);
+  p.off_llp = o; o = align256(o + (size_t)B * F * ((T + 255) / 256) * 8);
   p.off_ldp = o; o = align256(o + (size_t)B * F * 8);
   p.off_cs = o; o = align256(o + (size_t)B * F * NMAX * rs);
   p.off_V = o; o = align256(o + (size_t)B * F * d->M * d->M * d->M * sizeof(double2));
   p.off_cnt = o; o = align256(o + 64);
   p.off_tiles = o; o = align256(o + sizeof(unsigned) * (size_t)B * N * (p.nft + p.ntt));
+  p.off_fcnt = o; o = align256(o + sizeof(unsigned) * (size_t)B * F * 2);
   p.total = o;
   return p;
 }
@@ -110,9 +113,10 @@ template <typename R> struct Impl {
 
   static int prologue(const fm_dims* d, const fm_state* s, cudaStream_t st);
   static int iterate_phase(const fm_dims* d, const fm_state* s, int phase, void* hstat,
-                           cudaStream_t st, cudaEvent_t* ev = nullptr);  // ev: 9 events
+                           cudaStream_t st, cudaEvent_t* ev = nullptr);  // ev: 10 events
   static int lambda(const fm_dims* d, const R* W, const R* H, R* lam, cudaStream_t st);
-  static int front(const fm_dims* d, const fm_state* s, cudaStream_t st);
+  static int gain(const fm_dims* d, const fm_state* s, cudaStream_t st);
+  static int vacc(const fm_dims* d, const fm_state* s, cudaStream_t st);
   static int ip(const fm_dims* d, const fm_state* s, cudaStream_t st);
   static int back(const fm_dims* d, const fm_state* s, int tail_only, int record, cudaStream_t st);
 
@@ -157,26 +161,44 @@ int Impl<R>::lambda(const fm_dims* d, const R* W, const R* H, R* lam, cudaStream
 }
 
 template <typename R>
-int Impl<R>::front(const fm_dims* d, const fm_state* s, cudaStream_t st) {
+int Impl<R>::gain(const fm_dims* d, const fm_state* s, cudaStream_t st) {
   const Plan p = make_plan(d);
   unsigned char* w = reinterpret_cast<unsigned char*>(s->work);
-  FrontArgs<R> a;
-  a.X = reinterpret_cast<const C*>(s->X);
+  GainArgs<R> a;
   a.xt = reinterpret_cast<const R*>(s->xt);
-  a.Q = reinterpret_cast<C*>(s->Q);
-  a.g = reinterpret_cast<R*>(s->g);
-  a.W = reinterpret_cast<R*>(s->W);
   a.lam = reinterpret_cast<const R*>(w + p.off_lam);
+  a.g = reinterpret_cast<R*>(s->g);
   a.floorp = reinterpret_cast<const R*>(s->floor);
-  a.V = reinterpret_cast<double2*>(w + p.off_V);
-  a.F = (int)d->F; a.T = (int)d->T; a.N = (int)d->N; a.K = (int)d->K;
-  a.timing = g_front_timing;
-  dim3 grid((unsigned)d->F, (unsigned)d->B);
+  a.part = reinterpret_cast<R*>(w + p.off_part);
+  a.counters = reinterpret_cast<unsigned*>(w + p.off_fcnt);
+  a.F = (int)d->F; a.T = (int)d->T; a.N = (int)d->N;
   FM_DISPATCH_M(d->M, {
-    const size_t sm = FrontSmem<R, MM>::bytes;
-    if (int rc = ensure_smem(k_front<R, MM>, sm)) return rc;
-    k_front<R, MM><<<grid, FrCfg<MM>::BS, sm, st>>>(a);
-    FM_CHECK_LAUNCH("k_front");
+    constexpr int TB = GaCfg<R, MM>::TB;
+    dim3 grid((unsigned)((d->T + TB - 1) / TB), (unsigned)d->F, (unsigned)d->B);
+    k_gain<R, MM><<<grid, 256, 0, st>>>(a);
+    FM_CHECK_LAUNCH("k_gain");
+  });
+  return FM_OK;
+}
+
+template <typename R>
+int Impl<R>::vacc(const fm_dims* d, const fm_state* s, cudaStream_t st) {
+  const Plan p = make_plan(d);
+  unsigned char* w = reinterpret_cast<unsigned char*>(s->work);
+  VaccArgs<R> a;
+  a.X = reinterpret_cast<const C*>(s->X);
+  a.lam = reinterpret_cast<const R*>(w + p.off_lam);
+  a.g = reinterpret_cast<const R*>(s->g);
+  a.floorp = reinterpret_cast<const R*>(s->floor);
+  a.part = reinterpret_cast<R*>(w + p.off_part);
+  a.counters = reinterpret_cast<unsigned*>(w + p.off_fcnt) + (size_t)d->B * d->F;
+  a.V = reinterpret_cast<double2*>(w + p.off_V);
+  a.F = (int)d->F; a.T = (int)d->T; a.N = (int)d->N;
+  FM_DISPATCH_M(d->M, {
+    constexpr int TB = VaCfg<R, MM>::TB;
+    dim3 grid((unsigned)((d->T + TB - 1) / TB), (unsigned)d->F, (unsigned)d->B);
+    k_vacc<R, MM><<<grid, VaCfg<R, MM>::BS, 0, st>>>(a);
+    FM_CHECK_LAUNCH("k_vacc");
   });
   return FM_OK;
 }
@@ -229,7 +251,7 @@ int Impl<R>::back(const fm_dims* d, const fm_state* s, int tail_only, int record
   a.iter = a.counter + 1;
   a.B = (int)d->B; a.F = (int)d->F; a.T = (int)d->T; a.N = (int)d->N;
   a.record = record && s->trace != nullptr;
-  dim3 grid((unsigned)d->F, (unsigned)d->B);
+  dim3 grid((unsigned)((d->T + 255) / 256), (unsigned)d->F, (unsigned)d->B);
   FM_DISPATCH_M(d->M, {
     k_back<R, MM><<<grid, 256, 0, st>>>(a);
     FM_CHECK_LAUNCH("k_back");
@@ -305,12 +327,26 @@ int Impl<R>::iterate_phase(const fm_dims* d, const fm_state* s, int phase, void*
   FM_EV(4);
   if (int rc = lambda(d, W, H, lam, st)) return rc;
   FM_EV(5);
-  if (int rc = front(d, s, st)) return rc;
+  if (int rc = gain(d, s, st)) return rc;
   FM_EV(6);
-  if (int rc = ip(d, s, st)) return rc;
+  if (int rc = vacc(d, s, st)) return rc;
   FM_EV(7);
-  if (int rc = back(d, s, /*tail_only=*/0, /*record=*/1, st)) return rc;
+  if (int rc = ip(d, s, st)) return rc;
   FM_EV(8);
+  if (int rc = back(d, s, /*tail_only=*/0, /*record=*/1, st)) return rc;
+  FM_EV(9);
+  {  // trace entry of this iteration, then advance the device iteration counter
+    const unsigned* cnt = reinterpret_cast<const unsigned*>(w + p.off_cnt);
+    unsigned* itp = const_cast<unsigned*>(cnt) + 1;
+    k_trace<<<(unsigned)d->B, 256, 0, st>>>(
+        reinterpret_cast<const double*>(w + p.off_llp), reinterpret_cast<const double*>(w + p.off_ldp),
+        s->trace, itp, (int)d->B, F, (T + 255) / 256, T);
+    FM_CHECK_LAUNCH("k_trace");
+    if (d->B > 1) {
+      k_iter_advance<<<1, 1, 0, st>>>(itp);
+      FM_CHECK_LAUNCH("k_iter_advance");
+    }
+  }
   return FM_OK;
 #undef FM_EV
 }

@@ -169,11 +169,15 @@ __device__ bool warp_inv_hpd(double2* A, int lane) {
       const int e = lane + 32 * r;
       if (e < M * M) {
         const int i = e / M, j = e % M;
-        const double2 aik = A[i * M + k], akj = A[k * M + j];
-        if (i == k && j == k) nv[r] = rp;
-        else if (i == k) nv[r] = cmul(akj, rp);
-        else if (j == k) nv[r] = make_double2(-(aik.x * rp.x - aik.y * rp.y), -(aik.x * rp.y + aik.y * rp.x));
-        else nv[r] = csub(A[e], cmul(aik, cmul(akj, rp)));
+        const double2 aik = A[i * M + k], akj = A[k * M + j], aij = A[e];
+        // branch-free select (lanes of one warp take different cases)
+        const double2 akjr = cmul(akj, rp);
+        const double2 aikr = cmul(aik, rp);
+        const double2 other = csub(aij, cmul(aik, akjr));
+        const bool rk = i == k, ck = j == k;
+        double2 v = rk ? akjr : other;
+        v = ck ? (rk ? rp : make_double2(-aikr.x, -aikr.y)) : v;
+        nv[r] = v;
       }
     }
     __syncwarp();

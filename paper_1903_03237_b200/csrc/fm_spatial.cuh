@@ -1,9 +1,10 @@
 // fm_spatial.cuh -- the per-frequency part of the FastMNMF iteration.
 //
-// k_front (one CTA per (f, b)): gain statistics + g MU (separate.py:217-220;
-//   _kernels.py:244-250), the weighted covariances V_fm = (1/T) sum_t x x^H /
-//   y_ftm from the floored model power with the new gains (separate.py:221-222,
-//   spatial.py:182, _kernels.py:276-293), the iterative-projection row updates
+// k_gain / k_vacc (flat (f, t) tiles): gain statistics + g MU
+//   (separate.py:217-220; _kernels.py:244-250) and the weighted covariances
+//   V_fm = (1/T) sum_t x x^H / y_ftm from the floored model power with the new
+//   gains (separate.py:221-222, spatial.py:182, _kernels.py:276-293).
+// k_ip (one small CTA per (f, b)): the iterative-projection row updates
 //   (spatial.py:181-199), row normalisation (separate.py:223-229), log|det Q|
 //   (separate.py:236-238) and the gain normalisation folded into W
 //   (separate.py:231-233, spatial.py:244-249, sources.py:202-204).
@@ -44,290 +45,290 @@ __device__ __forceinline__ double2 fma2(double2 a, double2 b, double2 c) {
   return make_double2(fma(a.x, b.x, c.x), fma(a.y, b.y, c.y));
 }
 
-template <int M> struct FrCfg {
-  static constexpr int BS = (M <= 8) ? 256 : 512;
-  static constexpr int TC = 256;
-  static constexpr int P = M * (M + 1) / 2;
-  static constexpr int S2 = BS / P;
-};
-
-template <typename R> struct FrontArgs {
-  const cplx<R>* X;
+// ---------------------------------------------------------------------------
+// k_gain and k_vacc tile the (f, t) plane flat -- grid (ceil(T/256), F, B) --
+// so that every SM streams many independent 256-frame tiles. Each tile
+// writes its partial T-sums; the last tile of a bin (per-bin arrival counter)
+// reduces the partials in fixed tile order (deterministic) and finishes the
+// bin: the g MU for k_gain, the scaled and mirrored V_f (fp64) for k_vacc.
+// ---------------------------------------------------------------------------
+template <typename R> struct GainArgs {
   const R* xt;
-  cplx<R>* Q;
-  R* g;
-  R* W;
   const R* lam;
+  R* g;
   const R* floorp;
-  double2* V;       // (B, F, M, M, M) weighted covariances for k_ip
-  int F, T, N, K;
-  long long* timing;  // optional (F, 8) clock64 stamps per phase (profiling builds/tools)
+  R* part;             // (B, F, tiles, N, 2M)
+  unsigned* counters;  // (B, F)
+  int F, T, N;
 };
 
-template <typename R, int M> struct FrontSmem {
-  using C = cplx<R>;
-  static constexpr int BS = FrCfg<M>::BS, TC = FrCfg<M>::TC, P = FrCfg<M>::P;
-  static constexpr size_t al(size_t x) { return (x + 15) & ~size_t(15); }
-  // control region
-  static constexpr size_t o_gs = 0;
-  static constexpr size_t o_cs = o_gs + al(sizeof(R) * NMAX * M);
-  static constexpr size_t o_rown = o_cs + al(sizeof(R) * NMAX);
-  static constexpr size_t o_pairs = o_rown + al(sizeof(double) * M);
-  static constexpr size_t o_redw = o_pairs + al(sizeof(int) * 2 * P);
-  static constexpr size_t o_misc = o_redw + al(sizeof(R) * (BS / 32) * 2 * M);
-  static constexpr size_t o_Qd = o_misc + al(sizeof(double) * 8 + sizeof(int) * (M + 8));
-  static constexpr size_t o_Ai = o_Qd + al(sizeof(double2) * M * M);
-  static constexpr size_t o_vec = o_Ai + al(sizeof(double2) * M * 2 * M);
-  static constexpr size_t o_union = o_vec + al(sizeof(double2) * 3 * M);
-  // streaming buffers (phases A1/A2) ...
-  static constexpr size_t s_lam = 0;
-  static constexpr size_t s_iy = s_lam + al(sizeof(R) * NMAX * (TC + 1));
-  static constexpr size_t s_xr = s_iy + al(sizeof(R) * TC * M);
-  static constexpr size_t s_X = s_xr + al(sizeof(R) * TC * M);
-  static constexpr size_t s_end = s_X + al(sizeof(C) * TC * M);
-  // ... overlaid by V (fp64) once streaming is done
-  static constexpr size_t v_end = al(sizeof(double2) * M * M * M);
-  static constexpr size_t bytes = o_union + (s_end > v_end ? s_end : v_end);
+template <typename R, int M> struct GaCfg {
+  static constexpr int TB = (sizeof(R) == 4) ? 256 : 128;  // frames per tile (smem bound)
 };
 
+// gain statistics (separate.py:217; _kernels.py:244-250) + g MU (:218-220)
 template <typename R, int M>
-__global__ void __launch_bounds__(FrCfg<M>::BS, (M <= 8 ? 2 : 1)) k_front(FrontArgs<R> a) {
-  using C = cplx<R>;
-  using L = FrontSmem<R, M>;
-  constexpr int BS = FrCfg<M>::BS, TC = FrCfg<M>::TC, P = FrCfg<M>::P, S2 = FrCfg<M>::S2;
-  constexpr int NW = BS / 32;
-  extern __shared__ __align__(16) unsigned char sm[];
-  R* gs = reinterpret_cast<R*>(sm + L::o_gs);
-  int* pairs = reinterpret_cast<int*>(sm + L::o_pairs);
-  R* redw = reinterpret_cast<R*>(sm + L::o_redw);
-  unsigned char* un = sm + L::o_union;
-  R* lamc = reinterpret_cast<R*>(un + L::s_lam);
-  R* iys = reinterpret_cast<R*>(un + L::s_iy);
-  R* xrs = reinterpret_cast<R*>(un + L::s_xr);
-  C* Xc = reinterpret_cast<C*>(un + L::s_X);
-  double2* Vd = reinterpret_cast<double2*>(un);
-
-  const int f = blockIdx.x, b = blockIdx.y;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int N = a.N, T = a.T, F = a.F, K = a.K;
+__global__ void __launch_bounds__(256) k_gain(GainArgs<R> a) {
+  constexpr int TB = GaCfg<R, M>::TB;
+  __shared__ __align__(16) R lams[NMAX * (TB + 1)];
+  __shared__ __align__(16) R iys[TB * M];
+  __shared__ __align__(16) R xrs[TB * M];
+  __shared__ __align__(16) R gs[NMAX * M];
+  __shared__ R redb[512];
+  __shared__ int is_last;
+  const int tile = blockIdx.x, f = blockIdx.y, b = blockIdx.z, ntile = gridDim.x;
+  const int tid = threadIdx.x;
+  const int N = a.N, T = a.T, F = a.F;
   const size_t FT = (size_t)F * T;
-  const C* X = a.X + ((size_t)b * F + f) * T * M;
-  const R* xt = a.xt + ((size_t)b * F + f) * T * M;
-  const R* lam = a.lam + (size_t)b * N * FT + (size_t)f * T;
+  const int t = tile * TB + tid;
   R* gg = a.g + (size_t)b * N * F * M + (size_t)f * M;
-  const R fl = a.floorp[b];
-  long long* tstamp = (a.timing && b == 0) ? a.timing + (size_t)f * 8 : nullptr;
-#define FM_STAMP(i) \
-  if (tstamp && tid == 0) tstamp[i] = clock64();
-  FM_STAMP(0);
-
-  for (int e = tid; e < N * M; e += BS) gs[e] = gg[(size_t)(e / M) * F * M + (e % M)];
-  if (tid == 0) {
-    int p = 0;
-    for (int i = 0; i < M; ++i)
-      for (int j = i; j < M; ++j) {
-        pairs[2 * p] = i;
-        pairs[2 * p + 1] = j;
-        ++p;
-      }
+  for (int e = tid; e < N * M; e += 256) gs[e] = gg[(size_t)(e / M) * F * M + (e % M)];
+  R l[NMAX], x[M];
+  const bool tv = tid < TB && t < T;
+  const int tc = tv ? t : T - 1;
+  const R* lb = a.lam + (size_t)b * N * FT + (size_t)f * T + tc;
+#pragma unroll
+  for (int n = 0; n < NMAX; ++n) {
+    l[n] = R(0);
+    if (n >= N) break;
+    l[n] = tv ? lb[(size_t)n * FT] : R(0);
   }
+  RowIO<R, M>::load(a.xt + (((size_t)b * F + f) * T + tc) * M, x);
   __syncthreads();
-
-  // ---- A1: gain statistics + g MU ------------------------------------------
-  {
-    const int WPN = NW / N;  // warps per source
-    const int n1 = warp / WPN, sub = warp % WPN;
-    const bool act = n1 < N;
-    const int S1 = WPN * 32, s1 = sub * 32 + lane;
-    R num[M], den[M];
-#pragma unroll
-    for (int m = 0; m < M; ++m) num[m] = den[m] = 0;
-    // register prefetch of the next chunk's lambda and x~ (one t per thread)
-    R lp[NMAX], xp[M];
-    auto fetchA1 = [&](int t0) {
-      const int t = t0 + tid;
-      const int tc = t < T ? t : T - 1;
-#pragma unroll
-      for (int n = 0; n < NMAX; ++n) {
-        lp[n] = R(0);
-        if (n >= N) break;
-        lp[n] = lam[(size_t)n * FT + tc];
-      }
-      RowIO<R, M>::load(xt + (size_t)tc * M, xp);
-    };
-    if (tid < TC) fetchA1(0);
-    for (int t0 = 0; t0 < T; t0 += TC) {
-      if (tid < TC) {
-        const int tl = tid, t = t0 + tl;
-        R l[NMAX], x[M];
-#pragma unroll
-        for (int n = 0; n < NMAX; ++n) l[n] = t < T ? lp[n] : R(0);
-#pragma unroll
-        for (int m = 0; m < M; ++m) x[m] = xp[m];
-        if (t0 + TC < T) fetchA1(t0 + TC);
-#pragma unroll
-        for (int n = 0; n < NMAX; ++n) {
-          if (n >= N) break;
-          lamc[n * (TC + 1) + tl] = l[n];
-        }
-        R iy[M], y[M], xr[M];
-        model_power<R, M>(l, gs, N, fl, iy, y);
-#pragma unroll
-        for (int m = 0; m < M; ++m) {
-          if (t >= T) iy[m] = R(0);
-          xr[m] = x[m] * iy[m] * iy[m];
-        }
-        RowIO<R, M>::store(iys + tl * M, iy);
-        RowIO<R, M>::store(xrs + tl * M, xr);
-      }
-      __syncthreads();
-      if (act) {
-        for (int tl = s1; tl < TC; tl += S1) {
-          const R l = lamc[n1 * (TC + 1) + tl];
-          R iy[M], xr[M];
-          RowIO<R, M>::load(iys + tl * M, iy);
-          RowIO<R, M>::load(xrs + tl * M, xr);
-#pragma unroll
-          for (int m = 0; m < M; ++m) {
-            num[m] += l * xr[m];
-            den[m] += l * iy[m];
-          }
-        }
-      }
-      __syncthreads();
-    }
+  if (tid < TB) {
+    R iy[M], y[M], xr[M];
+    model_power<R, M>(l, gs, N, a.floorp[b], iy, y);
 #pragma unroll
     for (int m = 0; m < M; ++m) {
-      num[m] = warp_sum(num[m]);
-      den[m] = warp_sum(den[m]);
+      if (!tv) iy[m] = R(0);
+      xr[m] = x[m] * iy[m] * iy[m];
     }
-    if (act && lane == 0) {
+    RowIO<R, M>::store(iys + tid * M, iy);
+    RowIO<R, M>::store(xrs + tid * M, xr);
+#pragma unroll
+    for (int n = 0; n < NMAX; ++n) {
+      if (n >= N) break;
+      lams[n * (TB + 1) + tid] = l[n];
+    }
+  }
+  __syncthreads();
+  // thread = ((n, m) entry, slice); slices stride over the tile's frames
+  const int E = N * M, S = 256 / E;
+  const int e1 = tid % E, s1 = tid / E;
+  const int n1 = e1 / M, m1 = e1 % M;
+  R num = 0, den = 0;
+  if (s1 < S) {
+    for (int tl = s1; tl < TB; tl += S) {
+      const R lv = lams[n1 * (TB + 1) + tl];
+      num += lv * xrs[tl * M + m1];
+      den += lv * iys[tl * M + m1];
+    }
+  }
+  __syncthreads();
+  R* red = redb;  // S * E <= 256 entries of (num, den)
+  if (s1 < S) {
+    red[(s1 * E + e1) * 2] = num;
+    red[(s1 * E + e1) * 2 + 1] = den;
+  }
+  __syncthreads();
+  R* pb = a.part + (((size_t)b * F + f) * ntile + tile) * N * 2 * M;
+  if (tid < E) {
+    R vn = 0, vd = 0;
+    for (int s = 0; s < S; ++s) {
+      vn += red[(s * E + tid) * 2];
+      vd += red[(s * E + tid) * 2 + 1];
+    }
+    pb[n1 * 2 * M + m1] = vn;
+    pb[n1 * 2 * M + M + m1] = vd;
+  }
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) {
+    unsigned* c = a.counters + (size_t)b * F + f;
+    is_last = atomicAdd(c, 1u) == (unsigned)ntile - 1;
+    if (is_last) *c = 0u;
+  }
+  __syncthreads();
+  if (!is_last) return;
+  __threadfence();
+  for (int e = tid; e < N * M; e += 256) {
+    const int n = e / M, m = e % M;
+    R sn = 0, sd = 0;
+    for (int q = 0; q < ntile; ++q) {
+      const R* pq = a.part + (((size_t)b * F + f) * ntile + q) * N * 2 * M + n * 2 * M;
+      sn += __ldcg(pq + m);
+      sd += __ldcg(pq + M + m);
+    }
+    gg[(size_t)n * F * M + m] = gs[e] * mu_factor(sn, sd);
+  }
+}
+
+template <typename R, int M> struct VaCfg {
+  static constexpr int BS = (M <= 8) ? 256 : 512;
+  static constexpr int P = M * (M + 1) / 2;
+  static constexpr int S2 = BS / P;
+  // frames per tile: the staged (x, 1/y) rows must fit ~36 KB of static smem
+  static constexpr int ROWB = M * 3 * (int)sizeof(R);
+  static constexpr int TB = (256 * ROWB <= 36864) ? 256 : (128 * ROWB <= 36864) ? 128 : 64;
+};
+
+template <typename R> struct VaccArgs {
+  const cplx<R>* X;
+  const R* lam;
+  const R* g;
+  const R* floorp;
+  R* part;             // (B, F, tiles, M, P, 2)
+  unsigned* counters;  // (B, F)
+  double2* V;          // (B, F, M, M, M) for k_ip
+  int F, T, N;
+};
+
+// V_fm = (1/T) sum_t x x^H / y_ftm with y from the updated gains
+// (separate.py:221-222; spatial.py:182; _kernels.py:276-293)
+template <typename R, int M>
+__global__ void __launch_bounds__(VaCfg<R, M>::BS) k_vacc(VaccArgs<R> a) {
+  using C = cplx<R>;
+  constexpr int BS = VaCfg<R, M>::BS, TB = VaCfg<R, M>::TB, P = VaCfg<R, M>::P,
+                S2 = VaCfg<R, M>::S2;
+  constexpr int STAGE = TB * M * (int)(sizeof(R) + sizeof(C));
+  constexpr int REDB = M * P * (int)sizeof(C);
+  __shared__ __align__(16) unsigned char buf[STAGE > REDB ? STAGE : REDB];
+  R* iys = reinterpret_cast<R*>(buf);
+  C* Xc = reinterpret_cast<C*>(buf + TB * M * sizeof(R));
+  __shared__ __align__(16) R gs[NMAX * M];
+  __shared__ int pairs[2 * P];
+  __shared__ int is_last;
+  const int tile = blockIdx.x, f = blockIdx.y, b = blockIdx.z, ntile = gridDim.x;
+  const int tid = threadIdx.x;
+  const int N = a.N, T = a.T, F = a.F;
+  const size_t FT = (size_t)F * T;
+  for (int e = tid; e < N * M; e += BS)
+    gs[e] = a.g[(size_t)b * N * F * M + (size_t)(e / M) * F * M + (size_t)f * M + (e % M)];
+  if (tid < P) {
+    int i = 0, r = tid;
+    while (r >= M - i) {
+      r -= M - i;
+      ++i;
+    }
+    pairs[2 * tid] = i;
+    pairs[2 * tid + 1] = i + r;
+  }
+  // load phase: one t per thread
+  const int t = tile * TB + tid;
+  const bool tv = tid < TB && t < T;
+  R l[NMAX];
+  C xv[M];
+  if (tid < TB) {
+    const int tc = t < T ? t : T - 1;
+    const R* lb = a.lam + (size_t)b * N * FT + (size_t)f * T + tc;
+#pragma unroll
+    for (int n = 0; n < NMAX; ++n) {
+      l[n] = R(0);
+      if (n >= N) break;
+      l[n] = lb[(size_t)n * FT];
+    }
+    CRowIO<R, M>::load(a.X + (((size_t)b * F + f) * T + tc) * M, xv);
+  }
+  __syncthreads();
+  if (tid < TB) {
+    R iy[M], y[M];
+    model_power<R, M>(l, gs, N, a.floorp[b], iy, y);
+#pragma unroll
+    for (int m = 0; m < M; ++m) {
+      if (!tv) {
+        iy[m] = R(0);
+        xv[m] = cmake<C>(0.0, 0.0);
+      }
+    }
+    RowIO<R, M>::store(iys + tid * M, iy);
+    CRowIO<R, M>::store(Xc + tid * M, xv);
+  }
+  __syncthreads();
+  // accumulate: thread = (pair i <= j, slice)
+  const int p = tid % P, s2 = tid / P;
+  const bool act = s2 < S2;
+  const int pi = pairs[2 * p], pj = pairs[2 * p + 1];
+  C v[M];
+#pragma unroll
+  for (int m = 0; m < M; ++m) v[m] = cmake<C>(0.0, 0.0);
+  if (act) {
+    int tl = s2;
+    for (; tl + S2 < TB; tl += 2 * S2) {
+      const C xi0 = Xc[tl * M + pi], xj0 = Xc[tl * M + pj];
+      const C xi1 = Xc[(tl + S2) * M + pi], xj1 = Xc[(tl + S2) * M + pj];
+      R iy0[M], iy1[M];
+      RowIO<R, M>::load(iys + tl * M, iy0);
+      RowIO<R, M>::load(iys + (tl + S2) * M, iy1);
+      C p0, p1;  // x_i conj(x_j)
+      p0.x = xi0.x * xj0.x + xi0.y * xj0.y;
+      p0.y = xi0.y * xj0.x - xi0.x * xj0.y;
+      p1.x = xi1.x * xj1.x + xi1.y * xj1.y;
+      p1.y = xi1.y * xj1.x - xi1.x * xj1.y;
 #pragma unroll
       for (int m = 0; m < M; ++m) {
-        redw[warp * 2 * M + m] = num[m];
-        redw[warp * 2 * M + M + m] = den[m];
+        v[m] = fma2(cmake<C>(iy0[m], iy0[m]), p0, v[m]);
+        v[m] = fma2(cmake<C>(iy1[m], iy1[m]), p1, v[m]);
+      }
+    }
+    if (tl < TB) {
+      const C xi = Xc[tl * M + pi], xj = Xc[tl * M + pj];
+      C pr;
+      pr.x = xi.x * xj.x + xi.y * xj.y;
+      pr.y = xi.y * xj.x - xi.x * xj.y;
+      R iy[M];
+      RowIO<R, M>::load(iys + tl * M, iy);
+#pragma unroll
+      for (int m = 0; m < M; ++m) v[m] = fma2(cmake<C>(iy[m], iy[m]), pr, v[m]);
+    }
+  }
+  __syncthreads();
+  // fixed-order slice reduction in smem (staging area reused)
+  C* red = reinterpret_cast<C*>(buf);
+  for (int ss = 0; ss < S2; ++ss) {
+    if (act && s2 == ss) {
+#pragma unroll
+      for (int m = 0; m < M; ++m) {
+        C* d = red + m * P + p;
+        if (ss == 0) {
+          *d = v[m];
+        } else {
+          C o = *d;
+          o.x += v[m].x;
+          o.y += v[m].y;
+          *d = o;
+        }
       }
     }
     __syncthreads();
-    for (int e = tid; e < N * M; e += BS) {
-      const int n = e / M, m = e % M;
-      R sn = 0, sd = 0;
-      for (int s = 0; s < WPN; ++s) {
-        sn += redw[(n * WPN + s) * 2 * M + m];
-        sd += redw[(n * WPN + s) * 2 * M + M + m];
-      }
-      gs[e] = gs[e] * mu_factor(sn, sd);
-    }
-    __syncthreads();
   }
-
-  FM_STAMP(1);
-  // ---- A2: V_fm accumulation ------------------------------------------------
-  {
-    const int p = tid % P, s2 = tid / P;
-    const bool act = s2 < S2;
-    const int pi = pairs[2 * p], pj = pairs[2 * p + 1];
-    C v[M];  // (re, im) of V[m][pi][pj]
-#pragma unroll
-    for (int m = 0; m < M; ++m) v[m] = cmake<C>(0.0, 0.0);
-    R lp[NMAX];
-    C xp[M];
-    auto fetchA2 = [&](int t0) {
-      const int t = t0 + tid;
-      const int tc = t < T ? t : T - 1;
-#pragma unroll
-      for (int n = 0; n < NMAX; ++n) {
-        lp[n] = R(0);
-        if (n >= N) break;
-        lp[n] = lam[(size_t)n * FT + tc];
-      }
-      CRowIO<R, M>::load(X + (size_t)tc * M, xp);
-    };
-    if (tid < TC) fetchA2(0);
-    for (int t0 = 0; t0 < T; t0 += TC) {
-      if (tid < TC) {
-        const int tl = tid, t = t0 + tl;
-        R l[NMAX];
-        C xv[M];
-#pragma unroll
-        for (int n = 0; n < NMAX; ++n) l[n] = lp[n];
-#pragma unroll
-        for (int m = 0; m < M; ++m) xv[m] = t < T ? xp[m] : cmake<C>(0.0, 0.0);
-        if (t0 + TC < T) fetchA2(t0 + TC);
-        R iy[M], y[M];
-        model_power<R, M>(l, gs, N, fl, iy, y);
-#pragma unroll
-        for (int m = 0; m < M; ++m)
-          if (t >= T) iy[m] = R(0);
-        RowIO<R, M>::store(iys + tl * M, iy);
-        CRowIO<R, M>::store(Xc + tl * M, xv);
-      }
-      __syncthreads();
-      if (act) {
-        // two t per trip: both rows' loads are in flight before the FMAs
-        int tl = s2;
-        for (; tl + S2 < TC; tl += 2 * S2) {
-          const C xi0 = Xc[tl * M + pi], xj0 = Xc[tl * M + pj];
-          const C xi1 = Xc[(tl + S2) * M + pi], xj1 = Xc[(tl + S2) * M + pj];
-          R iy0[M], iy1[M];
-          RowIO<R, M>::load(iys + tl * M, iy0);
-          RowIO<R, M>::load(iys + (tl + S2) * M, iy1);
-          C p0, p1;  // x_i conj(x_j)
-          p0.x = xi0.x * xj0.x + xi0.y * xj0.y;
-          p0.y = xi0.y * xj0.x - xi0.x * xj0.y;
-          p1.x = xi1.x * xj1.x + xi1.y * xj1.y;
-          p1.y = xi1.y * xj1.x - xi1.x * xj1.y;
-#pragma unroll
-          for (int m = 0; m < M; ++m) {
-            v[m] = fma2(cmake<C>(iy0[m], iy0[m]), p0, v[m]);
-            v[m] = fma2(cmake<C>(iy1[m], iy1[m]), p1, v[m]);
-          }
-        }
-        if (tl < TC) {
-          const C xi = Xc[tl * M + pi], xj = Xc[tl * M + pj];
-          C pr;
-          pr.x = xi.x * xj.x + xi.y * xj.y;
-          pr.y = xi.y * xj.x - xi.x * xj.y;
-          R iy[M];
-          RowIO<R, M>::load(iys + tl * M, iy);
-#pragma unroll
-          for (int m = 0; m < M; ++m) v[m] = fma2(cmake<C>(iy[m], iy[m]), pr, v[m]);
-        }
-      }
-      __syncthreads();
-    }
-    // fixed-order reduction over the S2 slices into Vd (fp64), then 1/T + mirror
-    for (int ss = 0; ss < S2; ++ss) {
-      if (act && s2 == ss) {
-#pragma unroll
-        for (int m = 0; m < M; ++m) {
-          double2* d = Vd + ((size_t)m * M + pi) * M + pj;
-          if (ss == 0) *d = to_d2(v[m]);
-          else *d = cadd(*d, to_d2(v[m]));
-        }
-      }
-      __syncthreads();
-    }
-    const double invT = 1.0 / (double)T;
-    for (int e = tid; e < M * P; e += BS) {
-      const int m = e / P, pp = e % P;
-      const int i = pairs[2 * pp], j = pairs[2 * pp + 1];
-      double2 d = Vd[((size_t)m * M + i) * M + j];
-      d = make_double2(d.x * invT, d.y * invT);
-      Vd[((size_t)m * M + i) * M + j] = d;
-      if (i != j) Vd[((size_t)m * M + j) * M + i] = make_double2(d.x, -d.y);
-    }
-    __syncthreads();
+  C* pb = reinterpret_cast<C*>(a.part) + (((size_t)b * F + f) * ntile + tile) * M * P;
+  for (int e = tid; e < M * P; e += BS) pb[e] = red[e];
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) {
+    unsigned* c = a.counters + (size_t)b * F + f;
+    is_last = atomicAdd(c, 1u) == (unsigned)ntile - 1;
+    if (is_last) *c = 0u;
   }
-
-  // publish the updated gains and V_f (fp64) for k_ip
-  {
-    double2* Vg = a.V + ((size_t)b * F + f) * M * M * M;
-    for (int e = tid; e < M * M * M; e += BS) Vg[e] = Vd[e];
-    for (int e = tid; e < N * M; e += BS) gg[(size_t)(e / M) * F * M + (e % M)] = gs[e];
+  __syncthreads();
+  if (!is_last) return;
+  __threadfence();
+  const double invT = 1.0 / (double)T;
+  double2* Vf = a.V + ((size_t)b * F + f) * M * M * M;
+  const C* p0 = reinterpret_cast<const C*>(a.part) + ((size_t)b * F + f) * ntile * M * P;
+  for (int e = tid; e < M * P; e += BS) {
+    double2 acc = make_double2(0.0, 0.0);
+    for (int q = 0; q < ntile; ++q) {
+      const C c = p0[(size_t)q * M * P + e];
+      acc.x += (double)c.x;
+      acc.y += (double)c.y;
+    }
+    const int m = e / P, pp = e % P;
+    const int i = pairs[2 * pp], j = pairs[2 * pp + 1];
+    const double2 d = make_double2(acc.x * invT, acc.y * invT);
+    Vf[((size_t)m * M + i) * M + j] = d;
+    if (i != j) Vf[((size_t)m * M + j) * M + i] = make_double2(d.x, -d.y);
   }
-  FM_STAMP(2);
-#undef FM_STAMP
 }
 
 // ---------------------------------------------------------------------------
@@ -337,7 +338,7 @@ __global__ void __launch_bounds__(FrCfg<M>::BS, (M <= 8 ? 2 : 1)) k_front(FrontA
 // updates (one mat-vec each); all threads normalise and fold into W.
 // ---------------------------------------------------------------------------
 template <typename R> struct IpArgs {
-  const double2* V;  // (B, F, M, M, M) from k_front
+  const double2* V;  // (B, F, M, M, M) from k_vacc
   cplx<R>* Q;
   R* g;
   R* W;
@@ -425,6 +426,10 @@ __global__ void __launch_bounds__(IpCfg<M>::BS) k_ip(IpArgs<R> a) {
     if (warp == 0) {
       double ldet = misc[0], nprod = 1.0;
       int code = flags[0] ? 2 : 0, bad_m = 0;  // singular Q -> singular Q V at m = 0
+      // lanes per row for the mat-vecs: largest power of two with M * GL <= 32
+      constexpr int GL = M <= 1 ? 32 : M <= 2 ? 16 : M <= 4 ? 8 : M <= 8 ? 4 : M <= 16 ? 2 : 1;
+      const int ri = lane / GL, sub = lane % GL;
+      const bool rv = ri < M;
       for (int sw = 0; sw < a.ip_sweeps && code == 0; ++sw) {
         for (int m = 0; m < M; ++m) {
           if (vfail[m]) {
@@ -435,12 +440,20 @@ __global__ void __launch_bounds__(IpCfg<M>::BS) k_ip(IpArgs<R> a) {
           const double2* Vi = Vd + (size_t)m * M * M;
           if (lane < M) ub[lane] = Ai[lane * 2 * M + M + m];  // u = Q^-1 e_m
           __syncwarp();
+          // q = V_m^-1 u: GL lanes per row, strided partial dots + xor reduce
           double2 q = make_double2(0.0, 0.0);
-          double part = 0.0;
-          if (lane < M) {
+          if (rv) {
 #pragma unroll
-            for (int j = 0; j < M; ++j) q = cadd(q, cmul(Vi[lane * M + j], ub[j]));
-            const double2 u = ub[lane];
+            for (int j = sub; j < M; j += GL) q = cadd(q, cmul(Vi[ri * M + j], ub[j]));
+          }
+#pragma unroll
+          for (int o = GL / 2; o > 0; o >>= 1) {
+            q.x += __shfl_xor_sync(FM_FULL, q.x, o);
+            q.y += __shfl_xor_sync(FM_FULL, q.y, o);
+          }
+          double part = 0.0;
+          if (rv && sub == 0) {
+            const double2 u = ub[ri];
             part = q.x * u.x + q.y * u.y;  // Re(conj(q_i) u_i)
           }
           const double nrm = warp_sum(part);  // = q^H V q  (spatial.py:193)
@@ -449,19 +462,27 @@ __global__ void __launch_bounds__(IpCfg<M>::BS) k_ip(IpArgs<R> a) {
             bad_m = m;
             break;
           }
-          const double isn = rsqrt(nrm);  // 1 / sqrt(norm)
-          if (lane < M) {  // new row r = conj(q / sqrt(norm))  (spatial.py:199)
+          const double isn = drsqrt(nrm);  // 1 / sqrt(norm)
+          if (rv && sub == 0) {  // new row r = conj(q / sqrt(norm))  (spatial.py:199)
             const double2 r = make_double2(q.x * isn, -(q.y * isn));
-            qb[lane] = r;
-            Qd[m * M + lane] = r;
+            qb[ri] = r;
+            Qd[m * M + ri] = r;
           }
           __syncwarp();
-          if (lane < M) {  // s = (r Q^-1 - e_m^T) / sqrt(norm)
-            double2 s = make_double2(0.0, 0.0);
+          // s = (r Q^-1 - e_m^T) / sqrt(norm), column ri per lane group
+          double2 sv = make_double2(0.0, 0.0);
+          if (rv) {
 #pragma unroll
-            for (int j = 0; j < M; ++j) s = cadd(s, cmul(qb[j], Ai[j * 2 * M + M + lane]));
-            if (lane == m) s.x -= 1.0;
-            sk[lane] = make_double2(s.x * isn, s.y * isn);
+            for (int j = sub; j < M; j += GL) sv = cadd(sv, cmul(qb[j], Ai[j * 2 * M + M + ri]));
+          }
+#pragma unroll
+          for (int o = GL / 2; o > 0; o >>= 1) {
+            sv.x += __shfl_xor_sync(FM_FULL, sv.x, o);
+            sv.y += __shfl_xor_sync(FM_FULL, sv.y, o);
+          }
+          if (rv && sub == 0) {
+            if (ri == m) sv.x -= 1.0;
+            sk[ri] = make_double2(sv.x * isn, sv.y * isn);
           }
           __syncwarp();
           for (int e = lane; e < M * M; e += 32) {  // Q^-1 -= u s / sqrt(norm)
@@ -557,53 +578,45 @@ template <typename R> struct BackArgs {
   int record;
 };
 
+// One t per thread; grid (ceil(T/256), F, B): the (f, t) plane is tiled
+// flat so every SM streams many small tiles (no per-bin serial loop).
+// ll_part is (B, F, tiles) and reduced in fixed order by the last tile.
 template <typename R, int M>
-__global__ void __launch_bounds__(256, 2) k_back(BackArgs<R> a) {
+__global__ void __launch_bounds__(256, 3) k_back(BackArgs<R> a) {
   using C = cplx<R>;
-  __shared__ C Qr[M * M];
+  __shared__ __align__(16) C Qr[M * M];
   __shared__ __align__(16) R gs[NMAX * M];
   __shared__ R cs[NMAX];
   __shared__ double dred[8];
-  __shared__ int is_last;
-  const int f = blockIdx.x, b = blockIdx.y;
+  const int tile = blockIdx.x, f = blockIdx.y, b = blockIdx.z;
+  const int ntile = gridDim.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int N = a.N, T = a.T, F = a.F;
+  const int t = tile * 256 + tid;
   const size_t FT = (size_t)F * T;
-  const C* X = a.X + ((size_t)b * F + f) * T * M;
-  R* xt = a.xt + ((size_t)b * F + f) * T * M;
-  const R* lam = a.lam + (size_t)b * N * FT + (size_t)f * T;
-  R* phi = a.phi + (size_t)b * 2 * N * FT + (size_t)f * T;
-  const R fl = a.floorp[b];
   for (int e = tid; e < M * M; e += 256) Qr[e] = a.Q[((size_t)b * F + f) * M * M + e];
   for (int e = tid; e < N * M; e += 256)
     gs[e] = a.g[(size_t)b * N * F * M + (size_t)(e / M) * F * M + (size_t)f * M + (e % M)];
   if (tid < NMAX) cs[tid] = a.cs ? a.cs[((size_t)b * F + f) * NMAX + tid] : R(1);
-  __syncthreads();
   double ll = 0.0;
-  // register prefetch of the next step's x row and lambda values
-  C xp[M];
-  R lp[NMAX];
-  auto fetch = [&](int t) {
-    CRowIO<R, M>::load(X + (size_t)t * M, xp);
+  C xv[M];
+  R l[NMAX];
+  const bool tv = t < T;
+  if (tv) {
+    CRowIO<R, M>::load(a.X + (((size_t)b * F + f) * T + t) * M, xv);
+    const R* lb = a.lam + (size_t)b * N * FT + (size_t)f * T + t;
 #pragma unroll
     for (int n = 0; n < NMAX; ++n) {
-      lp[n] = R(0);
+      l[n] = R(0);
       if (n >= N) break;
-      lp[n] = lam[(size_t)n * FT + t];
+      l[n] = lb[(size_t)n * FT];
     }
-  };
-  if (tid < T) fetch(tid);
-  for (int t = tid; t < T; t += 256) {
-    // compiler barrier: re-read the (broadcast) shared-memory parameters each
-    // step instead of hoisting M*M + N*M of them into registers
-    asm volatile("" ::: "memory");
-    C xv[M];
-    R l[NMAX];
+  }
+  __syncthreads();
+  if (tv) {
+    const R fl = a.floorp[b];
 #pragma unroll
-    for (int m = 0; m < M; ++m) xv[m] = xp[m];
-#pragma unroll
-    for (int n = 0; n < NMAX; ++n) l[n] = lp[n] * cs[n];
-    if (t + 256 < T) fetch(t + 256);
+    for (int n = 0; n < NMAX; ++n) l[n] *= cs[n];
     R xtv[M];
 #pragma unroll
     for (int i = 0; i < M; ++i) {
@@ -616,14 +629,14 @@ __global__ void __launch_bounds__(256, 2) k_back(BackArgs<R> a) {
       }
       xtv[i] = s.x * s.x + s.y * s.y;
     }
-    RowIO<R, M>::store(xt + (size_t)t * M, xtv);
+    RowIO<R, M>::store(a.xt + (((size_t)b * F + f) * T + t) * M, xtv);
     R iy[M], y[M];
     model_power<R, M>(l, gs, N, fl, iy, y);
     R llt = 0;
 #pragma unroll
     for (int m = 0; m < M; ++m) llt += -xtv[m] * iy[m] - log_fast(y[m]);
-    ll += (double)llt;
-    phi_point<R, M>(xtv, iy, gs, N, phi, FT, (size_t)t);
+    ll = (double)llt;
+    phi_point<R, M>(xtv, iy, gs, N, a.phi + (size_t)b * 2 * N * FT, FT, (size_t)f * T + t);
   }
   ll = warp_sum(ll);
   if (lane == 0) dred[warp] = ll;
@@ -631,32 +644,44 @@ __global__ void __launch_bounds__(256, 2) k_back(BackArgs<R> a) {
   if (tid == 0) {
     double s = 0.0;
     for (int w = 0; w < 8; ++w) s += dred[w];
-    a.ll_part[(size_t)b * F + f] = s;
-  }
-  if (a.record) {
-    if (tid == 0) {
-      __threadfence();
-      const unsigned prev = atomicAdd(a.counter, 1u);
-      is_last = (prev == gridDim.x * gridDim.y - 1);
-    }
-    __syncthreads();
-    if (is_last) {
-      __threadfence();
-      const unsigned it = *a.iter;
-      for (int bb = tid; bb < a.B; bb += 256) {
-        double s1 = 0.0, s2 = 0.0;
-        for (int ff = 0; ff < F; ++ff) {
-          s1 += __ldcg(a.ll_part + (size_t)bb * F + ff);
-          s2 += __ldcg(a.ld_part + (size_t)bb * F + ff);
-        }
-        a.trace[(size_t)it * a.B + bb] = s1 + 2.0 * (double)T * s2;
-      }
-      if (tid == 0) {
-        *a.counter = 0u;
-        *a.iter = it + 1u;
-      }
-    }
+    a.ll_part[((size_t)b * F + f) * ntile + tile] = s;
   }
 }
+
+// trace entry of the state after this iteration (separate.py:313-318, :321):
+// sum of the data-term partials (B, F, tiles) + 2T sum_f log|det Q_f|, one CTA
+// per mixture, fixed-order strided + tree reduction (deterministic).
+static __global__ void __launch_bounds__(256) k_trace(const double* __restrict__ ll_part,
+                                               const double* __restrict__ ld_part,
+                                               double* __restrict__ trace, unsigned* iter, int B,
+                                               int F, int ntile, int T) {
+  __shared__ double r1[8], r2[8];
+  const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const size_t n1 = (size_t)F * ntile;
+  const double* p1 = ll_part + (size_t)b * n1;
+  const double* p2 = ld_part + (size_t)b * F;
+  double s1 = 0.0, s2 = 0.0;
+  for (size_t e = tid; e < n1; e += 256) s1 += p1[e];
+  for (int e = tid; e < F; e += 256) s2 += p2[e];
+  s1 = warp_sum(s1);
+  s2 = warp_sum(s2);
+  if (lane == 0) {
+    r1[warp] = s1;
+    r2[warp] = s2;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double a1 = 0.0, a2 = 0.0;
+    for (int w = 0; w < 8; ++w) {
+      a1 += r1[w];
+      a2 += r2[w];
+    }
+    const unsigned it = *iter;
+    if (trace) trace[(size_t)it * B + b] = a1 + 2.0 * (double)T * a2;
+    if (gridDim.x == 1) *iter = it + 1u;  // single mixture: advance here
+  }
+}
+
+static __global__ void k_iter_advance(unsigned* iter) { *iter += 1u; }
 
 }  // namespace fm
