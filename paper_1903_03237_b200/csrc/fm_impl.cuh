@@ -71,40 +71,53 @@ inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 // Workspace plan for the fused iteration.
 struct Plan {
-  int TS, FS, nft, ntt;  // split counts of k_wstats / k_hstats, their tile counts
-  size_t off_lam, off_phi, off_part, off_llp, off_ldp, off_cs, off_V, off_cnt, off_tiles, off_fcnt, total;
+  int FT, TT;    // k_wstats bins per CTA, k_hstats frames per CTA
+  int TR, nseg;  // k_gain / k_vacc frames per CTA segment and segments per bin
+  size_t off_lam, off_phi, off_gpart, off_vpart, off_gnew, off_llp, off_ldp, off_cs, off_cnt, total;
 };
 
 inline Plan make_plan(const fm_dims* d) {
   Plan p;
   const size_t rs = d->dtype == FM_F64 ? 8 : 4;
-  const long long B = d->B, F = d->F, T = d->T, N = d->N, K = d->K;
+  const long long B = d->B, F = d->F, T = d->T, N = d->N, M = d->M;
   const long long target = 2 * 148;  // >= 2 CTAs per SM
-  p.nft = (int)((F + 31) / 32);
-  p.ntt = (int)((T + 63) / 64);
-  long long ts = (target + B * N * p.nft - 1) / (B * N * p.nft);
-  p.TS = (int)std::max<long long>(1, std::min<long long>(ts, (T + 63) / 64));
-  long long fs = (target + B * N * p.ntt - 1) / (B * N * p.ntt);
-  p.FS = (int)std::max<long long>(1, std::min<long long>(fs, (F + 31) / 32));
-  const size_t partw = (size_t)B * N * p.TS * 2 * F * K;
-  const size_t parth = (size_t)B * N * p.FS * 2 * K * T;
-  const long long M = d->M, tiles64 = (T + 63) / 64;  // k_gain/k_vacc tiles >= 64 frames
-  const size_t partg = (size_t)B * F * tiles64 * N * 2 * M;
-  const size_t partv = (size_t)B * F * tiles64 * M * (M * (M + 1) / 2) * 2;
+  // largest tile that still gives ~2 CTAs per SM
+  p.FT = 32;
+  while (p.FT > 8 && ((F + p.FT - 1) / p.FT) * B * N < target) p.FT /= 2;
+  p.TT = 64;
+  while (p.TT > 16 && ((T + p.TT - 1) / p.TT) * B * N < target) p.TT /= 2;
+  // k_gain / k_vacc: segments per bin so that bins x segments >= ~4 CTAs per SM,
+  // each segment a multiple of 256 frames (the fp32 chunk; 64/128 divide it)
+  long long segs = std::max<long long>(1, (4 * 148 + F * B - 1) / (F * B));
+  long long tr = (T + segs - 1) / segs;
+  tr = ((tr + 255) / 256) * 256;
+  p.TR = (int)std::min<long long>(tr, std::max<long long>(T, 1));
+  if (p.TR < 256) p.TR = 256;
+  p.nseg = (int)((T + p.TR - 1) / p.TR);
+  const size_t gpart = (size_t)B * F * p.nseg * N * 2 * M;
+  const size_t vpart = (size_t)B * F * p.nseg * M * (M * (M + 1) / 2) * 2;
   size_t o = 0;
   p.off_lam = o; o = align256(o + (size_t)B * N * F * T * rs);
   p.off_phi = o; o = align256(o + (size_t)B * 2 * N * F * T * rs);
-  p.off_part = o; o = align256(o + std::max(std::max(partw, parth), std::max(partg, partv)) * rs);
+  p.off_gpart = o; o = align256(o + gpart * rs);
+  p.off_vpart = o; o = align256(o + vpart * rs);
+  p.off_gnew = o; o = align256(o + (size_t)B * N * F * M * rs);
   p.off_llp = o; o = align256(o + (size_t)B * F * ((T + 255) / 256) * 8);
   p.off_ldp = o; o = align256(o + (size_t)B * F * 8);
   p.off_cs = o; o = align256(o + (size_t)B * F * NMAX * rs);
-  p.off_V = o; o = align256(o + (size_t)B * F * d->M * d->M * d->M * sizeof(double2));
   p.off_cnt = o; o = align256(o + 64);
-  p.off_tiles = o; o = align256(o + sizeof(unsigned) * (size_t)B * N * (p.nft + p.ntt));
-  p.off_fcnt = o; o = align256(o + sizeof(unsigned) * (size_t)B * F * 2);
   p.total = o;
   return p;
 }
+
+#define FM_DISPATCH_TILE(X, NAME, ...)                                           \
+  switch (X) {                                                                   \
+    case 8: { constexpr int NAME = 8; __VA_ARGS__; } break;                     \
+    case 16: { constexpr int NAME = 16; __VA_ARGS__; } break;                   \
+    case 32: { constexpr int NAME = 32; __VA_ARGS__; } break;                   \
+    case 64: { constexpr int NAME = 64; __VA_ARGS__; } break;                   \
+    default: set_error("tile %d", (int)(X)); return FM_EINVAL;                  \
+  }
 
 int validate_dims(const fm_dims* d);
 
@@ -167,14 +180,12 @@ int Impl<R>::gain(const fm_dims* d, const fm_state* s, cudaStream_t st) {
   GainArgs<R> a;
   a.xt = reinterpret_cast<const R*>(s->xt);
   a.lam = reinterpret_cast<const R*>(w + p.off_lam);
-  a.g = reinterpret_cast<R*>(s->g);
+  a.g = reinterpret_cast<const R*>(s->g);
   a.floorp = reinterpret_cast<const R*>(s->floor);
-  a.part = reinterpret_cast<R*>(w + p.off_part);
-  a.counters = reinterpret_cast<unsigned*>(w + p.off_fcnt);
-  a.F = (int)d->F; a.T = (int)d->T; a.N = (int)d->N;
+  a.part = reinterpret_cast<R*>(w + p.off_gpart);
+  a.F = (int)d->F; a.T = (int)d->T; a.N = (int)d->N; a.TR = p.TR;
+  dim3 grid((unsigned)p.nseg, (unsigned)d->F, (unsigned)d->B);
   FM_DISPATCH_M(d->M, {
-    constexpr int TB = GaCfg<R, MM>::TB;
-    dim3 grid((unsigned)((d->T + TB - 1) / TB), (unsigned)d->F, (unsigned)d->B);
     k_gain<R, MM><<<grid, 256, 0, st>>>(a);
     FM_CHECK_LAUNCH("k_gain");
   });
@@ -189,14 +200,13 @@ int Impl<R>::vacc(const fm_dims* d, const fm_state* s, cudaStream_t st) {
   a.X = reinterpret_cast<const C*>(s->X);
   a.lam = reinterpret_cast<const R*>(w + p.off_lam);
   a.g = reinterpret_cast<const R*>(s->g);
+  a.gpart = reinterpret_cast<const R*>(w + p.off_gpart);
   a.floorp = reinterpret_cast<const R*>(s->floor);
-  a.part = reinterpret_cast<R*>(w + p.off_part);
-  a.counters = reinterpret_cast<unsigned*>(w + p.off_fcnt) + (size_t)d->B * d->F;
-  a.V = reinterpret_cast<double2*>(w + p.off_V);
-  a.F = (int)d->F; a.T = (int)d->T; a.N = (int)d->N;
+  a.gnew = reinterpret_cast<R*>(w + p.off_gnew);
+  a.part = reinterpret_cast<R*>(w + p.off_vpart);
+  a.F = (int)d->F; a.T = (int)d->T; a.N = (int)d->N; a.TR = p.TR;
+  dim3 grid((unsigned)p.nseg, (unsigned)d->F, (unsigned)d->B);
   FM_DISPATCH_M(d->M, {
-    constexpr int TB = VaCfg<R, MM>::TB;
-    dim3 grid((unsigned)((d->T + TB - 1) / TB), (unsigned)d->F, (unsigned)d->B);
     k_vacc<R, MM><<<grid, VaCfg<R, MM>::BS, 0, st>>>(a);
     FM_CHECK_LAUNCH("k_vacc");
   });
@@ -208,7 +218,10 @@ int Impl<R>::ip(const fm_dims* d, const fm_state* s, cudaStream_t st) {
   const Plan p = make_plan(d);
   unsigned char* w = reinterpret_cast<unsigned char*>(s->work);
   IpArgs<R> a;
-  a.V = reinterpret_cast<const double2*>(w + p.off_V);
+  a.Vpart = reinterpret_cast<const C*>(w + p.off_vpart);
+  a.nseg = p.nseg;
+  a.T = (int)d->T;
+  a.gnew = reinterpret_cast<const R*>(w + p.off_gnew);
   a.Q = reinterpret_cast<C*>(s->Q);
   a.g = reinterpret_cast<R*>(s->g);
   a.W = reinterpret_cast<R*>(s->W);
@@ -279,9 +292,6 @@ int Impl<R>::iterate_phase(const fm_dims* d, const fm_state* s, int phase, void*
   unsigned char* w = reinterpret_cast<unsigned char*>(s->work);
   R* lam = reinterpret_cast<R*>(w + p.off_lam);
   R* phi = reinterpret_cast<R*>(w + p.off_phi);
-  R* part = reinterpret_cast<R*>(w + p.off_part);
-  unsigned* wcnt = reinterpret_cast<unsigned*>(w + p.off_tiles);
-  unsigned* hcnt = wcnt + (size_t)d->B * d->N * p.nft;
   R* W = reinterpret_cast<R*>(s->W);
   R* H = reinterpret_cast<R*>(s->H);
   const int N = (int)d->N, F = (int)d->F, T = (int)d->T, K = (int)d->K;
@@ -289,13 +299,17 @@ int Impl<R>::iterate_phase(const fm_dims* d, const fm_state* s, int phase, void*
   if (phase == 0 || phase == 2) {
     // W step (separate.py:214-216 with step "W"): statistics from the phi of the
     // previous pass, MU, then the refresh with the new W (lambda + phi)
+    FM_EV(0);
     FM_DISPATCH_KB(K, {
-      FM_EV(0);
-      const size_t smw = WsCfg<R, KB>::bytes;
-      if (int rc = ensure_smem(k_wstats<R, KB>, smw)) return rc;
-      k_wstats<R, KB><<<dim3((unsigned)p.nft, (unsigned)p.TS, BN), 256, smw, st>>>(
-          phi, H, W, part, wcnt, N, F, T, K, p.TS);
-      FM_CHECK_LAUNCH("k_wstats");
+      FM_DISPATCH_TILE(p.FT, FTT, {
+        if constexpr (FTT <= 32) {
+          const size_t smw = WsCfg<R, KB, FTT>::bytes;
+          if (int rc = ensure_smem(k_wstats<R, KB, FTT>, smw)) return rc;
+          k_wstats<R, KB, FTT><<<dim3((unsigned)((F + FTT - 1) / FTT), BN), 256, smw, st>>>(
+              phi, H, W, N, F, T, K);
+          FM_CHECK_LAUNCH("k_wstats");
+        }
+      });
     });
     FM_EV(1);
     if (int rc = lambda(d, W, H, lam, st)) return rc;
@@ -309,19 +323,22 @@ int Impl<R>::iterate_phase(const fm_dims* d, const fm_state* s, int phase, void*
     // H step (separate.py:214-216 with step "H")
     FM_EV(3);
     FM_DISPATCH_KB(K, {
-      const size_t smh = HsCfg<R, KB>::bytes;
-      if (int rc = ensure_smem(k_hstats<R, KB>, smh)) return rc;
-      k_hstats<R, KB><<<dim3((unsigned)p.ntt, (unsigned)p.FS, BN), 256, smh, st>>>(
-          phi, W, H, part, hcnt, reinterpret_cast<R*>(hstat), N, F, T, K, p.FS,
-          phase == 0 ? 1 : 0);
-      FM_CHECK_LAUNCH("k_hstats");
+      FM_DISPATCH_TILE(p.TT, TTT, {
+        if constexpr (TTT >= 16) {
+          const size_t smh = HsCfg<R, KB, TTT>::bytes;
+          if (int rc = ensure_smem(k_hstats<R, KB, TTT>, smh)) return rc;
+          k_hstats<R, KB, TTT><<<dim3((unsigned)((T + TTT - 1) / TTT), BN), 256, smh, st>>>(
+              phi, W, H, reinterpret_cast<R*>(hstat), N, F, T, K, phase == 0 ? 1 : 0);
+          FM_CHECK_LAUNCH("k_hstats");
+        }
+      });
     });
   }
   if (phase == 0) return FM_OK;
   if (phase == 1) {
     const long long NKT = (long long)N * K * T, total = (long long)d->B * NKT;
     k_hupdate<R><<<(unsigned)((total + 255) / 256), 256, 0, st>>>(
-        part, H, reinterpret_cast<R*>(hstat), 1, NKT, total, 2);
+        nullptr, H, reinterpret_cast<R*>(hstat), 1, NKT, total, 2);
     FM_CHECK_LAUNCH("k_hupdate");
   }
   FM_EV(4);

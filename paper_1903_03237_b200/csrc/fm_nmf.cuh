@@ -42,47 +42,42 @@ template <int NPEND> __device__ __forceinline__ void cp_async_wait() {
 }
 
 // ---------------------------------------------------------------------------
-// W statistics + W MU. Tile: 32 f x KB k per CTA, T split in TS parts.
-// grid (ceil(F/32), TS, B*N), block 256.
-// Partials: part (B*N, TS, 2, F, K); counters: (B*N, ceil(F/32)).
+// W statistics + W MU (sources.py:191-194). One CTA owns FT bins of one
+// (b, n) and reduces over all of T itself (no split, no partials): operands
+// stream through a cp.async double buffer in TCH-frame chunks; thread tile
+// 4 f x 4 k (x2: num, den); slices of the CTA take interleaved frame quads
+// and are summed in one fixed-order pass at the end.
+// grid (ceil(F/FT), B*N), block 256.
 // ---------------------------------------------------------------------------
-template <typename R, int KB> struct WsCfg {
-  static constexpr int FT = 32;                          // f per CTA
-  static constexpr int TCH = sizeof(R) == 4 ? 64 : 32;   // t per staged chunk
+template <typename R, int KB, int FT> struct WsCfg {
+  static constexpr int TCH = sizeof(R) == 4 ? 128 : 64;  // frames per staged chunk
   static constexpr int LD = TCH + 4;                     // padded row
   static constexpr int NTH = (FT / 4) * (KB / 4);        // threads per slice
-  static constexpr int S = 256 / NTH;                    // reduction slices per CTA
+  static constexpr int S = 256 / NTH;                    // slices per CTA
   static constexpr int STAGE = (2 * FT + KB) * LD;       // staged operands (elements)
-  static constexpr int RED = 2 * FT * KB;                // slice reduction
+  static constexpr int RED = S * 2 * FT * KB;            // one-pass slice reduction
   static constexpr size_t bytes = sizeof(R) * (2 * STAGE > RED ? 2 * STAGE : RED);
 };
 
-template <typename R, int KB>
+template <typename R, int KB, int FT>
 __global__ void __launch_bounds__(256) k_wstats(const R* __restrict__ phi, const R* __restrict__ H,
-                                                R* __restrict__ W, R* __restrict__ part,
-                                                unsigned* __restrict__ counters, int N, int F,
-                                                int T, int K, int TS) {
-  using Cf = WsCfg<R, KB>;
-  constexpr int FT = Cf::FT, TCH = Cf::TCH, LD = Cf::LD, NTH = Cf::NTH, S = Cf::S;
+                                                R* __restrict__ W, int N, int F, int T, int K) {
+  using Cf = WsCfg<R, KB, FT>;
+  constexpr int TCH = Cf::TCH, LD = Cf::LD, NTH = Cf::NTH, S = Cf::S;
+  constexpr int FG = FT / 4, KG = KB / 4;
   extern __shared__ __align__(16) unsigned char smraw[];
   R* stage0 = reinterpret_cast<R*>(smraw);
-  __shared__ int is_last;
-  const int bn = blockIdx.z, ts = blockIdx.y, ftile = blockIdx.x;
-  const int f0 = ftile * FT;
+  const int bn = blockIdx.y, f0 = blockIdx.x * FT;
   const int tid = threadIdx.x;
   const int slot = tid % NTH, s = tid / NTH;
-  const int fg = slot % (FT / 4), kg = slot / (FT / 4);
+  const int fg = slot % FG, kg = slot / FG;
   const size_t FTs = (size_t)F * T;
   const int b = bn / N, n = bn % N;
   const R* P1 = phi + ((size_t)b * 2 * N + n) * FTs;
   const R* P2 = P1 + (size_t)N * FTs;
   const R* Hn = H + (size_t)bn * K * T;
-  // T range of this split (multiples of 4 keep the quads aligned)
-  const int tper = ((T + TS - 1) / TS + 3) & ~3;
-  const int ta = ts * tper, tb = min(T, ta + tper);
   const bool async = sizeof(R) == 4 && (T % 4) == 0;
   auto stage = [&](int st) { return stage0 + st * Cf::STAGE; };
-  // stage phi1/phi2 rows (FT x TCH) and H rows (KB x TCH) of chunk t0; t contiguous
   auto load = [&](int st, int t0) {
     R* p1s = stage(st);
     R* p2s = p1s + FT * LD;
@@ -91,28 +86,26 @@ __global__ void __launch_bounds__(256) k_wstats(const R* __restrict__ phi, const
       constexpr int Q = TCH / 4;
       for (int e = tid; e < FT * Q; e += 256) {
         const int fl = e / Q, q = e % Q, f = f0 + fl, t = t0 + 4 * q;
-        const bool v = f < F && t < tb;
+        const bool v = f < F && t < T;
         const size_t off = v ? (size_t)f * T + t : 0;
         cp_async16(p1s + fl * LD + 4 * q, P1 + off, v);
         cp_async16(p2s + fl * LD + 4 * q, P2 + off, v);
       }
       for (int e = tid; e < KB * Q; e += 256) {
         const int kl = e / Q, q = e % Q, t = t0 + 4 * q;
-        const bool v = kl < K && t < tb;
+        const bool v = kl < K && t < T;
         cp_async16(hs + kl * LD + 4 * q, Hn + (v ? (size_t)kl * T + t : 0), v);
       }
     } else {
       for (int e = tid; e < FT * TCH; e += 256) {
-        const int fl = e / TCH, tl = e % TCH;
-        const int f = f0 + fl, t = t0 + tl;
-        const bool v = f < F && t < tb;
+        const int fl = e / TCH, tl = e % TCH, f = f0 + fl, t = t0 + tl;
+        const bool v = f < F && t < T;
         p1s[fl * LD + tl] = v ? P1[(size_t)f * T + t] : R(0);
         p2s[fl * LD + tl] = v ? P2[(size_t)f * T + t] : R(0);
       }
       for (int e = tid; e < KB * TCH; e += 256) {
-        const int kl = e / TCH, tl = e % TCH;
-        const int t = t0 + tl;
-        hs[kl * LD + tl] = (kl < K && t < tb) ? Hn[(size_t)kl * T + t] : R(0);
+        const int kl = e / TCH, tl = e % TCH, t = t0 + tl;
+        hs[kl * LD + tl] = (kl < K && t < T) ? Hn[(size_t)kl * T + t] : R(0);
       }
     }
     cp_async_commit();
@@ -123,9 +116,9 @@ __global__ void __launch_bounds__(256) k_wstats(const R* __restrict__ phi, const
 #pragma unroll
     for (int j = 0; j < 4; ++j) a1[i][j] = a2[i][j] = 0;
   int st = 0;
-  if (ta < tb) load(0, ta);
-  for (int t0 = ta; t0 < tb; t0 += TCH, st ^= 1) {
-    if (t0 + TCH < tb) {
+  load(0, 0);
+  for (int t0 = 0; t0 < T; t0 += TCH, st ^= 1) {
+    if (t0 + TCH < T) {
       load(st ^ 1, t0 + TCH);  // next chunk in flight during this one
       cp_async_wait<1>();
     } else {
@@ -135,78 +128,45 @@ __global__ void __launch_bounds__(256) k_wstats(const R* __restrict__ phi, const
     const R* p1s = stage(st);
     const R* p2s = p1s + FT * LD;
     const R* hs = p2s + FT * LD;
-    if (s < S) {
-      for (int tq = s * 4; tq < TCH; tq += 4 * S) {
-        R x1[4][4], x2[4][4], h[4][4];
+    for (int tq = s * 4; tq < TCH; tq += 4 * S) {
+      R x1[4][4], x2[4][4], h[4][4];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          lds4(p1s + (fg + 8 * i) * LD + tq, x1[i]);
-          lds4(p2s + (fg + 8 * i) * LD + tq, x2[i]);
-          lds4(hs + (kg + (KB / 4) * i) * LD + tq, h[i]);
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-#pragma unroll
-          for (int i = 0; i < 4; ++i)
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              a1[i][j] += x1[i][u] * h[j][u];
-              a2[i][j] += x2[i][u] * h[j][u];
-            }
+      for (int i = 0; i < 4; ++i) {
+        lds4(p1s + (fg + FG * i) * LD + tq, x1[i]);
+        lds4(p2s + (fg + FG * i) * LD + tq, x2[i]);
+        lds4(hs + (kg + KG * i) * LD + tq, h[i]);
       }
-    }
-    __syncthreads();
-  }
-  // fixed-order reduction over the S slices (staging area reused)
-  R* red = stage0;
-  R* red2 = stage0 + FT * KB;
-  for (int ss = 0; ss < S; ++ss) {
-    if (s == ss) {
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int u = 0; u < 4; ++u)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int idx = (fg + 8 * i) * KB + kg + (KB / 4) * j;
-          if (ss == 0) {
-            red[idx] = a1[i][j];
-            red2[idx] = a2[i][j];
-          } else {
-            red[idx] += a1[i][j];
-            red2[idx] += a2[i][j];
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            a1[i][j] += x1[i][u] * h[j][u];
+            a2[i][j] += x2[i][u] * h[j][u];
           }
-        }
     }
     __syncthreads();
   }
-  // write this split's partial, then the last split of the tile reduces + MU
-  R* pb = part + ((size_t)bn * TS + ts) * 2 * (size_t)F * K;
-  for (int e = tid; e < FT * KB; e += 256) {
-    const int fl = e / KB, k = e % KB, f = f0 + fl;
-    if (f < F && k < K) {
-      pb[(size_t)f * K + k] = red[e];
-      pb[(size_t)F * K + (size_t)f * K + k] = red2[e];
+  // one-pass fixed-order reduction over the S slices
+  R* red = stage0;  // [S][2][FT][KB]
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int idx = (fg + FG * i) * KB + kg + KG * j;
+      red[(s * 2) * FT * KB + idx] = a1[i][j];
+      red[(s * 2 + 1) * FT * KB + idx] = a2[i][j];
     }
-  }
-  __threadfence();
   __syncthreads();
-  if (tid == 0) {
-    unsigned* c = counters + (size_t)bn * gridDim.x + ftile;
-    const unsigned prev = atomicAdd(c, 1u);
-    is_last = prev == (unsigned)TS - 1;
-    if (is_last) *c = 0u;
-  }
-  __syncthreads();
-  if (!is_last) return;
-  __threadfence();
   R* Wn = W + (size_t)bn * F * K;
   for (int e = tid; e < FT * KB; e += 256) {
     const int fl = e / KB, k = e % KB, f = f0 + fl;
     if (f < F && k < K) {
       R sn = 0, sd = 0;
-      for (int q = 0; q < TS; ++q) {
-        const R* pq = part + ((size_t)bn * TS + q) * 2 * (size_t)F * K;
-        sn += __ldcg(pq + (size_t)f * K + k);
-        sd += __ldcg(pq + (size_t)F * K + (size_t)f * K + k);
+      for (int q = 0; q < S; ++q) {
+        sn += red[(q * 2) * FT * KB + e];
+        sd += red[(q * 2 + 1) * FT * KB + e];
       }
       Wn[(size_t)f * K + k] *= mu_factor(sn, sd);  // sources.py:194
     }
@@ -214,47 +174,41 @@ __global__ void __launch_bounds__(256) k_wstats(const R* __restrict__ phi, const
 }
 
 // ---------------------------------------------------------------------------
-// H statistics + H MU. Tile: KB k x 64 t per CTA, F split in FS parts.
-// grid (ceil(T/64), FS, B*N), block 256.
-// Partials: part (B*N, FS, 2, K, T); counters (B*N, ceil(T/64)).
-// mode 0: apply the MU; mode 1: write the (num, den) sums to hout
+// H statistics + H MU (sources.py:195-198). One CTA owns TT frames of one
+// (b, n) and reduces over all local F itself; W rows and phi rows stream
+// through a cp.async double buffer in FCH-bin chunks; thread tile 4 k x 4 t
+// (x2). mode 0 applies the MU; mode 1 writes the (num, den) sums to hout
 // (B, 2, N, K, T) for the cross-shard all-reduce.
+// grid (ceil(T/TT), B*N), block 256.
 // ---------------------------------------------------------------------------
-template <typename R, int KB> struct HsCfg {
-  static constexpr int TT = 64;                          // t per CTA
-  static constexpr int FCH = sizeof(R) == 4 ? 32 : 16;   // f per staged chunk
+template <typename R, int KB, int TT> struct HsCfg {
+  static constexpr int FCH = sizeof(R) == 4 ? 32 : 16;   // bins per staged chunk
   static constexpr int NTH = (KB / 4) * (TT / 4);        // threads per slice
-  static constexpr int S = 256 / NTH;                    // reduction slices
+  static constexpr int S = 256 / NTH;                    // slices (over bins)
   static constexpr int LDW = KB + 4, LDP = TT + 4;
   static constexpr int STAGE = FCH * LDW + 2 * FCH * LDP;
-  static constexpr int RED = 2 * KB * TT;
+  static constexpr int RED = S * 2 * KB * TT;
   static constexpr size_t bytes = sizeof(R) * (2 * STAGE > RED ? 2 * STAGE : RED);
 };
 
-template <typename R, int KB>
+template <typename R, int KB, int TT>
 __global__ void __launch_bounds__(256) k_hstats(const R* __restrict__ phi, const R* __restrict__ W,
-                                                R* __restrict__ H, R* __restrict__ part,
-                                                unsigned* __restrict__ counters,
-                                                R* __restrict__ hout, int N, int F, int T, int K,
-                                                int FS, int mode) {
-  using Cf = HsCfg<R, KB>;
-  constexpr int TT = Cf::TT, FCH = Cf::FCH, NTH = Cf::NTH, S = Cf::S;
-  constexpr int LDW = Cf::LDW, LDP = Cf::LDP;
+                                                R* __restrict__ H, R* __restrict__ hout, int N,
+                                                int F, int T, int K, int mode) {
+  using Cf = HsCfg<R, KB, TT>;
+  constexpr int FCH = Cf::FCH, NTH = Cf::NTH, S = Cf::S, LDW = Cf::LDW, LDP = Cf::LDP;
+  constexpr int TG = TT / 4;
   extern __shared__ __align__(16) unsigned char smraw[];
   R* stage0 = reinterpret_cast<R*>(smraw);
-  __shared__ int is_last;
-  const int bn = blockIdx.z, fs = blockIdx.y, ttile = blockIdx.x;
-  const int t0 = ttile * TT;
+  const int bn = blockIdx.y, t0 = blockIdx.x * TT;
   const int tid = threadIdx.x;
   const int slot = tid % NTH, s = tid / NTH;
-  const int tg = slot % (TT / 4), kg = slot / (TT / 4);
+  const int tg = slot % TG, kg = slot / TG;
   const size_t FTs = (size_t)F * T;
   const int b = bn / N, n = bn % N;
   const R* P1 = phi + ((size_t)b * 2 * N + n) * FTs;
   const R* P2 = P1 + (size_t)N * FTs;
   const R* Wn = W + (size_t)bn * F * K;
-  const int fper = (F + FS - 1) / FS;
-  const int fa = fs * fper, fb = min(F, fa + fper);
   const bool async = sizeof(R) == 4 && (T % 4) == 0;
   auto stage = [&](int st) { return stage0 + st * Cf::STAGE; };
   auto load = [&](int st, int c0) {
@@ -263,13 +217,13 @@ __global__ void __launch_bounds__(256) k_hstats(const R* __restrict__ phi, const
     R* p2s = p1s + FCH * LDP;
     for (int e = tid; e < FCH * KB; e += 256) {
       const int fl = e / KB, k = e % KB, f = c0 + fl;
-      ws[fl * LDW + k] = (f < fb && k < K) ? Wn[(size_t)f * K + k] : R(0);
+      ws[fl * LDW + k] = (f < F && k < K) ? Wn[(size_t)f * K + k] : R(0);
     }
     if (async) {
       constexpr int Q = TT / 4;
       for (int e = tid; e < FCH * Q; e += 256) {
         const int fl = e / Q, q = e % Q, f = c0 + fl, t = t0 + 4 * q;
-        const bool v = f < fb && t < T;
+        const bool v = f < F && t < T;
         const size_t off = v ? (size_t)f * T + t : 0;
         cp_async16(p1s + fl * LDP + 4 * q, P1 + off, v);
         cp_async16(p2s + fl * LDP + 4 * q, P2 + off, v);
@@ -277,7 +231,7 @@ __global__ void __launch_bounds__(256) k_hstats(const R* __restrict__ phi, const
     } else {
       for (int e = tid; e < FCH * TT; e += 256) {
         const int fl = e / TT, tl = e % TT, f = c0 + fl, t = t0 + tl;
-        const bool v = f < fb && t < T;
+        const bool v = f < F && t < T;
         p1s[fl * LDP + tl] = v ? P1[(size_t)f * T + t] : R(0);
         p2s[fl * LDP + tl] = v ? P2[(size_t)f * T + t] : R(0);
       }
@@ -290,9 +244,9 @@ __global__ void __launch_bounds__(256) k_hstats(const R* __restrict__ phi, const
 #pragma unroll
     for (int j = 0; j < 4; ++j) a1[i][j] = a2[i][j] = 0;
   int st = 0;
-  if (fa < fb) load(0, fa);
-  for (int c0 = fa; c0 < fb; c0 += FCH, st ^= 1) {
-    if (c0 + FCH < fb) {
+  load(0, 0);
+  for (int c0 = 0; c0 < F; c0 += FCH, st ^= 1) {
+    if (c0 + FCH < F) {
       load(st ^ 1, c0 + FCH);
       cp_async_wait<1>();
     } else {
@@ -302,73 +256,40 @@ __global__ void __launch_bounds__(256) k_hstats(const R* __restrict__ phi, const
     const R* ws = stage(st);
     const R* p1s = ws + FCH * LDW;
     const R* p2s = p1s + FCH * LDP;
-    if (s < S) {
-      const int fe = min(FCH, fb - c0);
-      for (int fl = s; fl < fe; fl += S) {
-        R w[4], x1[4], x2[4];
-        lds4(ws + fl * LDW + kg * 4, w);
-        lds4(p1s + fl * LDP + tg * 4, x1);
-        lds4(p2s + fl * LDP + tg * 4, x2);
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            a1[i][j] += w[i] * x1[j];
-            a2[i][j] += w[i] * x2[j];
-          }
-      }
-    }
-    __syncthreads();
-  }
-  // fixed-order slice reduction into smem (KB x TT each; staging area reused)
-  R* red = stage0;
-  R* red2 = stage0 + KB * TT;
-  for (int ss = 0; ss < S; ++ss) {
-    if (s == ss) {
+    const int fe = min(FCH, F - c0);
+    for (int fl = s; fl < fe; fl += S) {
+      R w[4], x1[4], x2[4];
+      lds4(ws + fl * LDW + kg * 4, w);
+      lds4(p1s + fl * LDP + tg * 4, x1);
+      lds4(p2s + fl * LDP + tg * 4, x2);
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-          const int idx = (kg * 4 + i) * TT + tg * 4 + j;
-          if (ss == 0) {
-            red[idx] = a1[i][j];
-            red2[idx] = a2[i][j];
-          } else {
-            red[idx] += a1[i][j];
-            red2[idx] += a2[i][j];
-          }
+          a1[i][j] += w[i] * x1[j];
+          a2[i][j] += w[i] * x2[j];
         }
     }
     __syncthreads();
   }
-  R* pb = part + ((size_t)bn * FS + fs) * 2 * (size_t)K * T;
-  for (int e = tid; e < KB * TT; e += 256) {
-    const int k = e / TT, tl = e % TT, t = t0 + tl;
-    if (k < K && t < T) {
-      pb[(size_t)k * T + t] = red[e];
-      pb[(size_t)K * T + (size_t)k * T + t] = red2[e];
+  R* red = stage0;  // [S][2][KB][TT]
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int idx = (kg * 4 + i) * TT + tg * 4 + j;
+      red[(s * 2) * KB * TT + idx] = a1[i][j];
+      red[(s * 2 + 1) * KB * TT + idx] = a2[i][j];
     }
-  }
-  __threadfence();
   __syncthreads();
-  if (tid == 0) {
-    unsigned* c = counters + (size_t)bn * gridDim.x + ttile;
-    const unsigned prev = atomicAdd(c, 1u);
-    is_last = prev == (unsigned)FS - 1;
-    if (is_last) *c = 0u;
-  }
-  __syncthreads();
-  if (!is_last) return;
-  __threadfence();
   R* Hn = H + (size_t)bn * K * T;
   for (int e = tid; e < KB * TT; e += 256) {
     const int k = e / TT, tl = e % TT, t = t0 + tl;
     if (k < K && t < T) {
       R sn = 0, sd = 0;
-      for (int q = 0; q < FS; ++q) {
-        const R* pq = part + ((size_t)bn * FS + q) * 2 * (size_t)K * T;
-        sn += __ldcg(pq + (size_t)k * T + t);
-        sd += __ldcg(pq + (size_t)K * T + (size_t)k * T + t);
+      for (int q = 0; q < S; ++q) {
+        sn += red[(q * 2) * KB * TT + e];
+        sd += red[(q * 2 + 1) * KB * TT + e];
       }
       if (mode == 0) {
         Hn[(size_t)k * T + t] *= mu_factor(sn, sd);  // sources.py:198

@@ -1,6 +1,6 @@
 // fm_spatial.cuh -- the per-frequency part of the FastMNMF iteration.
 //
-// k_gain / k_vacc (flat (f, t) tiles): gain statistics + g MU
+// k_gain / k_vacc ((bin, frame-segment) CTAs): gain statistics + g MU
 //   (separate.py:217-220; _kernels.py:244-250) and the weighted covariances
 //   V_fm = (1/T) sum_t x x^H / y_ftm from the floored model power with the new
 //   gains (separate.py:221-222, spatial.py:182, _kernels.py:276-293).
@@ -46,27 +46,26 @@ __device__ __forceinline__ double2 fma2(double2 a, double2 b, double2 c) {
 }
 
 // ---------------------------------------------------------------------------
-// k_gain and k_vacc tile the (f, t) plane flat -- grid (ceil(T/256), F, B) --
-// so that every SM streams many independent 256-frame tiles. Each tile
-// writes its partial T-sums; the last tile of a bin (per-bin arrival counter)
-// reduces the partials in fixed tile order (deterministic) and finishes the
-// bin: the g MU for k_gain, the scaled and mirrored V_f (fp64) for k_vacc.
+// k_gain and k_vacc split the (f, t) plane into (bin, frame-segment) CTAs --
+// grid (ceil(T/TR), F, B) -- that stream their segment in TB-frame chunks
+// (register prefetch of the next chunk) and write fixed-order partial T-sums
+// per segment. The consumer reduces the segments in order (deterministic):
+// k_vacc finishes the g MU from the gain partials, k_ip finishes V_f.
 // ---------------------------------------------------------------------------
 template <typename R> struct GainArgs {
   const R* xt;
   const R* lam;
-  R* g;
+  const R* g;
   const R* floorp;
-  R* part;             // (B, F, tiles, N, 2M)
-  unsigned* counters;  // (B, F)
-  int F, T, N;
+  R* part;  // (B, F, nseg, N, 2M)
+  int F, T, N, TR;
 };
 
 template <typename R, int M> struct GaCfg {
-  static constexpr int TB = (sizeof(R) == 4) ? 256 : 128;  // frames per tile (smem bound)
+  static constexpr int TB = (sizeof(R) == 4) ? 256 : 128;  // frames per chunk (smem bound)
 };
 
-// gain statistics (separate.py:217; _kernels.py:244-250) + g MU (:218-220)
+// gain statistics (separate.py:217; _kernels.py:244-250)
 template <typename R, int M>
 __global__ void __launch_bounds__(256) k_gain(GainArgs<R> a) {
   constexpr int TB = GaCfg<R, M>::TB;
@@ -75,91 +74,83 @@ __global__ void __launch_bounds__(256) k_gain(GainArgs<R> a) {
   __shared__ __align__(16) R xrs[TB * M];
   __shared__ __align__(16) R gs[NMAX * M];
   __shared__ R redb[512];
-  __shared__ int is_last;
-  const int tile = blockIdx.x, f = blockIdx.y, b = blockIdx.z, ntile = gridDim.x;
+  const int seg = blockIdx.x, f = blockIdx.y, b = blockIdx.z, nseg = gridDim.x;
   const int tid = threadIdx.x;
   const int N = a.N, T = a.T, F = a.F;
   const size_t FT = (size_t)F * T;
-  const int t = tile * TB + tid;
-  R* gg = a.g + (size_t)b * N * F * M + (size_t)f * M;
-  for (int e = tid; e < N * M; e += 256) gs[e] = gg[(size_t)(e / M) * F * M + (e % M)];
-  R l[NMAX], x[M];
-  const bool tv = tid < TB && t < T;
-  const int tc = tv ? t : T - 1;
-  const R* lb = a.lam + (size_t)b * N * FT + (size_t)f * T + tc;
-#pragma unroll
-  for (int n = 0; n < NMAX; ++n) {
-    l[n] = R(0);
-    if (n >= N) break;
-    l[n] = tv ? lb[(size_t)n * FT] : R(0);
-  }
-  RowIO<R, M>::load(a.xt + (((size_t)b * F + f) * T + tc) * M, x);
-  __syncthreads();
-  if (tid < TB) {
-    R iy[M], y[M], xr[M];
-    model_power<R, M>(l, gs, N, a.floorp[b], iy, y);
-#pragma unroll
-    for (int m = 0; m < M; ++m) {
-      if (!tv) iy[m] = R(0);
-      xr[m] = x[m] * iy[m] * iy[m];
-    }
-    RowIO<R, M>::store(iys + tid * M, iy);
-    RowIO<R, M>::store(xrs + tid * M, xr);
+  const int ta = seg * a.TR, tb = min(T, ta + a.TR);
+  for (int e = tid; e < N * M; e += 256)
+    gs[e] = a.g[(size_t)b * N * F * M + (size_t)(e / M) * F * M + (size_t)f * M + (e % M)];
+  const R fl = a.floorp[b];
+  const R* lamb = a.lam + (size_t)b * N * FT + (size_t)f * T;
+  const R* xtb = a.xt + ((size_t)b * F + f) * T * M;
+  R lp[NMAX], xp[M];
+  auto fetch = [&](int c0) {
+    const int t = c0 + tid;
+    const int tc = t < tb ? t : tb - 1;
 #pragma unroll
     for (int n = 0; n < NMAX; ++n) {
+      lp[n] = R(0);
       if (n >= N) break;
-      lams[n * (TB + 1) + tid] = l[n];
+      lp[n] = lamb[(size_t)n * FT + tc];
     }
-  }
-  __syncthreads();
-  // thread = ((n, m) entry, slice); slices stride over the tile's frames
+    RowIO<R, M>::load(xtb + (size_t)tc * M, xp);
+  };
+  if (tid < TB) fetch(ta);
+  // accumulate mapping: thread = ((n, m) entry, slice)
   const int E = N * M, S = 256 / E;
   const int e1 = tid % E, s1 = tid / E;
   const int n1 = e1 / M, m1 = e1 % M;
   R num = 0, den = 0;
-  if (s1 < S) {
-    for (int tl = s1; tl < TB; tl += S) {
-      const R lv = lams[n1 * (TB + 1) + tl];
-      num += lv * xrs[tl * M + m1];
-      den += lv * iys[tl * M + m1];
+  __syncthreads();
+  for (int c0 = ta; c0 < tb; c0 += TB) {
+    if (tid < TB) {
+      const bool tv = c0 + tid < tb;
+      R l[NMAX], x[M];
+#pragma unroll
+      for (int n = 0; n < NMAX; ++n) l[n] = tv ? lp[n] : R(0);
+#pragma unroll
+      for (int m = 0; m < M; ++m) x[m] = xp[m];
+      if (c0 + TB < tb) fetch(c0 + TB);
+      R iy[M], y[M], xr[M];
+      model_power<R, M>(l, gs, N, fl, iy, y);
+#pragma unroll
+      for (int m = 0; m < M; ++m) {
+        if (!tv) iy[m] = R(0);
+        xr[m] = x[m] * iy[m] * iy[m];
+      }
+      RowIO<R, M>::store(iys + tid * M, iy);
+      RowIO<R, M>::store(xrs + tid * M, xr);
+#pragma unroll
+      for (int n = 0; n < NMAX; ++n) {
+        if (n >= N) break;
+        lams[n * (TB + 1) + tid] = l[n];
+      }
     }
+    __syncthreads();
+    if (s1 < S) {
+      for (int tl = s1; tl < TB; tl += S) {
+        const R lv = lams[n1 * (TB + 1) + tl];
+        num += lv * xrs[tl * M + m1];
+        den += lv * iys[tl * M + m1];
+      }
+    }
+    __syncthreads();
   }
-  __syncthreads();
-  R* red = redb;  // S * E <= 256 entries of (num, den)
   if (s1 < S) {
-    red[(s1 * E + e1) * 2] = num;
-    red[(s1 * E + e1) * 2 + 1] = den;
+    redb[(s1 * E + e1) * 2] = num;
+    redb[(s1 * E + e1) * 2 + 1] = den;
   }
   __syncthreads();
-  R* pb = a.part + (((size_t)b * F + f) * ntile + tile) * N * 2 * M;
   if (tid < E) {
     R vn = 0, vd = 0;
-    for (int s = 0; s < S; ++s) {
-      vn += red[(s * E + tid) * 2];
-      vd += red[(s * E + tid) * 2 + 1];
+    for (int q = 0; q < S; ++q) {
+      vn += redb[(q * E + tid) * 2];
+      vd += redb[(q * E + tid) * 2 + 1];
     }
+    R* pb = a.part + (((size_t)b * F + f) * nseg + seg) * N * 2 * M;
     pb[n1 * 2 * M + m1] = vn;
     pb[n1 * 2 * M + M + m1] = vd;
-  }
-  __threadfence();
-  __syncthreads();
-  if (tid == 0) {
-    unsigned* c = a.counters + (size_t)b * F + f;
-    is_last = atomicAdd(c, 1u) == (unsigned)ntile - 1;
-    if (is_last) *c = 0u;
-  }
-  __syncthreads();
-  if (!is_last) return;
-  __threadfence();
-  for (int e = tid; e < N * M; e += 256) {
-    const int n = e / M, m = e % M;
-    R sn = 0, sd = 0;
-    for (int q = 0; q < ntile; ++q) {
-      const R* pq = a.part + (((size_t)b * F + f) * ntile + q) * N * 2 * M + n * 2 * M;
-      sn += __ldcg(pq + m);
-      sd += __ldcg(pq + M + m);
-    }
-    gg[(size_t)n * F * M + m] = gs[e] * mu_factor(sn, sd);
   }
 }
 
@@ -167,43 +158,56 @@ template <typename R, int M> struct VaCfg {
   static constexpr int BS = (M <= 8) ? 256 : 512;
   static constexpr int P = M * (M + 1) / 2;
   static constexpr int S2 = BS / P;
-  // frames per tile: the staged (x, 1/y) rows must fit ~36 KB of static smem
+  // frames per chunk: the staged (x, 1/y) rows must fit ~36 KB of static smem
   static constexpr int ROWB = M * 3 * (int)sizeof(R);
   static constexpr int TB = (256 * ROWB <= 36864) ? 256 : (128 * ROWB <= 36864) ? 128 : 64;
+  static constexpr int STAGEB = TB * M * (int)(sizeof(R) + 2 * sizeof(R));
+  static constexpr bool ONEPASS = S2 * M * P * (int)(2 * sizeof(R)) <= STAGEB;
 };
 
 template <typename R> struct VaccArgs {
   const cplx<R>* X;
   const R* lam;
-  const R* g;
+  const R* g;      // gains before this iteration's MU
+  const R* gpart;  // k_gain partials (B, F, nseg, N, 2M)
   const R* floorp;
-  R* part;             // (B, F, tiles, M, P, 2)
-  unsigned* counters;  // (B, F)
-  double2* V;          // (B, F, M, M, M) for k_ip
-  int F, T, N;
+  R* gnew;         // (B, N, F, M) gains after the MU (written by segment 0)
+  R* part;         // (B, F, nseg, M, P) complex partial V sums
+  int F, T, N, TR;
 };
 
-// V_fm = (1/T) sum_t x x^H / y_ftm with y from the updated gains
-// (separate.py:221-222; spatial.py:182; _kernels.py:276-293)
+// g MU (separate.py:218-220) + V_fm = (1/T) sum_t x x^H / y_ftm with y from
+// the updated gains (separate.py:221-222; spatial.py:182; _kernels.py:276-293)
 template <typename R, int M>
 __global__ void __launch_bounds__(VaCfg<R, M>::BS) k_vacc(VaccArgs<R> a) {
   using C = cplx<R>;
-  constexpr int BS = VaCfg<R, M>::BS, TB = VaCfg<R, M>::TB, P = VaCfg<R, M>::P,
-                S2 = VaCfg<R, M>::S2;
-  constexpr int STAGE = TB * M * (int)(sizeof(R) + sizeof(C));
-  constexpr int REDB = M * P * (int)sizeof(C);
-  __shared__ __align__(16) unsigned char buf[STAGE > REDB ? STAGE : REDB];
+  using Cf = VaCfg<R, M>;
+  constexpr int BS = Cf::BS, TB = Cf::TB, P = Cf::P, S2 = Cf::S2;
+  constexpr int BUFB = (Cf::STAGEB > M * P * (int)sizeof(C)) ? Cf::STAGEB : M * P * (int)sizeof(C);
+  __shared__ __align__(16) unsigned char buf[BUFB];
   R* iys = reinterpret_cast<R*>(buf);
   C* Xc = reinterpret_cast<C*>(buf + TB * M * sizeof(R));
   __shared__ __align__(16) R gs[NMAX * M];
   __shared__ int pairs[2 * P];
-  __shared__ int is_last;
-  const int tile = blockIdx.x, f = blockIdx.y, b = blockIdx.z, ntile = gridDim.x;
+  const int seg = blockIdx.x, f = blockIdx.y, b = blockIdx.z, nseg = gridDim.x;
   const int tid = threadIdx.x;
   const int N = a.N, T = a.T, F = a.F;
   const size_t FT = (size_t)F * T;
-  for (int e = tid; e < N * M; e += BS)
-    gs[e] = a.g[(size_t)b * N * F * M + (size_t)(e / M) * F * M + (size_t)f * M + (e % M)];
+  const int ta = seg * a.TR, tb = min(T, ta + a.TR);
+  // finish the gain MU from the k_gain segment partials (fixed order)
+  for (int e = tid; e < N * M; e += BS) {
+    const int n = e / M, m = e % M;
+    const R* gp = a.gpart + ((size_t)b * F + f) * nseg * N * 2 * M + n * 2 * M;
+    R sn = 0, sd = 0;
+    for (int q = 0; q < nseg; ++q) {
+      sn += gp[(size_t)q * N * 2 * M + m];
+      sd += gp[(size_t)q * N * 2 * M + M + m];
+    }
+    const size_t gi = (size_t)b * N * F * M + (size_t)n * F * M + (size_t)f * M + m;
+    const R gv = a.g[gi] * mu_factor(sn, sd);
+    gs[e] = gv;
+    if (seg == 0) a.gnew[gi] = gv;
+  }
   if (tid < P) {
     int i = 0, r = tid;
     while (r >= M - i) {
@@ -213,121 +217,118 @@ __global__ void __launch_bounds__(VaCfg<R, M>::BS) k_vacc(VaccArgs<R> a) {
     pairs[2 * tid] = i;
     pairs[2 * tid + 1] = i + r;
   }
-  // load phase: one t per thread
-  const int t = tile * TB + tid;
-  const bool tv = tid < TB && t < T;
-  R l[NMAX];
-  C xv[M];
-  if (tid < TB) {
-    const int tc = t < T ? t : T - 1;
-    const R* lb = a.lam + (size_t)b * N * FT + (size_t)f * T + tc;
+  const R fl = a.floorp[b];
+  const R* lamb = a.lam + (size_t)b * N * FT + (size_t)f * T;
+  const C* Xb = a.X + ((size_t)b * F + f) * T * M;
+  R lp[NMAX];
+  C xp[M];
+  auto fetch = [&](int c0) {
+    const int t = c0 + tid;
+    const int tc = t < tb ? t : tb - 1;
 #pragma unroll
     for (int n = 0; n < NMAX; ++n) {
-      l[n] = R(0);
+      lp[n] = R(0);
       if (n >= N) break;
-      l[n] = lb[(size_t)n * FT];
+      lp[n] = lamb[(size_t)n * FT + tc];
     }
-    CRowIO<R, M>::load(a.X + (((size_t)b * F + f) * T + tc) * M, xv);
-  }
+    CRowIO<R, M>::load(Xb + (size_t)tc * M, xp);
+  };
+  if (tid < TB) fetch(ta);
   __syncthreads();
-  if (tid < TB) {
-    R iy[M], y[M];
-    model_power<R, M>(l, gs, N, a.floorp[b], iy, y);
-#pragma unroll
-    for (int m = 0; m < M; ++m) {
-      if (!tv) {
-        iy[m] = R(0);
-        xv[m] = cmake<C>(0.0, 0.0);
-      }
-    }
-    RowIO<R, M>::store(iys + tid * M, iy);
-    CRowIO<R, M>::store(Xc + tid * M, xv);
-  }
-  __syncthreads();
-  // accumulate: thread = (pair i <= j, slice)
   const int p = tid % P, s2 = tid / P;
   const bool act = s2 < S2;
   const int pi = pairs[2 * p], pj = pairs[2 * p + 1];
   C v[M];
 #pragma unroll
   for (int m = 0; m < M; ++m) v[m] = cmake<C>(0.0, 0.0);
-  if (act) {
-    int tl = s2;
-    for (; tl + S2 < TB; tl += 2 * S2) {
-      const C xi0 = Xc[tl * M + pi], xj0 = Xc[tl * M + pj];
-      const C xi1 = Xc[(tl + S2) * M + pi], xj1 = Xc[(tl + S2) * M + pj];
-      R iy0[M], iy1[M];
-      RowIO<R, M>::load(iys + tl * M, iy0);
-      RowIO<R, M>::load(iys + (tl + S2) * M, iy1);
-      C p0, p1;  // x_i conj(x_j)
-      p0.x = xi0.x * xj0.x + xi0.y * xj0.y;
-      p0.y = xi0.y * xj0.x - xi0.x * xj0.y;
-      p1.x = xi1.x * xj1.x + xi1.y * xj1.y;
-      p1.y = xi1.y * xj1.x - xi1.x * xj1.y;
+  for (int c0 = ta; c0 < tb; c0 += TB) {
+    if (tid < TB) {
+      const bool tv = c0 + tid < tb;
+      R l[NMAX];
+      C xv[M];
 #pragma unroll
-      for (int m = 0; m < M; ++m) {
-        v[m] = fma2(cmake<C>(iy0[m], iy0[m]), p0, v[m]);
-        v[m] = fma2(cmake<C>(iy1[m], iy1[m]), p1, v[m]);
-      }
+      for (int n = 0; n < NMAX; ++n) l[n] = lp[n];
+#pragma unroll
+      for (int m = 0; m < M; ++m) xv[m] = tv ? xp[m] : cmake<C>(0.0, 0.0);
+      if (c0 + TB < tb) fetch(c0 + TB);
+      R iy[M], y[M];
+      model_power<R, M>(l, gs, N, fl, iy, y);
+#pragma unroll
+      for (int m = 0; m < M; ++m)
+        if (!tv) iy[m] = R(0);
+      RowIO<R, M>::store(iys + tid * M, iy);
+      CRowIO<R, M>::store(Xc + tid * M, xv);
     }
-    if (tl < TB) {
-      const C xi = Xc[tl * M + pi], xj = Xc[tl * M + pj];
-      C pr;
-      pr.x = xi.x * xj.x + xi.y * xj.y;
-      pr.y = xi.y * xj.x - xi.x * xj.y;
-      R iy[M];
-      RowIO<R, M>::load(iys + tl * M, iy);
+    __syncthreads();
+    if (act) {
+      int tl = s2;
+      for (; tl + S2 < TB; tl += 2 * S2) {
+        const C xi0 = Xc[tl * M + pi], xj0 = Xc[tl * M + pj];
+        const C xi1 = Xc[(tl + S2) * M + pi], xj1 = Xc[(tl + S2) * M + pj];
+        R iy0[M], iy1[M];
+        RowIO<R, M>::load(iys + tl * M, iy0);
+        RowIO<R, M>::load(iys + (tl + S2) * M, iy1);
+        C p0, p1;  // x_i conj(x_j)
+        p0.x = xi0.x * xj0.x + xi0.y * xj0.y;
+        p0.y = xi0.y * xj0.x - xi0.x * xj0.y;
+        p1.x = xi1.x * xj1.x + xi1.y * xj1.y;
+        p1.y = xi1.y * xj1.x - xi1.x * xj1.y;
 #pragma unroll
-      for (int m = 0; m < M; ++m) v[m] = fma2(cmake<C>(iy[m], iy[m]), pr, v[m]);
-    }
-  }
-  __syncthreads();
-  // fixed-order slice reduction in smem (staging area reused)
-  C* red = reinterpret_cast<C*>(buf);
-  for (int ss = 0; ss < S2; ++ss) {
-    if (act && s2 == ss) {
-#pragma unroll
-      for (int m = 0; m < M; ++m) {
-        C* d = red + m * P + p;
-        if (ss == 0) {
-          *d = v[m];
-        } else {
-          C o = *d;
-          o.x += v[m].x;
-          o.y += v[m].y;
-          *d = o;
+        for (int m = 0; m < M; ++m) {
+          v[m] = fma2(cmake<C>(iy0[m], iy0[m]), p0, v[m]);
+          v[m] = fma2(cmake<C>(iy1[m], iy1[m]), p1, v[m]);
         }
+      }
+      if (tl < TB) {
+        const C xi = Xc[tl * M + pi], xj = Xc[tl * M + pj];
+        C pr;
+        pr.x = xi.x * xj.x + xi.y * xj.y;
+        pr.y = xi.y * xj.x - xi.x * xj.y;
+        R iy[M];
+        RowIO<R, M>::load(iys + tl * M, iy);
+#pragma unroll
+        for (int m = 0; m < M; ++m) v[m] = fma2(cmake<C>(iy[m], iy[m]), pr, v[m]);
       }
     }
     __syncthreads();
   }
-  C* pb = reinterpret_cast<C*>(a.part) + (((size_t)b * F + f) * ntile + tile) * M * P;
-  for (int e = tid; e < M * P; e += BS) pb[e] = red[e];
-  __threadfence();
-  __syncthreads();
-  if (tid == 0) {
-    unsigned* c = a.counters + (size_t)b * F + f;
-    is_last = atomicAdd(c, 1u) == (unsigned)ntile - 1;
-    if (is_last) *c = 0u;
-  }
-  __syncthreads();
-  if (!is_last) return;
-  __threadfence();
-  const double invT = 1.0 / (double)T;
-  double2* Vf = a.V + ((size_t)b * F + f) * M * M * M;
-  const C* p0 = reinterpret_cast<const C*>(a.part) + ((size_t)b * F + f) * ntile * M * P;
-  for (int e = tid; e < M * P; e += BS) {
-    double2 acc = make_double2(0.0, 0.0);
-    for (int q = 0; q < ntile; ++q) {
-      const C c = p0[(size_t)q * M * P + e];
-      acc.x += (double)c.x;
-      acc.y += (double)c.y;
+  // fixed-order slice reduction (staging area reused), then the segment partial
+  C* red = reinterpret_cast<C*>(buf);
+  C* pb = reinterpret_cast<C*>(a.part) + (((size_t)b * F + f) * nseg + seg) * M * P;
+  if constexpr (Cf::ONEPASS) {
+    if (act) {
+#pragma unroll
+      for (int m = 0; m < M; ++m) red[(s2 * M + m) * P + p] = v[m];
     }
-    const int m = e / P, pp = e % P;
-    const int i = pairs[2 * pp], j = pairs[2 * pp + 1];
-    const double2 d = make_double2(acc.x * invT, acc.y * invT);
-    Vf[((size_t)m * M + i) * M + j] = d;
-    if (i != j) Vf[((size_t)m * M + j) * M + i] = make_double2(d.x, -d.y);
+    __syncthreads();
+    for (int e = tid; e < M * P; e += BS) {
+      C acc = red[e];
+      for (int q = 1; q < S2; ++q) {
+        const C o = red[q * M * P + e];
+        acc.x += o.x;
+        acc.y += o.y;
+      }
+      pb[e] = acc;
+    }
+  } else {
+    for (int ss = 0; ss < S2; ++ss) {
+      if (act && s2 == ss) {
+#pragma unroll
+        for (int m = 0; m < M; ++m) {
+          C* d = red + m * P + p;
+          if (ss == 0) {
+            *d = v[m];
+          } else {
+            C o = *d;
+            o.x += v[m].x;
+            o.y += v[m].y;
+            *d = o;
+          }
+        }
+      }
+      __syncthreads();
+    }
+    for (int e = tid; e < M * P; e += BS) pb[e] = red[e];
   }
 }
 
@@ -338,7 +339,9 @@ __global__ void __launch_bounds__(VaCfg<R, M>::BS) k_vacc(VaccArgs<R> a) {
 // updates (one mat-vec each); all threads normalise and fold into W.
 // ---------------------------------------------------------------------------
 template <typename R> struct IpArgs {
-  const double2* V;  // (B, F, M, M, M) from k_vacc
+  const cplx<R>* Vpart;  // (B, F, nseg, M, P) partial V sums from k_vacc
+  int nseg, T;
+  const R* gnew;         // (B, N, F, M) gains after the MU (k_vacc)
   cplx<R>* Q;
   R* g;
   R* W;
@@ -395,10 +398,32 @@ __global__ void __launch_bounds__(IpCfg<M>::BS) k_ip(IpArgs<R> a) {
   R* Wg = a.W + (size_t)b * N * F * K + (size_t)f * K;
   const unsigned it = *a.iter;
   const long long fglob = a.f_offset + f;
-  const double2* Vg = a.V + ((size_t)b * F + f) * M * M * M;
-  for (int e = tid; e < M * M * M; e += BS) Vd[e] = Vg[e];
+  {  // V_f = (1/T) sum over the segment partials (fixed order, fp64), mirrored
+    constexpr int P = M * (M + 1) / 2;
+    const C* vp = a.Vpart + ((size_t)b * F + f) * a.nseg * M * P;
+    const double invT = 1.0 / (double)a.T;
+    for (int e = tid; e < M * P; e += BS) {
+      double2 acc = make_double2(0.0, 0.0);
+      for (int q = 0; q < a.nseg; ++q) {
+        const C c = vp[(size_t)q * M * P + e];
+        acc.x += (double)c.x;
+        acc.y += (double)c.y;
+      }
+      const int m = e / P;
+      int i = 0, r = e % P;
+      while (r >= M - i) {
+        r -= M - i;
+        ++i;
+      }
+      const int j = i + r;
+      const double2 d = make_double2(acc.x * invT, acc.y * invT);
+      Vd[((size_t)m * M + i) * M + j] = d;
+      if (i != j) Vd[((size_t)m * M + j) * M + i] = make_double2(d.x, -d.y);
+    }
+  }
   for (int e = tid; e < M * M; e += BS) Qd[e] = to_d2(Qg[e]);
-  for (int e = tid; e < N * M; e += BS) gs[e] = gg[(size_t)(e / M) * F * M + (e % M)];
+  for (int e = tid; e < N * M; e += BS)
+    gs[e] = a.gnew[(size_t)b * N * F * M + (size_t)(e / M) * F * M + (size_t)f * M + (e % M)];
   if (tid < NMAX) cs[tid] = R(1);
   if (tid == 0) flags[0] = flags[1] = 0;
   __syncthreads();
