@@ -37,6 +37,7 @@ CONFIGS = {
     "c2": dict(F=513, T=512, M=4, N=3, K=8, B=256, iters=100, precision="complex64"),
     "c3": dict(F=1025, T=8192, M=16, N=6, K=32, B=1, iters=100, precision="complex64"),
     "c0": dict(F=257, T=128, M=4, N=2, K=8, B=1, iters=50, precision="complex128"),
+    "c4": dict(F=513, T=512, M=8, N=2, K=32, B=1, iters=100, precision="complex64", dp=True),
 }
 METRIC = "FastMNMF TF-bin*ch updates/s (F*T*M*mixtures*iterations/s)"
 UNIT = "TF-bin*ch/s"
@@ -233,14 +234,23 @@ def main():
         loop = runner.loop
         Xs = Xl
         f_off = f0
+    elif cfg.get("dp"):
+        from paper_1903_03237_b200.dp import ExpMLPDecoder
+        from paper_1903_03237_b200.synth import dp_init, make_dp_mixture
+
+        dec = ExpMLPDecoder(F, seed=0)
+        X = torch.from_numpy(make_dp_mixture(F, T, M, K, dec, 0)).to(dev, torch.complex64)[None]
+        Q0, g0, u0, v0, z0, W0, H0 = dp_init(F, T, M, K, dec.latent_dim, 0)
+        init = tuple(torch.from_numpy(a)[None] for a in (Q0, g0, W0, H0))
+        Xs, scale, floor = _prepare_observation(X, scfg, torch)
+        loop = DeviceLoop(Xs, init[0], init[1], init[2], init[3], floor, True, 1, n_trace=iters,
+                          dp=(dec, u0, v0, z0, 10, 1e-2))
+        dp_init_dev = [t.clone() for t in (loop.dp.u, loop.dp.v, loop.dp.z)]
     else:
         Xs, scale, floor = _prepare_observation(X, scfg, torch)
         loop = DeviceLoop(Xs, init[0], init[1], init[2], init[3], floor, True, 1, n_trace=iters)
     init_dev = [t.to(dev, d.dtype) for t, d in zip(init if not sharded_f else initl,
                                                    (loop.Q, loop.g, loop.W, loop.H))]
-    if sharded_f:
-        init_dev = [init_dev[0], init_dev[1], init_dev[2], init_dev[3]]
-
     def reset():
         loop.Q.copy_(init_dev[0].reshape(loop.Q.shape))
         loop.g.copy_(init_dev[1].reshape(loop.g.shape))
@@ -248,6 +258,12 @@ def main():
         loop.H.copy_(init_dev[3].reshape(loop.H.shape))
         loop.status.fill_(-1)
         loop.iterations_done = 0
+        if loop.dp is not None:
+            for dst, src in zip((loop.dp.u, loop.dp.v, loop.dp.z), dp_init_dev):
+                dst.copy_(src)
+            loop.dp.m.zero_()
+            loop.dp.v2.zero_()
+            loop.dp.step.zero_()
 
     use_graph = not sharded_f
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
@@ -301,14 +317,14 @@ def main():
              "k_ip", "k_back"]
     acc = np.zeros(9)
     nprof = 10
-    if not sharded_f:
+    if not sharded_f and loop.dp is None:
         ms = (ctypes.c_float * 9)()
         for _ in range(nprof):
             _lib.check(lib.fm_iterate_profiled(ctypes.byref(loop.dims), ctypes.byref(loop.state), ms,
                                                _lib.stream_ptr()), "fm_iterate_profiled")
             acc += np.array(ms[:])
         acc /= nprof
-    dom = int(np.argmax(acc))
+    dom = int(np.argmax(acc)) if acc.any() else len(names) - 1
     rs = 4 if cfg["precision"] == "complex64" else 8
     Bl = cfg["B"]
     ftm = F * T * M * Bl if not sharded_f else (loop.F * T * M)
@@ -361,6 +377,8 @@ def main():
         cpu = cpu_baseline_sample(cfg)
 
     launches = args.steps * (2 + (10 if cfg['B'] == 1 else 11) * iters)
+    if cfg.get("dp"):  # 8 launches per Adam step x 10 + 2 + 17 per iteration, 4 in the prologue
+        launches = args.steps * (4 + (10 * 8 + 2 + 17) * iters)
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,

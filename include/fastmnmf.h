@@ -100,7 +100,8 @@ typedef struct fm_dims {
   int32_t dtype;    /* FM_F32 | FM_F64 */
   int32_t normalize;/* SeparatorConfig.normalize (separate.py:52) */
   int32_t ip_sweeps;/* SeparatorConfig.ip_sweeps (separate.py:53) */
-  int32_t reserved;
+  int32_t dp;       /* 1: FastMNMF-DP -- source 0 is the deep prior, W/H hold the
+                       N-1 NMF noise sources (DeepPriorPlusNmfSource, sources.py:223-271) */
 } fm_dims;
 
 typedef struct fm_state {
@@ -119,6 +120,40 @@ typedef struct fm_state {
 /* Workspace: lambda (B,N,F,T), phi (B,2,N,F,T), H-statistic partials, bin
  * partials of the log-likelihood, counters. */
 size_t fm_workspace_bytes(const fm_dims* d);
+
+/* ---- FastMNMF-DP (BASELINE config 4) ------------------------------------ */
+
+/* Deep-prior source 0: lambda_0[f,t] = u_f v_t r[t,f], r = exp(dec(z)) with the
+ * config-4 decoder dec: D -> Hd tanh -> Hd tanh -> F linear (weights as
+ * PyTorch Linear: W1 (Hd,D), W2 (Hd,Hd), W3 (F,Hd), biases b1, b2, b3), and
+ * `adam_steps` Adam steps on z per outer iteration at the reference's latent
+ * hook (separate.py:205-213) against the NLL sum(x~/y + log y) with the rest
+ * of the model frozen. All arrays device, real type of the dims' dtype. */
+typedef struct fm_dp {
+  int64_t D, Hd;
+  const void *W1, *b1, *W2, *b2, *W3, *b3;
+  void* u;        /* (B,F) */
+  void* v;        /* (B,T) */
+  void* z;        /* (B,T,D) */
+  void* r;        /* (B,T,F) decoder output */
+  void* adam_m;   /* (B,T,D) */
+  void* adam_v;   /* (B,T,D) */
+  uint32_t* adam_step; /* device counter, persists across iterations */
+  void* work;     /* fm_dp_workspace_bytes() */
+  int32_t adam_steps;
+  float lr, beta1, beta2, eps;
+} fm_dp;
+
+size_t fm_dp_workspace_bytes(const fm_dims* d, const fm_dp* p);
+/* decoder forward r = exp(dec(z)), lambda, projection and the first
+ * statistics pass (the DP analogue of fm_prologue) */
+int fm_prologue_dp(const fm_dims* d, const fm_state* s, const fm_dp* p, void* stream);
+/* one FastMNMF-DP iteration: latents (Adam), U, V, W, H steps with refreshes,
+ * gains, IP, normalisations (u absorbs c[0]), projection, statistics */
+int fm_iterate_dp(const fm_dims* d, const fm_state* s, const fm_dp* p, void* stream);
+/* n fm_iterate_dp calls, optionally from one captured CUDA graph */
+int fm_run_dp(const fm_dims* d, const fm_state* s, const fm_dp* p, int n_iterations, int use_graph,
+              void* stream);
 
 /* NmfSource.lam (sources.py:184-187): lam (B,N,F,T) = W (B,N,F,K) H (B,N,K,T). */
 int fm_nmf_lambda(const fm_dims* d, const void* W, const void* H, void* lam, void* stream);

@@ -144,8 +144,48 @@ def save_run(name, X, F, T, M, N, K_, seed, n_iter, full_images, round64=False, 
           f"{res.likelihood_trace[-1]:.6f}", flush=True)
 
 
+def save_dp(name, F, T, M, K, n_iter, adam_steps, seed=5):
+    """fastsep.run(method="fast-mnmf-dp") with the config-4 exp-MLP decoder and
+    the Adam latent hook in place of the Metropolis chain (separate.py:205-213
+    calls sources.update_latents_fast, monkeypatched here)."""
+    from oracle.fastmnmf_dp_oracle import AdamLatents, ExpMLPDecoder, dp_init, make_dp_mixture
+
+    dec = ExpMLPDecoder(F, seed=seed)
+    X = make_dp_mixture(F, T, M, K, dec, seed=seed).astype(np.complex64).astype(np.complex128)
+    Q0, g0, u0, v0, z0, W0, H0 = dp_init(F, T, M, K, dec.latent_dim, seed)
+    hook = AdamLatents(adam_steps)
+    orig = (S._build_spatial, S._build_source, SRC.update_latents_fast)
+    S._build_spatial = lambda cfg, Xs: SP.DiagSpatial(Q0.copy(), g0.copy())
+    S._build_source = lambda cfg, Xs, rng: SRC.DeepPriorPlusNmfSource(
+        SRC.DeepPriorFactors(u0.copy(), v0.copy(), z0.copy()), SRC.NmfSource(W0.copy(), H0.copy()),
+        dec)
+    SRC.update_latents_fast = hook
+    st = {}
+
+    def snap(it, loop):
+        src = loop.source
+        st.update(u=src.dp.u_F.copy(), v=src.dp.v_T.copy(), z=src.dp.z_TD.copy(),
+                  W=src.noise.W_NFK.copy(), H=src.noise.H_NKT.copy(),
+                  g=loop.spatial.g_NFM.copy(), Q=loop.spatial.Q_FMM.copy())
+
+    try:
+        cfg = fastsep.SeparatorConfig(method="fast-mnmf-dp", n_sources=2, n_basis=K,
+                                      n_iterations=n_iter, seed=0, decoder=dec,
+                                      metropolis_enabled=adam_steps > 0)
+        res = fastsep.run(cfg, X, on_iteration=snap)
+    finally:
+        S._build_spatial, S._build_source, SRC.update_latents_fast = orig
+    np.savez_compressed(os.path.join(OUT, name), shape=np.array([F, T, M, K, seed, n_iter, adam_steps]),
+                        trace=res.likelihood_trace, images=res.images_NFTM, **st)
+    print(f"{name}: LL {res.likelihood_trace[0]:.6f} -> {res.likelihood_trace[-1]:.6f}", flush=True)
+
+
 def main():
     os.makedirs(OUT, exist_ok=True)
+    if "--dp-only" in sys.argv:
+        save_dp("run_dp_mu.npz", 33, 64, 4, 8, 8, 0)
+        save_dp("run_dp_adam.npz", 33, 64, 4, 8, 8, 10)
+        return
     np.savez_compressed(os.path.join(OUT, "kernels.npz"), **kernel_cases())
     print("kernels.npz written", flush=True)
     # small end-to-end shapes (full images)
@@ -163,6 +203,8 @@ def main():
     # config 0 shape in complex64 mode (oracle fed the c64-rounded X)
     save_run("run_c0_c64.npz", X0, 257, 128, 4, 2, 8, 0, 50, False, round64=True)
     # config 1 shape, complex64-rounded X, 100 iterations
+    save_dp("run_dp_mu.npz", 33, 64, 4, 8, 8, 0)
+    save_dp("run_dp_adam.npz", 33, 64, 4, 8, 8, 10)
     if "--with-c1" in sys.argv:
         X1 = make_mixture(513, 1024, 8, 4, 16, seed=0)
         save_run("run_c1_c64.npz", X1, 513, 1024, 8, 4, 16, 0, 100, False, round64=True)

@@ -26,7 +26,7 @@ class FmDims(ctypes.Structure):
         ("B", _c_i64), ("F", _c_i64), ("T", _c_i64), ("M", _c_i64), ("N", _c_i64),
         ("K", _c_i64), ("f_offset", _c_i64), ("dtype", ctypes.c_int32),
         ("normalize", ctypes.c_int32), ("ip_sweeps", ctypes.c_int32),
-        ("reserved", ctypes.c_int32),
+        ("dp", ctypes.c_int32),
     ]
 
 
@@ -34,6 +34,17 @@ class FmState(ctypes.Structure):
     _fields_ = [
         ("X", _vp), ("xt", _vp), ("Q", _vp), ("g", _vp), ("W", _vp), ("H", _vp),
         ("floor", _vp), ("trace", _vp), ("status", _vp), ("work", _vp),
+    ]
+
+
+class FmDp(ctypes.Structure):
+    _fields_ = [
+        ("D", _c_i64), ("Hd", _c_i64),
+        ("W1", _vp), ("b1", _vp), ("W2", _vp), ("b2", _vp), ("W3", _vp), ("b3", _vp),
+        ("u", _vp), ("v", _vp), ("z", _vp), ("r", _vp), ("adam_m", _vp), ("adam_v", _vp),
+        ("adam_step", _vp), ("work", _vp),
+        ("adam_steps", ctypes.c_int32), ("lr", ctypes.c_float), ("beta1", ctypes.c_float),
+        ("beta2", ctypes.c_float), ("eps", ctypes.c_float),
     ]
 
 
@@ -53,6 +64,14 @@ SIGNATURES = [
     ("fm_wiener_fast", ctypes.c_int,
      [ctypes.c_int, _c_i64, _c_i64, _c_i64, _c_i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     ("fm_nmf_lambda", ctypes.c_int, [ctypes.POINTER(FmDims), _vp, _vp, _vp, _vp]),
+    ("fm_dp_workspace_bytes", ctypes.c_size_t, [ctypes.POINTER(FmDims), ctypes.POINTER(FmDp)]),
+    ("fm_prologue_dp", ctypes.c_int,
+     [ctypes.POINTER(FmDims), ctypes.POINTER(FmState), ctypes.POINTER(FmDp), _vp]),
+    ("fm_iterate_dp", ctypes.c_int,
+     [ctypes.POINTER(FmDims), ctypes.POINTER(FmState), ctypes.POINTER(FmDp), _vp]),
+    ("fm_run_dp", ctypes.c_int,
+     [ctypes.POINTER(FmDims), ctypes.POINTER(FmState), ctypes.POINTER(FmDp), ctypes.c_int,
+      ctypes.c_int, _vp]),
     ("fm_workspace_bytes", ctypes.c_size_t, [ctypes.POINTER(FmDims)]),
     ("fm_prologue", ctypes.c_int, [ctypes.POINTER(FmDims), ctypes.POINTER(FmState), _vp]),
     ("fm_iterate", ctypes.c_int, [ctypes.POINTER(FmDims), ctypes.POINTER(FmState), _vp]),

@@ -40,11 +40,12 @@ static int check_m(int64_t M) {
 struct GraphCache {
   fm_dims d;
   fm_state s;
+  fm_dp p;
   cudaGraphExec_t exec = nullptr;
   cudaStream_t cap = nullptr;
   bool valid = false;
 };
-static GraphCache g_graph;
+static GraphCache g_graph, g_graph_dp;
 static std::mutex g_graph_mu;
 
 }  // namespace fm
@@ -121,11 +122,13 @@ int fm_nmf_lambda(const fm_dims* d, const void* W, const void* H, void* lam, voi
 
 int fm_prologue(const fm_dims* d, const fm_state* s, void* stream) {
   if (int rc = validate_dims(d)) return rc;
+  if (d->dp) { set_error("dims.dp set: use fm_prologue_dp"); return FM_EINVAL; }
   return FM_BY_DTYPE(d->dtype, prologue(d, s, (cudaStream_t)stream));
 }
 
 int fm_iterate(const fm_dims* d, const fm_state* s, void* stream) {
   if (int rc = validate_dims(d)) return rc;
+  if (d->dp) { set_error("dims.dp set: use fm_iterate_dp"); return FM_EINVAL; }
   return FM_BY_DTYPE(d->dtype, iterate_phase(d, s, 2, nullptr, (cudaStream_t)stream));
 }
 
@@ -150,26 +153,53 @@ int fm_iterate_profiled(const fm_dims* d, const fm_state* s, float* ms_host, voi
   return rc;
 }
 
-int fm_run(const fm_dims* d, const fm_state* s, int n_iterations, int use_graph, void* stream) {
+static int validate_dp(const fm_dims* d, const fm_dp* p) {
+  if (!p) { set_error("null fm_dp"); return FM_EINVAL; }
+  if (!d->dp) { set_error("fm_dims.dp must be 1 for the deep-prior entry points"); return FM_EINVAL; }
+  if (d->N < 2) { set_error("deep-prior methods need n_sources >= 2"); return FM_EINVAL; }
+  if (p->D < 1 || p->Hd < 1) { set_error("decoder sizes D=%lld Hd=%lld", (long long)p->D, (long long)p->Hd); return FM_EINVAL; }
+  return FM_OK;
+}
+
+size_t fm_dp_workspace_bytes(const fm_dims* d, const fm_dp* p) {
+  if (validate_dims(d) || !p) return 0;
+  return dp_ws(d, p).total;
+}
+
+int fm_prologue_dp(const fm_dims* d, const fm_state* s, const fm_dp* p, void* stream) {
   if (int rc = validate_dims(d)) return rc;
+  if (int rc = validate_dp(d, p)) return rc;
+  return FM_BY_DTYPE(d->dtype, prologue_dp(d, s, p, (cudaStream_t)stream));
+}
+
+int fm_iterate_dp(const fm_dims* d, const fm_state* s, const fm_dp* p, void* stream) {
+  if (int rc = validate_dims(d)) return rc;
+  if (int rc = validate_dp(d, p)) return rc;
+  return FM_BY_DTYPE(d->dtype, iterate_dp(d, s, p, (cudaStream_t)stream));
+}
+
+// n iterations, optionally from one captured CUDA graph of a single iteration
+// (cached on the exact (dims, state[, dp]) it was captured for).
+static int run_common(GraphCache& c, const fm_dims* d, const fm_state* s, const fm_dp* p,
+                      int n_iterations, int use_graph, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
+  auto one = [&](void* strm) { return p ? fm_iterate_dp(d, s, p, strm) : fm_iterate(d, s, strm); };
   if (!use_graph) {
     for (int i = 0; i < n_iterations; ++i)
-      if (int rc = fm_iterate(d, s, stream)) return rc;
+      if (int rc = one(stream)) return rc;
     return FM_OK;
   }
   std::lock_guard<std::mutex> lk(g_graph_mu);
-  GraphCache& c = g_graph;
   const bool same = c.valid && std::memcmp(&c.d, d, sizeof(fm_dims)) == 0 &&
-                    std::memcmp(&c.s, s, sizeof(fm_state)) == 0;
+                    std::memcmp(&c.s, s, sizeof(fm_state)) == 0 &&
+                    (!p || std::memcmp(&c.p, p, sizeof(fm_dp)) == 0);
   if (!same) {
     if (c.exec) { cudaGraphExecDestroy(c.exec); c.exec = nullptr; }
     c.valid = false;
-    // first call un-captured: sets kernel attributes outside the capture
     if (!c.cap) FM_CUDA(cudaStreamCreateWithFlags(&c.cap, cudaStreamNonBlocking));
     cudaGraph_t graph = nullptr;
     FM_CUDA(cudaStreamBeginCapture(c.cap, cudaStreamCaptureModeThreadLocal));
-    int rc = fm_iterate(d, s, (void*)c.cap);
+    int rc = one((void*)c.cap);
     cudaError_t ce = cudaStreamEndCapture(c.cap, &graph);
     if (rc) { if (graph) cudaGraphDestroy(graph); return rc; }
     if (ce != cudaSuccess) { set_error("graph capture: %s", cudaGetErrorString(ce)); return FM_ECUDA; }
@@ -178,10 +208,23 @@ int fm_run(const fm_dims* d, const fm_state* s, int n_iterations, int use_graph,
     if (ce != cudaSuccess) { set_error("graph instantiate: %s", cudaGetErrorString(ce)); return FM_ECUDA; }
     c.d = *d;
     c.s = *s;
+    if (p) c.p = *p;
     c.valid = true;
   }
   for (int i = 0; i < n_iterations; ++i) FM_CUDA(cudaGraphLaunch(c.exec, st));
   return FM_OK;
+}
+
+int fm_run(const fm_dims* d, const fm_state* s, int n_iterations, int use_graph, void* stream) {
+  if (int rc = validate_dims(d)) return rc;
+  return run_common(g_graph, d, s, nullptr, n_iterations, use_graph, stream);
+}
+
+int fm_run_dp(const fm_dims* d, const fm_state* s, const fm_dp* p, int n_iterations, int use_graph,
+              void* stream) {
+  if (int rc = validate_dims(d)) return rc;
+  if (int rc = validate_dp(d, p)) return rc;
+  return run_common(g_graph_dp, d, s, p, n_iterations, use_graph, stream);
 }
 
 int fm_observation_stats(const fm_dims* d, const void* X, double* sumsq_host, double* maxsq_host,

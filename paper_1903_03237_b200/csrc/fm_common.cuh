@@ -101,6 +101,16 @@ template <typename R> __device__ __forceinline__ R floor_max(R acc, R fl) {
   return acc > fl ? acc : fl;
 }
 
+// Programmatic dependent launch (sm_90+): let the next kernel in the stream
+// start its launch now, then wait until every prerequisite grid has completed
+// and its memory is visible. A no-op for kernels launched without the PDL
+// attribute. Used at the top of every kernel of the fused iteration so launch
+// latency and CTA rasterisation overlap the previous kernel's tail.
+__device__ __forceinline__ void pdl_entry() {
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+}
+
 template <typename T> __device__ __forceinline__ T warp_sum(T v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

@@ -13,6 +13,7 @@
 #include "../../include/fastmnmf.h"
 #include "fm_kernels.cuh"
 #include "fm_ops.cuh"
+#include "fm_dp.cuh"
 
 namespace fm {
 
@@ -68,6 +69,25 @@ void set_error(const char* fmt, ...);
   else { set_error("K=%d outside the supported 1..64", (int)(Krt)); return FM_EINVAL; }
 
 inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+// Launch with programmatic stream serialisation (PDL): the kernel may begin
+// launching while its predecessor drains; it waits in pdl_entry() before
+// touching the predecessor's outputs. Works inside CUDA-graph capture.
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
 
 // Workspace plan for the fused iteration.
 struct Plan {
@@ -130,7 +150,13 @@ template <typename R> struct Impl {
   static int lambda(const fm_dims* d, const R* W, const R* H, R* lam, cudaStream_t st);
   static int gain(const fm_dims* d, const fm_state* s, cudaStream_t st);
   static int vacc(const fm_dims* d, const fm_state* s, cudaStream_t st);
-  static int ip(const fm_dims* d, const fm_state* s, cudaStream_t st);
+  static int ip(const fm_dims* d, const fm_state* s, cudaStream_t st, R* u = nullptr);
+  static int lambda_nmf(const fm_dims* d, const fm_state* s, cudaStream_t st);
+  static int phi_pass(const fm_dims* d, const fm_state* s, cudaStream_t st);
+  static int dp_forward(const fm_dims* d, const fm_dp* p, cudaStream_t st);
+  static int dp_lambda(const fm_dims* d, const fm_state* s, const fm_dp* p, cudaStream_t st);
+  static int prologue_dp(const fm_dims* d, const fm_state* s, const fm_dp* p, cudaStream_t st);
+  static int iterate_dp(const fm_dims* d, const fm_state* s, const fm_dp* p, cudaStream_t st);
   static int back(const fm_dims* d, const fm_state* s, int tail_only, int record, cudaStream_t st);
 
   static int fast_stats(int64_t F, int64_t T, int64_t M, int64_t N, const void* xt,
@@ -167,8 +193,11 @@ inline int ensure_smem(Kern k, size_t bytes) {
 
 template <typename R>
 int Impl<R>::lambda(const fm_dims* d, const R* W, const R* H, R* lam, cudaStream_t st) {
-  dim3 grid((unsigned)((d->T + 63) / 64), (unsigned)((d->F + 63) / 64), (unsigned)(d->B * d->N));
-  k_lambda<R><<<grid, 256, 0, st>>>(W, H, lam, (int)d->F, (int)d->T, (int)d->K);
+  const int n0 = d->dp ? 1 : 0;
+  dim3 grid((unsigned)((d->T + 63) / 64), (unsigned)((d->F + 63) / 64),
+            (unsigned)(d->B * (d->N - n0)));
+  launch_pdl(k_lambda<R>, grid, dim3(256), 0, st, W, H, lam, (int)d->F, (int)d->T, (int)d->K,
+             (int)d->N, n0);
   FM_CHECK_LAUNCH("k_lambda");
   return FM_OK;
 }
@@ -186,7 +215,7 @@ int Impl<R>::gain(const fm_dims* d, const fm_state* s, cudaStream_t st) {
   a.F = (int)d->F; a.T = (int)d->T; a.N = (int)d->N; a.TR = p.TR;
   dim3 grid((unsigned)p.nseg, (unsigned)d->F, (unsigned)d->B);
   FM_DISPATCH_M(d->M, {
-    k_gain<R, MM><<<grid, 256, 0, st>>>(a);
+    launch_pdl(k_gain<R, MM>, grid, dim3(256), 0, st, a);
     FM_CHECK_LAUNCH("k_gain");
   });
   return FM_OK;
@@ -207,14 +236,14 @@ int Impl<R>::vacc(const fm_dims* d, const fm_state* s, cudaStream_t st) {
   a.F = (int)d->F; a.T = (int)d->T; a.N = (int)d->N; a.TR = p.TR;
   dim3 grid((unsigned)p.nseg, (unsigned)d->F, (unsigned)d->B);
   FM_DISPATCH_M(d->M, {
-    k_vacc<R, MM><<<grid, VaCfg<R, MM>::BS, 0, st>>>(a);
+    launch_pdl(k_vacc<R, MM>, grid, dim3(VaCfg<R, MM>::BS), 0, st, a);
     FM_CHECK_LAUNCH("k_vacc");
   });
   return FM_OK;
 }
 
 template <typename R>
-int Impl<R>::ip(const fm_dims* d, const fm_state* s, cudaStream_t st) {
+int Impl<R>::ip(const fm_dims* d, const fm_state* s, cudaStream_t st, R* u) {
   const Plan p = make_plan(d);
   unsigned char* w = reinterpret_cast<unsigned char*>(s->work);
   IpArgs<R> a;
@@ -230,6 +259,8 @@ int Impl<R>::ip(const fm_dims* d, const fm_state* s, cudaStream_t st) {
   a.iter = reinterpret_cast<const unsigned*>(w + p.off_cnt) + 1;
   a.status = reinterpret_cast<unsigned long long*>(s->status);
   a.F = (int)d->F; a.N = (int)d->N; a.K = (int)d->K;
+  a.n0 = d->dp ? 1 : 0;
+  a.u = u;
   a.f_offset = d->f_offset;
   a.normalize = d->normalize;
   a.ip_sweeps = d->ip_sweeps;
@@ -237,7 +268,7 @@ int Impl<R>::ip(const fm_dims* d, const fm_state* s, cudaStream_t st) {
   FM_DISPATCH_M(d->M, {
     const size_t sm = IpSmem<R, MM>::bytes;
     if (int rc = ensure_smem(k_ip<R, MM>, sm)) return rc;
-    k_ip<R, MM><<<grid, IpCfg<MM>::BS, sm, st>>>(a);
+    launch_pdl(k_ip<R, MM>, grid, dim3(IpCfg<MM>::BS), sm, st, a);
     FM_CHECK_LAUNCH("k_ip");
   });
   return FM_OK;
@@ -266,7 +297,7 @@ int Impl<R>::back(const fm_dims* d, const fm_state* s, int tail_only, int record
   a.record = record && s->trace != nullptr;
   dim3 grid((unsigned)((d->T + 255) / 256), (unsigned)d->F, (unsigned)d->B);
   FM_DISPATCH_M(d->M, {
-    k_back<R, MM><<<grid, 256, 0, st>>>(a);
+    launch_pdl(k_back<R, MM>, grid, dim3(256), 0, st, a);
     FM_CHECK_LAUNCH("k_back");
   });
   return FM_OK;
@@ -295,7 +326,8 @@ int Impl<R>::iterate_phase(const fm_dims* d, const fm_state* s, int phase, void*
   R* W = reinterpret_cast<R*>(s->W);
   R* H = reinterpret_cast<R*>(s->H);
   const int N = (int)d->N, F = (int)d->F, T = (int)d->T, K = (int)d->K;
-  const unsigned BN = (unsigned)(d->B * d->N);
+  const int n0 = d->dp ? 1 : 0;
+  const unsigned BN = (unsigned)(d->B * (d->N - n0));
   if (phase == 0 || phase == 2) {
     // W step (separate.py:214-216 with step "W"): statistics from the phi of the
     // previous pass, MU, then the refresh with the new W (lambda + phi)
@@ -305,8 +337,8 @@ int Impl<R>::iterate_phase(const fm_dims* d, const fm_state* s, int phase, void*
         if constexpr (FTT <= 32) {
           const size_t smw = WsCfg<R, KB, FTT>::bytes;
           if (int rc = ensure_smem(k_wstats<R, KB, FTT>, smw)) return rc;
-          k_wstats<R, KB, FTT><<<dim3((unsigned)((F + FTT - 1) / FTT), BN), 256, smw, st>>>(
-              phi, H, W, N, F, T, K);
+          launch_pdl(k_wstats<R, KB, FTT>, dim3((unsigned)((F + FTT - 1) / FTT), BN), dim3(256),
+                     smw, st, phi, H, W, N, F, T, K, 0);
           FM_CHECK_LAUNCH("k_wstats");
         }
       });
@@ -315,9 +347,10 @@ int Impl<R>::iterate_phase(const fm_dims* d, const fm_state* s, int phase, void*
     if (int rc = lambda(d, W, H, lam, st)) return rc;
     FM_EV(2);
     FM_DISPATCH_M(d->M, {
-      k_phi<R, MM><<<dim3((unsigned)((T + 255) / 256), (unsigned)F, (unsigned)d->B), 256, 0, st>>>(
-          lam, reinterpret_cast<const R*>(s->xt), reinterpret_cast<const R*>(s->g),
-          reinterpret_cast<const R*>(s->floor), phi, N, F, T);
+      launch_pdl(k_phi<R, MM>, dim3((unsigned)((T + 255) / 256), (unsigned)F, (unsigned)d->B),
+                 dim3(256), 0, st, lam, reinterpret_cast<const R*>(s->xt),
+                 reinterpret_cast<const R*>(s->g), reinterpret_cast<const R*>(s->floor), phi, N, F,
+                 T);
       FM_CHECK_LAUNCH("k_phi");
     });
     // H step (separate.py:214-216 with step "H")
@@ -327,8 +360,9 @@ int Impl<R>::iterate_phase(const fm_dims* d, const fm_state* s, int phase, void*
         if constexpr (TTT >= 16) {
           const size_t smh = HsCfg<R, KB, TTT>::bytes;
           if (int rc = ensure_smem(k_hstats<R, KB, TTT>, smh)) return rc;
-          k_hstats<R, KB, TTT><<<dim3((unsigned)((T + TTT - 1) / TTT), BN), 256, smh, st>>>(
-              phi, W, H, reinterpret_cast<R*>(hstat), N, F, T, K, phase == 0 ? 1 : 0);
+          launch_pdl(k_hstats<R, KB, TTT>, dim3((unsigned)((T + TTT - 1) / TTT), BN), dim3(256),
+                     smh, st, phi, W, H, reinterpret_cast<R*>(hstat), N, F, T, K,
+                     phase == 0 ? 1 : 0, 0);
           FM_CHECK_LAUNCH("k_hstats");
         }
       });
@@ -355,17 +389,224 @@ int Impl<R>::iterate_phase(const fm_dims* d, const fm_state* s, int phase, void*
   {  // trace entry of this iteration, then advance the device iteration counter
     const unsigned* cnt = reinterpret_cast<const unsigned*>(w + p.off_cnt);
     unsigned* itp = const_cast<unsigned*>(cnt) + 1;
-    k_trace<<<(unsigned)d->B, 256, 0, st>>>(
-        reinterpret_cast<const double*>(w + p.off_llp), reinterpret_cast<const double*>(w + p.off_ldp),
-        s->trace, itp, (int)d->B, F, (T + 255) / 256, T);
+    launch_pdl(k_trace, dim3((unsigned)d->B), dim3(256), 0, st,
+               reinterpret_cast<const double*>(w + p.off_llp),
+               reinterpret_cast<const double*>(w + p.off_ldp), s->trace, itp, (int)d->B, F,
+               (T + 255) / 256, T);
     FM_CHECK_LAUNCH("k_trace");
     if (d->B > 1) {
-      k_iter_advance<<<1, 1, 0, st>>>(itp);
+      launch_pdl(k_iter_advance, dim3(1), dim3(1), 0, st, itp);
       FM_CHECK_LAUNCH("k_iter_advance");
     }
   }
   return FM_OK;
 #undef FM_EV
+}
+
+// ---------------------------------------------------------------------------
+// FastMNMF-DP (config 4)
+// ---------------------------------------------------------------------------
+struct DpWs {
+  size_t h1, h2, d1, d2, go, gz, total;
+};
+inline DpWs dp_ws(const fm_dims* d, const fm_dp* p) {
+  const size_t rs = d->dtype == FM_F64 ? 8 : 4;
+  const size_t BT = (size_t)d->B * d->T;
+  DpWs w;
+  size_t o = 0;
+  w.h1 = o; o = align256(o + BT * p->Hd * rs);
+  w.h2 = o; o = align256(o + BT * p->Hd * rs);
+  w.d1 = o; o = align256(o + BT * p->Hd * rs);
+  w.d2 = o; o = align256(o + BT * p->Hd * rs);
+  w.go = o; o = align256(o + BT * d->F * rs);
+  w.gz = o; o = align256(o + BT * p->D * rs);
+  w.total = o;
+  return w;
+}
+
+template <typename R, bool BT, int EPI>
+inline int mlp_gemm(const R* A, const R* Bm, const R* bias, const R* aux, R* Cm, int Rows, int Ncol,
+                    int K, long long sA, long long sC, int B, cudaStream_t st) {
+  dim3 grid((unsigned)((Ncol + 63) / 64), (unsigned)((Rows + 63) / 64), (unsigned)B);
+  launch_pdl(k_mlp_gemm<R, BT, EPI>, grid, dim3(256), 0, st, A, Bm, bias, aux, Cm, Rows, Ncol, K,
+             sA, sC);
+  FM_CHECK_LAUNCH("k_mlp_gemm");
+  return FM_OK;
+}
+
+template <typename R>
+int Impl<R>::dp_forward(const fm_dims* d, const fm_dp* p, cudaStream_t st) {
+  const DpWs w = dp_ws(d, p);
+  unsigned char* ws = reinterpret_cast<unsigned char*>(p->work);
+  const int T = (int)d->T, F = (int)d->F, D = (int)p->D, Hd = (int)p->Hd, B = (int)d->B;
+  R* h1 = reinterpret_cast<R*>(ws + w.h1);
+  R* h2 = reinterpret_cast<R*>(ws + w.h2);
+  if (int rc = mlp_gemm<R, true, 1>(reinterpret_cast<const R*>(p->z), reinterpret_cast<const R*>(p->W1),
+                                    reinterpret_cast<const R*>(p->b1), nullptr, h1, T, Hd, D,
+                                    (long long)T * D, (long long)T * Hd, B, st)) return rc;
+  if (int rc = mlp_gemm<R, true, 1>(h1, reinterpret_cast<const R*>(p->W2),
+                                    reinterpret_cast<const R*>(p->b2), nullptr, h2, T, Hd, Hd,
+                                    (long long)T * Hd, (long long)T * Hd, B, st)) return rc;
+  return mlp_gemm<R, true, 2>(h2, reinterpret_cast<const R*>(p->W3), reinterpret_cast<const R*>(p->b3),
+                              nullptr, reinterpret_cast<R*>(p->r), T, F, Hd, (long long)T * Hd,
+                              (long long)T * F, B, st);
+}
+
+template <typename R>
+int Impl<R>::dp_lambda(const fm_dims* d, const fm_state* s, const fm_dp* p, cudaStream_t st) {
+  const Plan pl = make_plan(d);
+  R* lam = reinterpret_cast<R*>(reinterpret_cast<unsigned char*>(s->work) + pl.off_lam);
+  dim3 grid((unsigned)((d->T + 31) / 32), (unsigned)((d->F + 31) / 32), (unsigned)d->B);
+  launch_pdl(k_dp_lambda<R>, grid, dim3(32, 8), 0, st, reinterpret_cast<const R*>(p->u),
+             reinterpret_cast<const R*>(p->v), reinterpret_cast<const R*>(p->r), lam, (int)d->N,
+             (int)d->F, (int)d->T);
+  FM_CHECK_LAUNCH("k_dp_lambda");
+  return FM_OK;
+}
+
+template <typename R>
+int Impl<R>::lambda_nmf(const fm_dims* d, const fm_state* s, cudaStream_t st) {
+  const Plan pl = make_plan(d);
+  return lambda(d, reinterpret_cast<const R*>(s->W), reinterpret_cast<const R*>(s->H),
+                reinterpret_cast<R*>(reinterpret_cast<unsigned char*>(s->work) + pl.off_lam), st);
+}
+
+template <typename R>
+int Impl<R>::phi_pass(const fm_dims* d, const fm_state* s, cudaStream_t st) {
+  const Plan pl = make_plan(d);
+  unsigned char* w = reinterpret_cast<unsigned char*>(s->work);
+  const int N = (int)d->N, F = (int)d->F, T = (int)d->T;
+  FM_DISPATCH_M(d->M, {
+    launch_pdl(k_phi<R, MM>, dim3((unsigned)((T + 255) / 256), (unsigned)F, (unsigned)d->B),
+               dim3(256), 0, st, reinterpret_cast<const R*>(w + pl.off_lam),
+               reinterpret_cast<const R*>(s->xt), reinterpret_cast<const R*>(s->g),
+               reinterpret_cast<const R*>(s->floor), reinterpret_cast<R*>(w + pl.off_phi), N, F, T);
+    FM_CHECK_LAUNCH("k_phi");
+  });
+  return FM_OK;
+}
+
+template <typename R>
+int Impl<R>::prologue_dp(const fm_dims* d, const fm_state* s, const fm_dp* p, cudaStream_t st) {
+  const Plan pl = make_plan(d);
+  unsigned char* w = reinterpret_cast<unsigned char*>(s->work);
+  FM_CUDA(cudaMemsetAsync(w + pl.off_cnt, 0, pl.total - pl.off_cnt, st));
+  if (int rc = dp_forward(d, p, st)) return rc;
+  if (int rc = dp_lambda(d, s, p, st)) return rc;
+  if (int rc = lambda_nmf(d, s, st)) return rc;
+  return back(d, s, /*tail_only=*/1, /*record=*/0, st);
+}
+
+template <typename R>
+int Impl<R>::iterate_dp(const fm_dims* d, const fm_state* s, const fm_dp* p, cudaStream_t st) {
+  const Plan pl = make_plan(d);
+  unsigned char* w = reinterpret_cast<unsigned char*>(s->work);
+  R* lam = reinterpret_cast<R*>(w + pl.off_lam);
+  R* phi = reinterpret_cast<R*>(w + pl.off_phi);
+  R* W = reinterpret_cast<R*>(s->W);
+  R* H = reinterpret_cast<R*>(s->H);
+  R* u = reinterpret_cast<R*>(p->u);
+  R* v = reinterpret_cast<R*>(p->v);
+  const R* r = reinterpret_cast<const R*>(p->r);
+  const int N = (int)d->N, F = (int)d->F, T = (int)d->T, K = (int)d->K, B = (int)d->B;
+  const int D = (int)p->D, Hd = (int)p->Hd;
+  const unsigned BN = (unsigned)(d->B * (d->N - 1));
+  const DpWs dw = dp_ws(d, p);
+  unsigned char* ws = reinterpret_cast<unsigned char*>(p->work);
+  R* h1 = reinterpret_cast<R*>(ws + dw.h1);
+  R* h2 = reinterpret_cast<R*>(ws + dw.h2);
+  R* d1 = reinterpret_cast<R*>(ws + dw.d1);
+  R* d2 = reinterpret_cast<R*>(ws + dw.d2);
+  R* go = reinterpret_cast<R*>(ws + dw.go);
+  R* gz = reinterpret_cast<R*>(ws + dw.gz);
+  // lambda of the state after the previous iteration (u absorbed c[0], W c[1:])
+  if (int rc = lambda_nmf(d, s, st)) return rc;
+  if (int rc = dp_lambda(d, s, p, st)) return rc;
+  // latent hook (separate.py:205-213): Adam on z against the frozen y_rest
+  for (int step = 0; step < p->adam_steps; ++step) {
+    if (int rc = dp_forward(d, p, st)) return rc;
+    if (int rc = dp_lambda(d, s, p, st)) return rc;
+    FM_DISPATCH_M(d->M, {
+      launch_pdl(k_dp_grad<R, MM>, dim3((unsigned)((T + 31) / 32), (unsigned)((F + 31) / 32), (unsigned)B),
+                 dim3(32, 8), 0, st, (const R*)lam, reinterpret_cast<const R*>(s->xt),
+                 reinterpret_cast<const R*>(s->g), go, N, F, T);
+      FM_CHECK_LAUNCH("k_dp_grad");
+    });
+    // backward to z: d2 = (go W3) (1 - h2^2); d1 = (d2 W2) (1 - h1^2); gz = d1 W1
+    if (int rc = mlp_gemm<R, false, 3>(go, reinterpret_cast<const R*>(p->W3), nullptr, h2, d2, T, Hd, F,
+                                       (long long)T * F, (long long)T * Hd, B, st)) return rc;
+    if (int rc = mlp_gemm<R, false, 3>(d2, reinterpret_cast<const R*>(p->W2), nullptr, h1, d1, T, Hd, Hd,
+                                       (long long)T * Hd, (long long)T * Hd, B, st)) return rc;
+    if (int rc = mlp_gemm<R, false, 0>(d1, reinterpret_cast<const R*>(p->W1), nullptr, nullptr, gz, T, D,
+                                       Hd, (long long)T * Hd, (long long)T * D, B, st)) return rc;
+    const long long nz = (long long)B * T * D;
+    launch_pdl(k_adam<R>, dim3((unsigned)((nz + 255) / 256)), dim3(256), 0, st,
+               reinterpret_cast<R*>(p->z), (const R*)gz, reinterpret_cast<R*>(p->adam_m),
+               reinterpret_cast<R*>(p->adam_v), p->adam_step, nz, p->lr, p->beta1, p->beta2, p->eps);
+    FM_CHECK_LAUNCH("k_adam");
+    launch_pdl(k_dp_tick, dim3(1), dim3(1), 0, st, p->adam_step);
+    FM_CHECK_LAUNCH("k_dp_tick");
+  }
+  if (p->adam_steps > 0) {
+    if (int rc = dp_forward(d, p, st)) return rc;  // r = dec(z) for the new latents
+    if (int rc = dp_lambda(d, s, p, st)) return rc;
+  }
+  // U step (sources.py:258-261)
+  if (int rc = phi_pass(d, s, st)) return rc;
+  launch_pdl(k_dp_umu<R>, dim3((unsigned)F, (unsigned)B), dim3(256), 0, st, u, (const R*)v, r,
+             (const R*)phi, N, F, T);
+  FM_CHECK_LAUNCH("k_dp_umu");
+  if (int rc = dp_lambda(d, s, p, st)) return rc;
+  // V step (sources.py:262-265)
+  if (int rc = phi_pass(d, s, st)) return rc;
+  launch_pdl(k_dp_vmu<R>, dim3((unsigned)((T + 31) / 32), (unsigned)B), dim3(32, 8), 0, st,
+             (const R*)u, v, r, (const R*)phi, N, F, T);
+  FM_CHECK_LAUNCH("k_dp_vmu");
+  if (int rc = dp_lambda(d, s, p, st)) return rc;
+  // W step (noise NMF, sources.py:253 -> 191-194)
+  if (int rc = phi_pass(d, s, st)) return rc;
+  FM_DISPATCH_KB(K, {
+    FM_DISPATCH_TILE(pl.FT, FTT, {
+      if constexpr (FTT <= 32) {
+        const size_t smw = WsCfg<R, KB, FTT>::bytes;
+        if (int rc = ensure_smem(k_wstats<R, KB, FTT>, smw)) return rc;
+        launch_pdl(k_wstats<R, KB, FTT>, dim3((unsigned)((F + FTT - 1) / FTT), BN), dim3(256), smw,
+                   st, (const R*)phi, (const R*)H, W, N, F, T, K, 1);
+        FM_CHECK_LAUNCH("k_wstats");
+      }
+    });
+  });
+  // H step
+  if (int rc = lambda_nmf(d, s, st)) return rc;
+  if (int rc = phi_pass(d, s, st)) return rc;
+  FM_DISPATCH_KB(K, {
+    FM_DISPATCH_TILE(pl.TT, TTT, {
+      if constexpr (TTT >= 16) {
+        const size_t smh = HsCfg<R, KB, TTT>::bytes;
+        if (int rc = ensure_smem(k_hstats<R, KB, TTT>, smh)) return rc;
+        launch_pdl(k_hstats<R, KB, TTT>, dim3((unsigned)((T + TTT - 1) / TTT), BN), dim3(256), smh,
+                   st, (const R*)phi, (const R*)W, H, (R*)nullptr, N, F, T, K, 0, 1);
+        FM_CHECK_LAUNCH("k_hstats");
+      }
+    });
+  });
+  if (int rc = lambda_nmf(d, s, st)) return rc;
+  // spatial part as in the plain iteration; k_ip folds c[0] into u
+  if (int rc = gain(d, s, st)) return rc;
+  if (int rc = vacc(d, s, st)) return rc;
+  if (int rc = ip(d, s, st, u)) return rc;
+  if (int rc = back(d, s, /*tail_only=*/0, /*record=*/1, st)) return rc;
+  unsigned* itp = reinterpret_cast<unsigned*>(w + pl.off_cnt) + 1;
+  launch_pdl(k_trace, dim3((unsigned)d->B), dim3(256), 0, st,
+             reinterpret_cast<const double*>(w + pl.off_llp),
+             reinterpret_cast<const double*>(w + pl.off_ldp), s->trace, itp, (int)d->B, F,
+             (T + 255) / 256, T);
+  FM_CHECK_LAUNCH("k_trace");
+  if (d->B > 1) {
+    launch_pdl(k_iter_advance, dim3(1), dim3(1), 0, st, itp);
+    FM_CHECK_LAUNCH("k_iter_advance");
+  }
+  return FM_OK;
 }
 
 // ---------------------------------------------------------------------------

@@ -30,14 +30,17 @@ namespace fm {
 // ---------------------------------------------------------------------------
 template <typename R>
 __global__ void __launch_bounds__(256) k_lambda(const R* __restrict__ W, const R* __restrict__ H,
-                                                R* __restrict__ lam, int F, int T, int K) {
+                                                R* __restrict__ lam, int F, int T, int K, int N,
+                                                int n0) {
+  pdl_entry();
   __shared__ __align__(16) R Ws[32][64 + 4];
   __shared__ __align__(16) R Hs[32][64 + 4];
-  const int bn = blockIdx.z;
+  const int bn = blockIdx.z;  // (b, NMF source); NMF sources are lambda sources n0..N-1
+  const int Nn = N - n0;
   const int t0 = blockIdx.x * 64, f0 = blockIdx.y * 64;
   const R* Wb = W + (size_t)bn * F * K;
   const R* Hb = H + (size_t)bn * K * T;
-  R* Lb = lam + (size_t)bn * F * T;
+  R* Lb = lam + ((size_t)(bn / Nn) * N + n0 + bn % Nn) * F * T;
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
   // 16-B vector paths need 4-element alignment of rows (fp32 only)
   const bool vec = sizeof(R) == 4 && (K % 4) == 0 && (T % 4) == 0;
@@ -112,6 +115,7 @@ template <typename R>
 __global__ void __launch_bounds__(256) k_hupdate(const R* __restrict__ part, R* __restrict__ H,
                                                  R* __restrict__ hbuf, int FC, long long NKT,
                                                  long long total, int mode) {
+  pdl_entry();
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= total) return;
   const long long b = i / NKT, r = i % NKT;

@@ -61,7 +61,9 @@ template <typename R, int KB, int FT> struct WsCfg {
 
 template <typename R, int KB, int FT>
 __global__ void __launch_bounds__(256) k_wstats(const R* __restrict__ phi, const R* __restrict__ H,
-                                                R* __restrict__ W, int N, int F, int T, int K) {
+                                                R* __restrict__ W, int N, int F, int T, int K,
+                                                int n0) {
+  pdl_entry();
   using Cf = WsCfg<R, KB, FT>;
   constexpr int TCH = Cf::TCH, LD = Cf::LD, NTH = Cf::NTH, S = Cf::S;
   constexpr int FG = FT / 4, KG = KB / 4;
@@ -72,7 +74,7 @@ __global__ void __launch_bounds__(256) k_wstats(const R* __restrict__ phi, const
   const int slot = tid % NTH, s = tid / NTH;
   const int fg = slot % FG, kg = slot / FG;
   const size_t FTs = (size_t)F * T;
-  const int b = bn / N, n = bn % N;
+  const int b = bn / (N - n0), n = n0 + bn % (N - n0);  // W/H hold the NMF sources n0..N-1
   const R* P1 = phi + ((size_t)b * 2 * N + n) * FTs;
   const R* P2 = P1 + (size_t)N * FTs;
   const R* Hn = H + (size_t)bn * K * T;
@@ -194,7 +196,8 @@ template <typename R, int KB, int TT> struct HsCfg {
 template <typename R, int KB, int TT>
 __global__ void __launch_bounds__(256) k_hstats(const R* __restrict__ phi, const R* __restrict__ W,
                                                 R* __restrict__ H, R* __restrict__ hout, int N,
-                                                int F, int T, int K, int mode) {
+                                                int F, int T, int K, int mode, int n0) {
+  pdl_entry();
   using Cf = HsCfg<R, KB, TT>;
   constexpr int FCH = Cf::FCH, NTH = Cf::NTH, S = Cf::S, LDW = Cf::LDW, LDP = Cf::LDP;
   constexpr int TG = TT / 4;
@@ -205,7 +208,8 @@ __global__ void __launch_bounds__(256) k_hstats(const R* __restrict__ phi, const
   const int slot = tid % NTH, s = tid / NTH;
   const int tg = slot % TG, kg = slot / TG;
   const size_t FTs = (size_t)F * T;
-  const int b = bn / N, n = bn % N;
+  const int Nn = N - n0;
+  const int b = bn / Nn, nl = bn % Nn, n = n0 + nl;
   const R* P1 = phi + ((size_t)b * 2 * N + n) * FTs;
   const R* P2 = P1 + (size_t)N * FTs;
   const R* Wn = W + (size_t)bn * F * K;
@@ -294,9 +298,9 @@ __global__ void __launch_bounds__(256) k_hstats(const R* __restrict__ phi, const
       if (mode == 0) {
         Hn[(size_t)k * T + t] *= mu_factor(sn, sd);  // sources.py:198
       } else {
-        const size_t NKT = (size_t)N * K * T;
-        hout[(size_t)b * 2 * NKT + (size_t)n * K * T + (size_t)k * T + t] = sn;
-        hout[(size_t)b * 2 * NKT + NKT + (size_t)n * K * T + (size_t)k * T + t] = sd;
+        const size_t NKT = (size_t)Nn * K * T;
+        hout[(size_t)b * 2 * NKT + (size_t)nl * K * T + (size_t)k * T + t] = sn;
+        hout[(size_t)b * 2 * NKT + NKT + (size_t)nl * K * T + (size_t)k * T + t] = sd;
       }
     }
   }
@@ -363,6 +367,7 @@ template <typename R, int M>
 __global__ void __launch_bounds__(256) k_phi(const R* __restrict__ lam, const R* __restrict__ xt,
                                              const R* __restrict__ g, const R* __restrict__ floorp,
                                              R* __restrict__ phi, int N, int F, int T) {
+  pdl_entry();
   __shared__ __align__(16) R gs[NMAX * M];
   const int f = blockIdx.y, b = blockIdx.z, tid = threadIdx.x;
   const int t = blockIdx.x * 256 + tid;

@@ -68,6 +68,7 @@ template <typename R, int M> struct GaCfg {
 // gain statistics (separate.py:217; _kernels.py:244-250)
 template <typename R, int M>
 __global__ void __launch_bounds__(256) k_gain(GainArgs<R> a) {
+  pdl_entry();
   constexpr int TB = GaCfg<R, M>::TB;
   __shared__ __align__(16) R lams[NMAX * (TB + 1)];
   __shared__ __align__(16) R iys[TB * M];
@@ -180,6 +181,7 @@ template <typename R> struct VaccArgs {
 // the updated gains (separate.py:221-222; spatial.py:182; _kernels.py:276-293)
 template <typename R, int M>
 __global__ void __launch_bounds__(VaCfg<R, M>::BS) k_vacc(VaccArgs<R> a) {
+  pdl_entry();
   using C = cplx<R>;
   using Cf = VaCfg<R, M>;
   constexpr int BS = Cf::BS, TB = Cf::TB, P = Cf::P, S2 = Cf::S2;
@@ -349,6 +351,8 @@ template <typename R> struct IpArgs {
   double* ld_part;
   const unsigned* iter;
   unsigned long long* status;
+  R* u;    // deep-prior scale u (B, F) when n0 == 1 (absorbs c[0], sources.py:269-271)
+  int n0;  // first NMF source (0, or 1 for FastMNMF-DP)
   int F, N, K;
   long long f_offset;
   int normalize, ip_sweeps;
@@ -374,6 +378,7 @@ template <typename R, int M> struct IpSmem {
 
 template <typename R, int M>
 __global__ void __launch_bounds__(IpCfg<M>::BS) k_ip(IpArgs<R> a) {
+  pdl_entry();
   using C = cplx<R>;
   using L = IpSmem<R, M>;
   constexpr int NW = IpCfg<M>::NW, BS = IpCfg<M>::BS;
@@ -395,7 +400,7 @@ __global__ void __launch_bounds__(IpCfg<M>::BS) k_ip(IpArgs<R> a) {
   const int N = a.N, F = a.F, K = a.K;
   C* Qg = a.Q + ((size_t)b * F + f) * M * M;
   R* gg = a.g + (size_t)b * N * F * M + (size_t)f * M;
-  R* Wg = a.W + (size_t)b * N * F * K + (size_t)f * K;
+  R* Wg = a.W + (size_t)b * (N - a.n0) * F * K + (size_t)f * K;
   const unsigned it = *a.iter;
   const long long fglob = a.f_offset + f;
   {  // V_f = (1/T) sum over the segment partials (fixed order, fp64), mirrored
@@ -571,11 +576,13 @@ __global__ void __launch_bounds__(IpCfg<M>::BS) k_ip(IpArgs<R> a) {
       cs[tid] = s / R(M);
     }
     __syncthreads();
-    for (int e = tid; e < N * K; e += BS) {
+    const int Nn = N - a.n0;
+    for (int e = tid; e < Nn * K; e += BS) {
       const int n = e / K, k = e % K;
       R* wp = Wg + (size_t)n * F * K + k;
-      *wp = *wp * cs[n];
+      *wp = *wp * cs[a.n0 + n];
     }
+    if (a.n0 && tid == 0) a.u[(size_t)b * F + f] *= cs[0];
   }
   for (int e = tid; e < M * M; e += BS) Qg[e] = cmake<C>(Qd[e].x, Qd[e].y);
   for (int e = tid; e < N * M; e += BS) gg[(size_t)(e / M) * F * M + (e % M)] = gs[e];
@@ -608,6 +615,7 @@ template <typename R> struct BackArgs {
 // ll_part is (B, F, tiles) and reduced in fixed order by the last tile.
 template <typename R, int M>
 __global__ void __launch_bounds__(256, 3) k_back(BackArgs<R> a) {
+  pdl_entry();
   using C = cplx<R>;
   __shared__ __align__(16) C Qr[M * M];
   __shared__ __align__(16) R gs[NMAX * M];
@@ -680,6 +688,7 @@ static __global__ void __launch_bounds__(256) k_trace(const double* __restrict__
                                                const double* __restrict__ ld_part,
                                                double* __restrict__ trace, unsigned* iter, int B,
                                                int F, int ntile, int T) {
+  pdl_entry();
   __shared__ double r1[8], r2[8];
   const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const size_t n1 = (size_t)F * ntile;
@@ -707,6 +716,7 @@ static __global__ void __launch_bounds__(256) k_trace(const double* __restrict__
   }
 }
 
-static __global__ void k_iter_advance(unsigned* iter) { *iter += 1u; }
+static __global__ void k_iter_advance(unsigned* iter) {
+  pdl_entry(); *iter += 1u; }
 
 }  // namespace fm

@@ -20,7 +20,7 @@ from .errors import InvalidInputError, NumericalBreakdownError, SingularMatrixEr
 METHODS = ("fca", "mnmf", "mnmf-dp", "fast-fca", "fast-mnmf", "fast-mnmf-dp")  # separate.py:39
 FAST_METHODS = ("fast-fca", "fast-mnmf", "fast-mnmf-dp")
 DP_METHODS = ("mnmf-dp", "fast-mnmf-dp")
-SUPPORTED_METHODS = ("fast-mnmf",)  # the hot path this backend provides
+SUPPORTED_METHODS = ("fast-mnmf", "fast-mnmf-dp")  # the hot path this backend provides
 PRECISIONS = ("complex128", "complex64")
 
 
@@ -58,6 +58,11 @@ class SeparatorConfig:
     precision: str = "complex128"
     use_graph: bool = True
     device: str = "cuda"
+    # FastMNMF-DP latent update (BASELINE config 4): Adam steps on z per outer
+    # iteration in place of the reference's Metropolis chain; disabled, like
+    # the chain, by metropolis_enabled=False
+    adam_steps: int = 10
+    adam_lr: float = 1e-2
 
     def validate(self):  # separate.py:59-71
         if self.method not in METHODS:
@@ -153,13 +158,14 @@ class DeviceLoop:
     """
 
     def __init__(self, X, Q, g, W, H, floor, normalize=True, ip_sweeps=1, n_trace=1,
-                 f_offset=0, hstat_allreduce=None):
+                 f_offset=0, hstat_allreduce=None, dp=None):
         torch = _torch()
         self.torch = torch
         self.X = X
         self.real = torch.float32 if X.dtype == torch.complex64 else torch.float64
         self.B, self.F, self.T, self.M = X.shape
-        self.N, self.K = W.shape[1], W.shape[3]
+        self.dp_args = dp  # (decoder, u, v, z, adam_steps, lr) for FastMNMF-DP
+        self.N, self.K = W.shape[1] + (1 if dp is not None else 0), W.shape[3]
         dev = X.device
         self.Q = Q.to(dev, X.dtype).resolve_conj().contiguous()
         self.g = g.to(dev, self.real).contiguous()
@@ -172,7 +178,7 @@ class DeviceLoop:
         self.status = torch.full((1,), -1, dtype=torch.int64, device=dev)
         self.dims = _lib.FmDims(self.B, self.F, self.T, self.M, self.N, self.K, int(f_offset),
                                 _lib.FM_F32 if self.real == torch.float32 else _lib.FM_F64,
-                                int(bool(normalize)), int(ip_sweeps), 0)
+                                int(bool(normalize)), int(ip_sweeps), int(dp is not None))
         lib = _lib.load()
         nbytes = lib.fm_workspace_bytes(ctypes.byref(self.dims))
         if nbytes == 0:
@@ -185,6 +191,12 @@ class DeviceLoop:
         self.hstat = (torch.empty((self.B, 2, self.N, self.K, self.T), device=dev, dtype=self.real)
                       if hstat_allreduce is not None else None)
         self.iterations_done = 0
+        self.dp = None
+        if dp is not None:
+            from .dp import DeviceDP
+
+            decoder, u, v, z, steps, lr = dp
+            self.dp = DeviceDP(decoder, u, v, z, self.dims, self.real, dev, adam_steps=steps, lr=lr)
         self.spatial = _SpatialView(self, 0)
         self.source = _SourceView(self, 0)
 
@@ -200,10 +212,17 @@ class DeviceLoop:
         lib = _lib.load()
         _lib.check(lib.fm_nmf_lambda(ctypes.byref(self.dims), _lib.ptr(self.W), _lib.ptr(self.H),
                                      _lib.ptr(lam), _lib.stream_ptr()), "fm_nmf_lambda")
+        if self.dp is not None:  # source 0: u v r (sources.py:248-249)
+            lam[:, 0] = self.dp.lam0()
         return lam
 
     def prologue(self):
         lib = _lib.load()
+        if self.dp is not None:
+            _lib.check(lib.fm_prologue_dp(ctypes.byref(self.dims), ctypes.byref(self.state),
+                                          ctypes.byref(self.dp.struct), _lib.stream_ptr()),
+                       "fm_prologue_dp")
+            return
         _lib.check(lib.fm_prologue(ctypes.byref(self.dims), ctypes.byref(self.state),
                                    _lib.stream_ptr()), "fm_prologue")
 
@@ -211,7 +230,11 @@ class DeviceLoop:
         lib = _lib.load()
         if self.iterations_done + n > self.n_trace:
             raise InvalidInputError("trace buffer too small for the requested iterations")
-        if self.hstat_allreduce is None:
+        if self.dp is not None:
+            _lib.check(lib.fm_run_dp(ctypes.byref(self.dims), ctypes.byref(self.state),
+                                     ctypes.byref(self.dp.struct), int(n), int(bool(use_graph)),
+                                     _lib.stream_ptr()), "fm_run_dp")
+        elif self.hstat_allreduce is None:
             _lib.check(lib.fm_run(ctypes.byref(self.dims), ctypes.byref(self.state), int(n),
                                   int(bool(use_graph)), _lib.stream_ptr()), "fm_run")
         else:
@@ -247,7 +270,7 @@ class DeviceLoop:
 # initialisation (separate.py:246-264)
 # ---------------------------------------------------------------------------
 
-def default_init(cfg, Xs, rng):
+def default_init(cfg, Xs, rng, n_nmf=None):
     """Reference default init: circular spatial init (spatial.py:109-121) and
     NmfSource.random (sources.py:177-182) drawn from the run's rng.
 
@@ -278,8 +301,9 @@ def default_init(cfg, Xs, rng):
     else:  # "observed": init_spatial diagonalizable (spatial.py:100-105)
         g = torch.ones((N, F, M), dtype=torch.float64, device=Xd.device)
         g[0] = torch.maximum(w, w.max(dim=-1, keepdim=True).values * 1e-12)
-    Wn = rng.uniform(0.1, 1.1, (N, F, cfg.n_basis))  # sources.py:180-181
-    Hn = rng.uniform(0.1, 1.1, (N, cfg.n_basis, T))
+    Nn = N if n_nmf is None else n_nmf  # DP: the noise NMF holds n_sources - 1
+    Wn = rng.uniform(0.1, 1.1, (Nn, F, cfg.n_basis))  # sources.py:180-181
+    Hn = rng.uniform(0.1, 1.1, (Nn, cfg.n_basis, T))
     return Q, g, torch.from_numpy(Wn), torch.from_numpy(Hn)
 
 
@@ -355,13 +379,32 @@ def run(cfg: SeparatorConfig, X_FTM, on_iteration=None, init=None) -> Separation
         raise InvalidInputError(f"observation must have shape (F, T, M), got {tuple(X_FTM.shape)}")
     Xs, scale, floor = _prepare_observation(X_FTM, cfg, torch)
     rng = np.random.default_rng(cfg.seed)  # separate.py:295
-    if init is None:
+    dp = None
+    if cfg.method == "fast-mnmf-dp":
+        from .dp import ExpMLPDecoder
+
+        F, T = Xs.shape[1], Xs.shape[2]
+        decoder = cfg.decoder if cfg.decoder is not None else ExpMLPDecoder(F, seed=cfg.seed)
+        if getattr(decoder, "n_freq", F) != F:  # separate.py:266-270
+            raise InvalidInputError(f"decoder output length {decoder.n_freq} does not match F={F}")
+        if not all(hasattr(decoder, a) for a in ("W1", "W2", "W3", "b1", "b2", "b3")):
+            raise InvalidInputError("the B200 deep prior needs an ExpMLPDecoder-style decoder "
+                                    "(weights W1, b1, W2, b2, W3, b3)")
+        if init is None:
+            Q0, g0, W0, H0 = default_init(cfg, Xs[0], rng, n_nmf=cfg.n_sources - 1)
+            u0, v0 = np.ones(F), np.ones(T)  # DeepPriorPlusNmfSource.init (sources.py:240-244)
+            z0 = np.zeros((T, decoder.latent_dim))
+        else:
+            Q0, g0, u0, v0, z0, W0, H0 = init
+        steps = cfg.adam_steps if cfg.metropolis_enabled else 0
+        dp = (decoder, u0, v0, z0, steps, cfg.adam_lr)
+    elif init is None:
         Q0, g0, W0, H0 = default_init(cfg, Xs[0], rng)
     else:
         Q0, g0, W0, H0 = init
     loop = DeviceLoop(Xs, _as_batch(Q0, torch, 1), _as_batch(g0, torch, 1),
                       _as_batch(W0, torch, 1), _as_batch(H0, torch, 1), floor,
-                      cfg.normalize, cfg.ip_sweeps, n_trace=cfg.n_iterations)
+                      cfg.normalize, cfg.ip_sweeps, n_trace=cfg.n_iterations, dp=dp)
     loop.X_FTM = Xs[0]
     loop.floor_value = float(floor[0])
     loop.prologue()

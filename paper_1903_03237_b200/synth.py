@@ -26,6 +26,8 @@ CONFIGS = {
     "c1": dict(F=513, T=1024, M=8, N=4, K=16, precision="complex64", iterations=100, batch=1),
     "c2": dict(F=513, T=512, M=4, N=3, K=8, precision="complex64", iterations=100, batch=256),
     "c3": dict(F=1025, T=8192, M=16, N=6, K=32, precision="complex64", iterations=100, batch=1),
+    # FastMNMF-DP: speech (deep prior, D=16 -> 128 -> 128 -> F) + NMF noise K=32
+    "c4": dict(F=513, T=512, M=8, N=2, K=32, precision="complex64", iterations=100, batch=1),
 }
 
 
@@ -78,3 +80,35 @@ def baseline_init(F, T, M, N, K, seed=0):
     W = rng.uniform(0.0, 1.0, (N, F, K))
     H = rng.uniform(0.0, 1.0, (N, K, T))
     return Q, g, W, H
+
+
+def make_dp_mixture(F, T, M, K, decoder, seed=0):
+    """BASELINE config 4: speech PSD u v exp(dec(z)) at z ~ N(0, I) with
+    u = v = 1, noise NMF K (Gamma(1,1)), otherwise the config-0 generator."""
+    rng = np.random.default_rng(seed)
+    z = rng.standard_normal((T, decoder.latent_dim))
+    lam0 = decoder(z).T
+    Wn = rng.gamma(1.0, 1.0, (F, K))
+    Hn = rng.gamma(1.0, 1.0, (K, T))
+    lam = np.stack([lam0, Wn @ Hn])
+    A = (rng.standard_normal((2, F, M, M)) + 1j * rng.standard_normal((2, F, M, M))) / np.sqrt(2.0)
+    R = A @ np.conj(A.swapaxes(-1, -2)) + 1e-3 * np.eye(M)
+    L = np.linalg.cholesky(R)
+    X = np.zeros((F, T, M), dtype=np.complex128)
+    for n in range(2):
+        zz = (rng.standard_normal((F, T, M)) + 1j * rng.standard_normal((F, T, M))) / np.sqrt(2.0)
+        X += np.sqrt(lam[n])[..., None] * np.einsum("fij,ftj->fti", L[n], zz)
+    return X
+
+
+def dp_init(F, T, M, K, latent_dim=16, seed=0):
+    """(Q, g, u, v, z, W, H) for config 4: Q = I, one-hot g (N = 2) with the
+    1e-2 floor, u = v = 1, z = 0, noise W, H ~ U(0,1) from default_rng(seed)."""
+    rng = np.random.default_rng(seed)
+    Q = np.tile(np.eye(M, dtype=np.complex128), (F, 1, 1))
+    g = np.full((2, F, M), 1e-2)
+    for m in range(M):
+        g[m % 2, :, m] = 1.0
+    W = rng.uniform(0.0, 1.0, (1, F, K))
+    H = rng.uniform(0.0, 1.0, (1, K, T))
+    return Q, g, np.ones(F), np.ones(T), np.zeros((T, latent_dim)), W, H

@@ -28,6 +28,7 @@ def test_library_exports_header():
 def test_structs_match_header_layout():
     assert ctypes.sizeof(_lib.FmDims) == 7 * 8 + 4 * 4
     assert ctypes.sizeof(_lib.FmState) == 10 * 8
+    assert ctypes.sizeof(_lib.FmDp) == 2 * 8 + 14 * 8 + 5 * 4 + 4  # padded to 8
 
 
 def test_version_and_validation_without_gpu():
