@@ -138,7 +138,8 @@ typedef struct fm_dp {
   void* r;        /* (B,T,F) decoder output */
   void* adam_m;   /* (B,T,D) */
   void* adam_v;   /* (B,T,D) */
-  uint32_t* adam_step; /* device counter, persists across iterations */
+  uint32_t* adam_step; /* unused (reserved); the Adam step index is
+                          iteration * adam_steps + s + 1 from the device counter */
   void* work;     /* fm_dp_workspace_bytes() */
   int32_t adam_steps;
   float lr, beta1, beta2, eps;

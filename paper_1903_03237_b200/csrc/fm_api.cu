@@ -157,7 +157,11 @@ static int validate_dp(const fm_dims* d, const fm_dp* p) {
   if (!p) { set_error("null fm_dp"); return FM_EINVAL; }
   if (!d->dp) { set_error("fm_dims.dp must be 1 for the deep-prior entry points"); return FM_EINVAL; }
   if (d->N < 2) { set_error("deep-prior methods need n_sources >= 2"); return FM_EINVAL; }
-  if (p->D < 1 || p->Hd < 1) { set_error("decoder sizes D=%lld Hd=%lld", (long long)p->D, (long long)p->Hd); return FM_EINVAL; }
+  if (p->D < 1 || p->Hd < 1 || p->D > DEC_DMAX || p->Hd > DEC_HMAX) {
+    set_error("decoder sizes D=%lld Hd=%lld outside 1..%d / 1..%d", (long long)p->D, (long long)p->Hd,
+              DEC_DMAX, DEC_HMAX);
+    return FM_EINVAL;
+  }
   return FM_OK;
 }
 

@@ -424,12 +424,13 @@ inline DpWs dp_ws(const fm_dims* d, const fm_dp* p) {
   return w;
 }
 
-template <typename R, bool BT, int EPI>
+template <typename R, bool BT, int EPI, int TM = 32, int TN = 32>
 inline int mlp_gemm(const R* A, const R* Bm, const R* bias, const R* aux, R* Cm, int Rows, int Ncol,
-                    int K, long long sA, long long sC, int B, cudaStream_t st) {
-  dim3 grid((unsigned)((Ncol + 63) / 64), (unsigned)((Rows + 63) / 64), (unsigned)B);
-  launch_pdl(k_mlp_gemm<R, BT, EPI>, grid, dim3(256), 0, st, A, Bm, bias, aux, Cm, Rows, Ncol, K,
-             sA, sC);
+                    int K, long long sA, long long sC, int B, cudaStream_t st,
+                    AdamEpi<R> ad = AdamEpi<R>{}) {
+  dim3 grid((unsigned)((Ncol + TN - 1) / TN), (unsigned)((Rows + TM - 1) / TM), (unsigned)B);
+  launch_pdl(k_mlp_gemm<R, BT, EPI, TM, TN>, grid, dim3(256), 0, st, A, Bm, bias, aux, Cm, Rows, Ncol,
+             K, sA, sC, ad);
   FM_CHECK_LAUNCH("k_mlp_gemm");
   return FM_OK;
 }
@@ -441,12 +442,11 @@ int Impl<R>::dp_forward(const fm_dims* d, const fm_dp* p, cudaStream_t st) {
   const int T = (int)d->T, F = (int)d->F, D = (int)p->D, Hd = (int)p->Hd, B = (int)d->B;
   R* h1 = reinterpret_cast<R*>(ws + w.h1);
   R* h2 = reinterpret_cast<R*>(ws + w.h2);
-  if (int rc = mlp_gemm<R, true, 1>(reinterpret_cast<const R*>(p->z), reinterpret_cast<const R*>(p->W1),
-                                    reinterpret_cast<const R*>(p->b1), nullptr, h1, T, Hd, D,
-                                    (long long)T * D, (long long)T * Hd, B, st)) return rc;
-  if (int rc = mlp_gemm<R, true, 1>(h1, reinterpret_cast<const R*>(p->W2),
-                                    reinterpret_cast<const R*>(p->b2), nullptr, h2, T, Hd, Hd,
-                                    (long long)T * Hd, (long long)T * Hd, B, st)) return rc;
+  launch_pdl(k_dec_fwd12<R>, dim3((unsigned)((T + DEC_RT - 1) / DEC_RT), (unsigned)B), dim3(256), 0, st,
+             reinterpret_cast<const R*>(p->z), reinterpret_cast<const R*>(p->W1),
+             reinterpret_cast<const R*>(p->b1), reinterpret_cast<const R*>(p->W2),
+             reinterpret_cast<const R*>(p->b2), h1, h2, T, D, Hd);
+  FM_CHECK_LAUNCH("k_dec_fwd12");
   return mlp_gemm<R, true, 2>(h2, reinterpret_cast<const R*>(p->W3), reinterpret_cast<const R*>(p->b3),
                               nullptr, reinterpret_cast<R*>(p->r), T, F, Hd, (long long)T * Hd,
                               (long long)T * F, B, st);
@@ -515,37 +515,33 @@ int Impl<R>::iterate_dp(const fm_dims* d, const fm_state* s, const fm_dp* p, cud
   unsigned char* ws = reinterpret_cast<unsigned char*>(p->work);
   R* h1 = reinterpret_cast<R*>(ws + dw.h1);
   R* h2 = reinterpret_cast<R*>(ws + dw.h2);
-  R* d1 = reinterpret_cast<R*>(ws + dw.d1);
   R* d2 = reinterpret_cast<R*>(ws + dw.d2);
   R* go = reinterpret_cast<R*>(ws + dw.go);
-  R* gz = reinterpret_cast<R*>(ws + dw.gz);
   // lambda of the state after the previous iteration (u absorbed c[0], W c[1:])
   if (int rc = lambda_nmf(d, s, st)) return rc;
   if (int rc = dp_lambda(d, s, p, st)) return rc;
   // latent hook (separate.py:205-213): Adam on z against the frozen y_rest
+  const unsigned* iterp = reinterpret_cast<const unsigned*>(w + pl.off_cnt) + 1;
   for (int step = 0; step < p->adam_steps; ++step) {
     if (int rc = dp_forward(d, p, st)) return rc;
-    if (int rc = dp_lambda(d, s, p, st)) return rc;
     FM_DISPATCH_M(d->M, {
       launch_pdl(k_dp_grad<R, MM>, dim3((unsigned)((T + 31) / 32), (unsigned)((F + 31) / 32), (unsigned)B),
-                 dim3(32, 8), 0, st, (const R*)lam, reinterpret_cast<const R*>(s->xt),
-                 reinterpret_cast<const R*>(s->g), go, N, F, T);
+                 dim3(32, 8), 0, st, (const R*)u, (const R*)v, r, (const R*)lam,
+                 reinterpret_cast<const R*>(s->xt), reinterpret_cast<const R*>(s->g), go, N, F, T);
       FM_CHECK_LAUNCH("k_dp_grad");
     });
-    // backward to z: d2 = (go W3) (1 - h2^2); d1 = (d2 W2) (1 - h1^2); gz = d1 W1
-    if (int rc = mlp_gemm<R, false, 3>(go, reinterpret_cast<const R*>(p->W3), nullptr, h2, d2, T, Hd, F,
-                                       (long long)T * F, (long long)T * Hd, B, st)) return rc;
-    if (int rc = mlp_gemm<R, false, 3>(d2, reinterpret_cast<const R*>(p->W2), nullptr, h1, d1, T, Hd, Hd,
-                                       (long long)T * Hd, (long long)T * Hd, B, st)) return rc;
-    if (int rc = mlp_gemm<R, false, 0>(d1, reinterpret_cast<const R*>(p->W1), nullptr, nullptr, gz, T, D,
-                                       Hd, (long long)T * Hd, (long long)T * D, B, st)) return rc;
-    const long long nz = (long long)B * T * D;
-    launch_pdl(k_adam<R>, dim3((unsigned)((nz + 255) / 256)), dim3(256), 0, st,
-               reinterpret_cast<R*>(p->z), (const R*)gz, reinterpret_cast<R*>(p->adam_m),
-               reinterpret_cast<R*>(p->adam_v), p->adam_step, nz, p->lr, p->beta1, p->beta2, p->eps);
-    FM_CHECK_LAUNCH("k_adam");
-    launch_pdl(k_dp_tick, dim3(1), dim3(1), 0, st, p->adam_step);
-    FM_CHECK_LAUNCH("k_dp_tick");
+    // backward to z: d2 = (go W3) (1 - h2^2) (tiled, F-long reduction), then
+    // d1 = (d2 W2) (1 - h1^2) and Adam(z, d1 W1) fused per 32-frame tile
+    if (int rc = mlp_gemm<R, false, 3, 16, 16>(go, reinterpret_cast<const R*>(p->W3), nullptr, h2, d2, T,
+                                               Hd, F, (long long)T * F, (long long)T * Hd, B, st))
+      return rc;
+    AdamEpi<R> ad{reinterpret_cast<R*>(p->z), reinterpret_cast<R*>(p->adam_m),
+                  reinterpret_cast<R*>(p->adam_v), iterp, step, p->adam_steps, p->lr, p->beta1,
+                  p->beta2, p->eps};
+    launch_pdl(k_dec_bwd21<R>, dim3((unsigned)((T + DEC_RT - 1) / DEC_RT), (unsigned)B), dim3(256), 0,
+               st, (const R*)d2, (const R*)h1, reinterpret_cast<const R*>(p->W1),
+               reinterpret_cast<const R*>(p->W2), T, D, Hd, ad);
+    FM_CHECK_LAUNCH("k_dec_bwd21");
   }
   if (p->adam_steps > 0) {
     if (int rc = dp_forward(d, p, st)) return rc;  // r = dec(z) for the new latents
