@@ -1,4 +1,4 @@
 ARGS="--config c4 --steps 1 --warmup 3 --iters 2 --no-e2e --no-cpu-baseline"
 timeout 300 python bench.py $ARGS > gpurun_out/plain11.log 2>&1 && \
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -s 300 -c 200 --csv --log-file gpurun_out/launches_c4.csv python bench.py $ARGS > gpurun_out/ncu11.log 2>&1
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -s 60 -c 100 --csv --log-file gpurun_out/launches_c4.csv python bench.py $ARGS > gpurun_out/ncu11.log 2>&1
 echo done

@@ -162,6 +162,16 @@ static int validate_dp(const fm_dims* d, const fm_dp* p) {
               DEC_DMAX, DEC_HMAX);
     return FM_EINVAL;
   }
+  if (p->D % 4 || p->Hd % 4) {
+    set_error("decoder sizes D=%lld Hd=%lld must be multiples of 4", (long long)p->D, (long long)p->Hd);
+    return FM_EINVAL;
+  }
+  const void* wp[] = {p->W1, p->W2, p->W3};
+  for (const void* q : wp)
+    if (reinterpret_cast<uintptr_t>(q) % 16) {
+      set_error("decoder weights must be 16-byte aligned");
+      return FM_EINVAL;
+    }
   return FM_OK;
 }
 

@@ -13,7 +13,7 @@
 #include "../../include/fastmnmf.h"
 #include "fm_kernels.cuh"
 #include "fm_ops.cuh"
-#include "fm_dp.cuh"
+#include "fm_dp_latent.cuh"
 
 namespace fm {
 
@@ -153,7 +153,7 @@ template <typename R> struct Impl {
   static int ip(const fm_dims* d, const fm_state* s, cudaStream_t st, R* u = nullptr);
   static int lambda_nmf(const fm_dims* d, const fm_state* s, cudaStream_t st);
   static int phi_pass(const fm_dims* d, const fm_state* s, cudaStream_t st);
-  static int dp_forward(const fm_dims* d, const fm_dp* p, cudaStream_t st);
+  static int dp_latent(const fm_dims* d, const fm_state* s, const fm_dp* p, int steps, cudaStream_t st);
   static int dp_lambda(const fm_dims* d, const fm_state* s, const fm_dp* p, cudaStream_t st);
   static int prologue_dp(const fm_dims* d, const fm_state* s, const fm_dp* p, cudaStream_t st);
   static int iterate_dp(const fm_dims* d, const fm_state* s, const fm_dp* p, cudaStream_t st);
@@ -435,21 +435,48 @@ inline int mlp_gemm(const R* A, const R* Bm, const R* bias, const R* aux, R* Cm,
   return FM_OK;
 }
 
+// The latent hook in one launch (fm_dp_latent.cuh): `steps` Adam steps and the
+// refresh r = exp(dec(z)); steps = 0 is the refresh alone.
 template <typename R>
-int Impl<R>::dp_forward(const fm_dims* d, const fm_dp* p, cudaStream_t st) {
-  const DpWs w = dp_ws(d, p);
-  unsigned char* ws = reinterpret_cast<unsigned char*>(p->work);
-  const int T = (int)d->T, F = (int)d->F, D = (int)p->D, Hd = (int)p->Hd, B = (int)d->B;
-  R* h1 = reinterpret_cast<R*>(ws + w.h1);
-  R* h2 = reinterpret_cast<R*>(ws + w.h2);
-  launch_pdl(k_dec_fwd12<R>, dim3((unsigned)((T + DEC_RT - 1) / DEC_RT), (unsigned)B), dim3(256), 0, st,
-             reinterpret_cast<const R*>(p->z), reinterpret_cast<const R*>(p->W1),
-             reinterpret_cast<const R*>(p->b1), reinterpret_cast<const R*>(p->W2),
-             reinterpret_cast<const R*>(p->b2), h1, h2, T, D, Hd);
-  FM_CHECK_LAUNCH("k_dec_fwd12");
-  return mlp_gemm<R, true, 2>(h2, reinterpret_cast<const R*>(p->W3), reinterpret_cast<const R*>(p->b3),
-                              nullptr, reinterpret_cast<R*>(p->r), T, F, Hd, (long long)T * Hd,
-                              (long long)T * F, B, st);
+int Impl<R>::dp_latent(const fm_dims* d, const fm_state* s, const fm_dp* p, int steps, cudaStream_t st) {
+  const Plan pl = make_plan(d);
+  unsigned char* w = reinterpret_cast<unsigned char*>(s->work);
+  LatentArgs<R> a;
+  a.W1 = reinterpret_cast<const R*>(p->W1);
+  a.b1 = reinterpret_cast<const R*>(p->b1);
+  a.W2 = reinterpret_cast<const R*>(p->W2);
+  a.b2 = reinterpret_cast<const R*>(p->b2);
+  a.W3 = reinterpret_cast<const R*>(p->W3);
+  a.b3 = reinterpret_cast<const R*>(p->b3);
+  a.u = reinterpret_cast<const R*>(p->u);
+  a.v = reinterpret_cast<const R*>(p->v);
+  a.z = reinterpret_cast<R*>(p->z);
+  a.m = reinterpret_cast<R*>(p->adam_m);
+  a.v2 = reinterpret_cast<R*>(p->adam_v);
+  a.r = reinterpret_cast<R*>(p->r);
+  a.lam = reinterpret_cast<const R*>(w + pl.off_lam);
+  a.xt = reinterpret_cast<const R*>(s->xt);
+  a.g = reinterpret_cast<const R*>(s->g);
+  a.iter = reinterpret_cast<const unsigned*>(w + pl.off_cnt) + 1;
+  a.T = (int)d->T;
+  a.F = (int)d->F;
+  a.D = (int)p->D;
+  a.Hd = (int)p->Hd;
+  a.N = (int)d->N;
+  a.steps = steps;
+  a.lr = p->lr;
+  a.b1a = p->beta1;
+  a.b2a = p->beta2;
+  a.eps = p->eps;
+  constexpr int FR = 4;
+  dim3 grid((unsigned)((d->T + FR - 1) / FR), (unsigned)d->B);
+  FM_DISPATCH_M(d->M, {
+    const size_t sm = sizeof(R) * LtCfg<R, MM, FR>::TOTAL;
+    if (int rc = ensure_smem(k_dp_latent<R, MM, FR>, sm)) return rc;
+    launch_pdl(k_dp_latent<R, MM, FR>, grid, dim3(LT_NT), sm, st, a);
+    FM_CHECK_LAUNCH("k_dp_latent");
+  });
+  return FM_OK;
 }
 
 template <typename R>
@@ -491,7 +518,7 @@ int Impl<R>::prologue_dp(const fm_dims* d, const fm_state* s, const fm_dp* p, cu
   const Plan pl = make_plan(d);
   unsigned char* w = reinterpret_cast<unsigned char*>(s->work);
   FM_CUDA(cudaMemsetAsync(w + pl.off_cnt, 0, pl.total - pl.off_cnt, st));
-  if (int rc = dp_forward(d, p, st)) return rc;
+  if (int rc = dp_latent(d, s, p, 0, st)) return rc;
   if (int rc = dp_lambda(d, s, p, st)) return rc;
   if (int rc = lambda_nmf(d, s, st)) return rc;
   return back(d, s, /*tail_only=*/1, /*record=*/0, st);
@@ -501,7 +528,6 @@ template <typename R>
 int Impl<R>::iterate_dp(const fm_dims* d, const fm_state* s, const fm_dp* p, cudaStream_t st) {
   const Plan pl = make_plan(d);
   unsigned char* w = reinterpret_cast<unsigned char*>(s->work);
-  R* lam = reinterpret_cast<R*>(w + pl.off_lam);
   R* phi = reinterpret_cast<R*>(w + pl.off_phi);
   R* W = reinterpret_cast<R*>(s->W);
   R* H = reinterpret_cast<R*>(s->H);
@@ -509,42 +535,14 @@ int Impl<R>::iterate_dp(const fm_dims* d, const fm_state* s, const fm_dp* p, cud
   R* v = reinterpret_cast<R*>(p->v);
   const R* r = reinterpret_cast<const R*>(p->r);
   const int N = (int)d->N, F = (int)d->F, T = (int)d->T, K = (int)d->K, B = (int)d->B;
-  const int D = (int)p->D, Hd = (int)p->Hd;
   const unsigned BN = (unsigned)(d->B * (d->N - 1));
-  const DpWs dw = dp_ws(d, p);
-  unsigned char* ws = reinterpret_cast<unsigned char*>(p->work);
-  R* h1 = reinterpret_cast<R*>(ws + dw.h1);
-  R* h2 = reinterpret_cast<R*>(ws + dw.h2);
-  R* d2 = reinterpret_cast<R*>(ws + dw.d2);
-  R* go = reinterpret_cast<R*>(ws + dw.go);
   // lambda of the state after the previous iteration (u absorbed c[0], W c[1:])
   if (int rc = lambda_nmf(d, s, st)) return rc;
   if (int rc = dp_lambda(d, s, p, st)) return rc;
-  // latent hook (separate.py:205-213): Adam on z against the frozen y_rest
-  const unsigned* iterp = reinterpret_cast<const unsigned*>(w + pl.off_cnt) + 1;
-  for (int step = 0; step < p->adam_steps; ++step) {
-    if (int rc = dp_forward(d, p, st)) return rc;
-    FM_DISPATCH_M(d->M, {
-      launch_pdl(k_dp_grad<R, MM>, dim3((unsigned)((T + 31) / 32), (unsigned)((F + 31) / 32), (unsigned)B),
-                 dim3(32, 8), 0, st, (const R*)u, (const R*)v, r, (const R*)lam,
-                 reinterpret_cast<const R*>(s->xt), reinterpret_cast<const R*>(s->g), go, N, F, T);
-      FM_CHECK_LAUNCH("k_dp_grad");
-    });
-    // backward to z: d2 = (go W3) (1 - h2^2) (tiled, F-long reduction), then
-    // d1 = (d2 W2) (1 - h1^2) and Adam(z, d1 W1) fused per 32-frame tile
-    if (int rc = mlp_gemm<R, false, 3, 16, 16>(go, reinterpret_cast<const R*>(p->W3), nullptr, h2, d2, T,
-                                               Hd, F, (long long)T * F, (long long)T * Hd, B, st))
-      return rc;
-    AdamEpi<R> ad{reinterpret_cast<R*>(p->z), reinterpret_cast<R*>(p->adam_m),
-                  reinterpret_cast<R*>(p->adam_v), iterp, step, p->adam_steps, p->lr, p->beta1,
-                  p->beta2, p->eps};
-    launch_pdl(k_dec_bwd21<R>, dim3((unsigned)((T + DEC_RT - 1) / DEC_RT), (unsigned)B), dim3(256), 0,
-               st, (const R*)d2, (const R*)h1, reinterpret_cast<const R*>(p->W1),
-               reinterpret_cast<const R*>(p->W2), T, D, Hd, ad);
-    FM_CHECK_LAUNCH("k_dec_bwd21");
-  }
+  // latent hook (separate.py:205-213): Adam on z against the frozen y_rest,
+  // then r = exp(dec(z)) -- one launch
   if (p->adam_steps > 0) {
-    if (int rc = dp_forward(d, p, st)) return rc;  // r = dec(z) for the new latents
+    if (int rc = dp_latent(d, s, p, p->adam_steps, st)) return rc;
     if (int rc = dp_lambda(d, s, p, st)) return rc;
   }
   // U step (sources.py:258-261)
