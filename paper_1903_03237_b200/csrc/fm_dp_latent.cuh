@@ -4,12 +4,10 @@
 // steps on z against the frozen rest-of-model power, then refreshes
 // r = exp(dec(z)). Frame t's latent z_t only reaches r[t, :], and its
 // gradient only involves frame t, so every frame's Adam trajectory is
-// independent: one CTA owns RT frames of one mixture and runs all steps,
+// independent: one CTA owns FR = 4 frames of one mixture and runs all steps,
 // forward and backward, with activations, Adam moments and the output-layer
 // gradient on chip. The decoder weights stream from L2 through a cp.async
-// double buffer in 32-row chunks (16-byte segments, XOR-swizzled by row so
-// both the row-parallel forward and the column-parallel backward products
-// read shared memory conflict-free); the output layer W3 is read ONCE per step:
+// double buffer in 32-row chunks; the output layer W3 is read ONCE per step:
 // each W3 chunk gives o[t, f-chunk] (forward), the NLL gradient dL/do for
 // those bins, and the chunk's contribution to W3^T dL/do (backward).
 //
@@ -20,17 +18,30 @@
 //   C2: d1 += W2^T (d2 (1 - h2^2))
 //   C1: gz += W1^T (d1 (1 - h1^2)); Adam(z, gz)
 // and the final refresh runs A1, A2, O writing r to HBM.
-// grid (ceil(T/RT), B), block 256.
+//
+// Work split inside a chunk: warp w owns chunk rows 4w..4w+3, lane l owns the
+// 4 columns of 16-byte segment(s) l (+32). A forward row product is a lane
+// partial over the lane's columns, reduced across the warp by a 16-value
+// butterfly (lane l ends with output (row, frame) = ((l/2)/4, (l/2)%4)); the
+// backward product reuses the same staged weights in registers
+// (acc[col][frame] += coef[row][frame] * W[row][col]), so an O chunk needs no
+// barrier between its forward, gradient and backward parts. Warp partials of
+// the backward products meet once per layer in a fixed-order sum.
+// grid (ceil(T/4), B), block 256.
 #pragma once
+#include <type_traits>
+
 #include "fm_dp.cuh"
 #include "fm_spatial.cuh"
 
 namespace fm {
 
-constexpr int LT_NT = 256;             // threads per CTA
-constexpr int LT_CH = 32;              // weight rows per chunk
-constexpr int LT_LDW = DEC_HMAX;       // row pitch of a staged chunk (elements)
-constexpr int LT_KQ = LT_NT / LT_CH;   // k-slices of the forward chunk product
+constexpr int LT_NT = 256;            // threads per CTA
+constexpr int LT_NW = LT_NT / 32;     // warps
+constexpr int LT_CH = 32;             // weight rows per chunk
+constexpr int LT_RPW = LT_CH / LT_NW; // chunk rows per warp (4)
+constexpr int LT_LDW = DEC_HMAX;      // row pitch of a staged chunk (elements)
+constexpr int LT_FR = 4;              // frames per CTA
 
 template <typename R> struct LatentArgs {
   const R *W1, *b1, *W2, *b2, *W3, *b3;  // decoder (W1 Hd x D, W2 Hd x Hd, W3 F x Hd)
@@ -45,48 +56,41 @@ template <typename R> struct LatentArgs {
   float lr, b1a, b2a, eps;
 };
 
-template <typename R, int M, int RT> struct LtCfg {
+template <typename R, int M> struct LtCfg {
+  static constexpr int FR = LT_FR;
   static constexpr int VEC = 16 / (int)sizeof(R);           // elements per 16-byte segment
-  static constexpr int SEGMAX = DEC_HMAX / VEC;             // segments per staged row
-  static constexpr int NQ = LT_NT / SEGMAX;                 // backward: threads per column segment
-  static constexpr int RP = 2;                              // backward: frames per thread
-  static constexpr int NRP = RT / RP;                       // backward: frame groups
-  static constexpr int NIQ = NQ / NRP;                      // backward: chunk-row slices
+  static constexpr int SPL = DEC_HMAX / VEC / 32;           // segments per lane
+  static constexpr int NCL = SPL * VEC;                     // columns per lane (4)
   static constexpr bool XVEC = (M * sizeof(R)) % 16 == 0;   // x~ / g rows in 16-byte segments
-  static_assert(RT % RP == 0 && NQ % NRP == 0, "frame tiling");
-  // shared-memory carve (elements of R)
-  static constexpr int RED_A = LT_KQ * RT * LT_CH, RED_C = NIQ * RT * DEC_HMAX;
-  static constexpr int W = 0;                                    // [2][LT_CH][LT_LDW] swizzled
-  static constexpr int XS = W + 2 * LT_CH * LT_LDW;              // [2][LT_CH][RT][M]
-  static constexpr int LS = XS + 2 * LT_CH * RT * M;             // [2][NMAX-1][LT_CH][RT]
-  static constexpr int GS = LS + 2 * (NMAX - 1) * LT_CH * RT;    // [2][NMAX][LT_CH][M]
+  static_assert(LT_RPW * FR == 16, "butterfly is specialised to 16 outputs per warp");
+  static_assert(NCL % 2 == 0, "column pairs");
+  // shared-memory carve (elements of R); the layer-end warp partials
+  // [NW][FR][HMAX] reuse the consumed weight buffer
+  static constexpr int WB = LT_CH * LT_LDW;                      // one weight buffer
+  static_assert(LT_NW * FR * DEC_HMAX <= WB, "partials fit a weight buffer");
+  static constexpr int W = 0;                                    // [2][LT_CH][LT_LDW]
+  static constexpr int XS = W + 2 * WB;                          // [2][LT_CH][FR][M]
+  static constexpr int LS = XS + 2 * LT_CH * FR * M;             // [2][NMAX-1][LT_CH][FR]
+  static constexpr int GS = LS + 2 * (NMAX - 1) * LT_CH * FR;    // [2][NMAX][LT_CH][M]
   static constexpr int US = GS + 2 * NMAX * LT_CH * M;           // [2][LT_CH]
   static constexpr int BS = US + 2 * LT_CH;                      // [2][LT_CH]
-  static constexpr int ZT = BS + 2 * LT_CH;                      // [DMAX][RT]
-  static constexpr int H1 = ZT + DEC_DMAX * RT;                  // [HMAX][RT]
-  static constexpr int H2 = H1 + DEC_HMAX * RT;
-  static constexpr int D1 = H2 + DEC_HMAX * RT;
-  static constexpr int D2 = D1 + DEC_HMAX * RT;
-  static constexpr int RED = D2 + DEC_HMAX * RT;                 // partial sums (both phases)
-  static constexpr int GO = RED + (RED_A > RED_C ? RED_A : RED_C);  // [LT_CH][RT]
-  static constexpr int AM = GO + LT_CH * RT;                     // [RT][DMAX]
-  static constexpr int AV = AM + RT * DEC_DMAX;
-  static constexpr int B1 = AV + RT * DEC_DMAX;                  // [HMAX]
+  static constexpr int ZT = BS + 2 * LT_CH;                      // [DMAX][FR]
+  static constexpr int H1 = ZT + DEC_DMAX * FR;                  // [HMAX][FR]
+  static constexpr int H2 = H1 + DEC_HMAX * FR;
+  static constexpr int D1 = H2 + DEC_HMAX * FR;
+  static constexpr int D2 = D1 + DEC_HMAX * FR;
+  static constexpr int AM = D2 + DEC_HMAX * FR;                  // [FR][DMAX]
+  static constexpr int AV = AM + FR * DEC_DMAX;
+  static constexpr int B1 = AV + FR * DEC_DMAX;                  // [HMAX]
   static constexpr int B2 = B1 + DEC_HMAX;
-  static constexpr int VS = B2 + DEC_HMAX;                       // [RT]
-  static constexpr int TOTAL = ((VS + RT) + 3) / 4 * 4;
+  static constexpr int VS = B2 + DEC_HMAX;                       // [FR]
+  static constexpr int TOTAL = ((VS + FR) + 3) / 4 * 4;
 };
 
 template <typename R> __device__ __forceinline__ void cp_async_el(R* s, const R* gp) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], %2;\n" ::"r"(
                    (unsigned)__cvta_generic_to_shared(s)),
                "l"(gp), "n"((int)sizeof(R)));
-}
-
-// swizzled position of element (row, k) in a staged chunk: 16-byte segment
-// k / VEC lands at segment (k / VEC) ^ (row & 7)
-template <int VEC> __device__ __forceinline__ int lt_swz(int row, int k) {
-  return row * LT_LDW + ((((k / VEC) ^ (row & 7))) * VEC) + (k % VEC);
 }
 
 enum { LT_A1 = 0, LT_A2 = 1, LT_O = 2, LT_C2 = 3, LT_C1 = 4, LT_END = 5 };
@@ -105,7 +109,7 @@ struct LtIt {
   }
 };
 
-template <typename R, int VEC> __device__ __forceinline__ void lds_vec(const R* p, R (&v)[VEC]) {
+template <typename R, int VEC> __device__ __forceinline__ void lds_vec(const R* p, R* v) {
   if constexpr (VEC == 4) {
     const float4 q = *reinterpret_cast<const float4*>(p);
     v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
@@ -115,23 +119,43 @@ template <typename R, int VEC> __device__ __forceinline__ void lds_vec(const R* 
   }
 }
 
-template <typename R, int M, int RT>
+// one butterfly level: lanes with bit `MASK` set keep the upper half
+template <int HALF, int MASK, typename R> __device__ __forceinline__ void lt_fold(R* v, int lane) {
+  const bool hi = lane & MASK;
+#pragma unroll
+  for (int j = 0; j < HALF; ++j) {
+    const R send = hi ? v[j] : v[j + HALF];
+    const R keep = hi ? v[j + HALF] : v[j];
+    v[j] = keep + __shfl_xor_sync(0xffffffffu, send, MASK);
+  }
+}
+// warp sum of 16 per-lane partials; lane l returns the total of output l / 2
+template <typename R> __device__ __forceinline__ R lt_reduce16(R (&v)[16], int lane) {
+  lt_fold<8, 16>(v, lane);
+  lt_fold<4, 8>(v, lane);
+  lt_fold<2, 4>(v, lane);
+  lt_fold<1, 2>(v, lane);
+  return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 1);
+}
+
+template <typename R, int M>
 __global__ void __launch_bounds__(LT_NT) k_dp_latent(LatentArgs<R> a) {
   pdl_entry();
-  using C = LtCfg<R, M, RT>;
-  constexpr int VEC = C::VEC;
-  using R2 = typename std::conditional<sizeof(R) == 4, float2, double2>::type;
+  using C = LtCfg<R, M>;
+  constexpr int FR = C::FR, VEC = C::VEC, NCL = C::NCL, SPL = C::SPL;
+  using R2 = typename RT<R>::C;
   extern __shared__ __align__(16) unsigned char lt_raw[];
   R* sm = reinterpret_cast<R*>(lt_raw);
-  const int tid = threadIdx.x, b = blockIdx.y, t0 = blockIdx.x * RT;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int b = blockIdx.y, t0 = blockIdx.x * FR;
   const int T = a.T, F = a.F, D = a.D, Hd = a.Hd, N = a.N;
-  const int nr = min(RT, T - t0);
+  const int nr = min(FR, T - t0);
   const int nc1 = (Hd + LT_CH - 1) / LT_CH, nc3 = (F + LT_CH - 1) / LT_CH;
   const size_t FT = (size_t)F * T;
 
   // latents, Adam moments, biases, v of this CTA's frames
-  for (int e = tid; e < DEC_DMAX * RT; e += LT_NT) {
-    const int d = e / RT, r = e % RT;
+  for (int e = tid; e < DEC_DMAX * FR; e += LT_NT) {
+    const int d = e / FR, r = e % FR;
     const bool ok = d < D && r < nr;
     const size_t i = ((size_t)b * T + t0 + r) * D + d;
     sm[C::ZT + e] = ok ? a.z[i] : R(0);
@@ -142,7 +166,7 @@ __global__ void __launch_bounds__(LT_NT) k_dp_latent(LatentArgs<R> a) {
     sm[C::B1 + j] = j < Hd ? a.b1[j] : R(0);
     sm[C::B2 + j] = j < Hd ? a.b2[j] : R(0);
   }
-  if (tid < RT) sm[C::VS + tid] = tid < nr ? a.v[(size_t)b * T + t0 + tid] : R(0);
+  if (tid < FR) sm[C::VS + tid] = tid < nr ? a.v[(size_t)b * T + t0 + tid] : R(0);
 
   // per-thread weight-staging maps for the two row widths (D and Hd)
   const int sgD = D / VEC, sgH = Hd / VEC;
@@ -155,32 +179,32 @@ __global__ void __launch_bounds__(LT_NT) k_dp_latent(LatentArgs<R> a) {
     const R* Wm = narrow ? a.W1 : c.grp == LT_O ? a.W3 : a.W2;
     const int rows = c.grp == LT_O ? F : Hd, K = narrow ? D : Hd;
     const int row0 = c.idx * LT_CH, nrow = min(LT_CH, rows - row0);
-    R* Wc = sm + C::W + buf * LT_CH * LT_LDW;
+    R* Wc = sm + C::W + buf * C::WB;
     const R* Wg = Wm + (size_t)row0 * K;
     const int i0 = narrow ? iD0 : iH0, sg = narrow ? sD : sH, st = narrow ? stD : stH;
     for (int i = i0; i < nrow; i += st)
-      cp_async16(Wc + i * LT_LDW + ((sg ^ (i & 7)) * VEC), Wg + (size_t)i * K + sg * VEC, true);
+      cp_async16(Wc + i * LT_LDW + sg * VEC, Wg + (size_t)i * K + sg * VEC, true);
     if (c.grp != LT_O) return;
     const int f0 = row0;
-    R* xs = sm + C::XS + buf * LT_CH * RT * M;
+    R* xs = sm + C::XS + buf * LT_CH * FR * M;
     if constexpr (C::XVEC) {
       constexpr int MS = M / VEC;
-      for (int e = tid; e < LT_CH * RT * MS; e += LT_NT) {
-        const int fl = e / (RT * MS), q = e % (RT * MS), r = q / MS, sgm = q % MS;
+      for (int e = tid; e < LT_CH * FR * MS; e += LT_NT) {
+        const int fl = e / (FR * MS), q = e % (FR * MS), r = q / MS, sgm = q % MS;
         if (fl < nrow && r < nr)
-          cp_async16(xs + (fl * RT + r) * M + sgm * VEC,
+          cp_async16(xs + (fl * FR + r) * M + sgm * VEC,
                      a.xt + (((size_t)b * F + f0 + fl) * T + t0 + r) * M + sgm * VEC, true);
       }
     } else {
-      for (int e = tid; e < LT_CH * RT * M; e += LT_NT) {
-        const int fl = e / (RT * M), q = e % (RT * M), r = q / M;
+      for (int e = tid; e < LT_CH * FR * M; e += LT_NT) {
+        const int fl = e / (FR * M), q = e % (FR * M), r = q / M;
         if (fl < nrow && r < nr)
-          cp_async_el(xs + fl * RT * M + q, a.xt + (((size_t)b * F + f0 + fl) * T + t0) * M + q);
+          cp_async_el(xs + fl * FR * M + q, a.xt + (((size_t)b * F + f0 + fl) * T + t0) * M + q);
       }
     }
-    R* ls = sm + C::LS + buf * (NMAX - 1) * LT_CH * RT;
-    for (int e = tid; e < (N - 1) * LT_CH * RT; e += LT_NT) {
-      const int n = e / (LT_CH * RT), q = e % (LT_CH * RT), fl = q / RT, r = q % RT;
+    R* ls = sm + C::LS + buf * (NMAX - 1) * LT_CH * FR;
+    for (int e = tid; e < (N - 1) * LT_CH * FR; e += LT_NT) {
+      const int n = e / (LT_CH * FR), q = e % (LT_CH * FR), fl = q / FR, r = q % FR;
       if (fl < nrow && r < nr)
         cp_async_el(ls + e, a.lam + ((size_t)b * N + n + 1) * FT + (size_t)(f0 + fl) * T + t0 + r);
     }
@@ -205,17 +229,18 @@ __global__ void __launch_bounds__(LT_NT) k_dp_latent(LatentArgs<R> a) {
     }
   };
 
-  // backward-product thread map: column segment, frame pair, chunk-row slice
-  const int cseg = tid % C::SEGMAX, cq = tid / C::SEGMAX;
-  const int crp = cq % C::NRP, ciq = cq / C::NRP;
-  R accC[VEC][C::RP];
+  // lane's columns: segment (lane + 32 j) of a staged row, j < SPL
+  auto colof = [&](int c) { return (lane + 32 * (c / VEC)) * VEC + (c % VEC); };
+  const int q = lane >> 1, qi = q / FR, qr = q % FR;  // lane's output after the butterfly
+
+  R2 acc[NCL / 2][FR];   // backward partials: (column pair, frame)
+  R2 xin[NCL][FR / 2];   // forward input rows of the lane's k columns, per frame pair
 #pragma unroll
-  for (int v = 0; v < VEC; ++v)
+  for (int c = 0; c < NCL / 2; ++c)
 #pragma unroll
-    for (int h = 0; h < C::RP; ++h) accC[v][h] = 0;
+    for (int r = 0; r < FR; ++r) acc[c][r] = R2{0, 0};
 
   LtIt cur{LT_A1, 0, 0};
-  if (a.steps == 0) cur.s = 0;
   LtIt nxt = cur;
   load(cur, 0);
   cp_async_commit();
@@ -226,119 +251,147 @@ __global__ void __launch_bounds__(LT_NT) k_dp_latent(LatentArgs<R> a) {
     if (nxt.grp != LT_END) load(nxt, (gi + 1) & 1);
     cp_async_commit();
     const int buf = gi & 1;
-    const R* Wc = sm + C::W + buf * LT_CH * LT_LDW;
+    R* Wc = sm + C::W + buf * C::WB;
     const bool refresh = cur.s == a.steps;
+    const bool fwd = cur.grp <= LT_O;
     const int row0 = cur.idx * LT_CH;
+    const int K = (cur.grp == LT_A1 || cur.grp == LT_C1) ? D : Hd;   // staged row width
+    const int nrow = min(LT_CH, (cur.grp == LT_O ? F : Hd) - row0);
 
-    if (cur.grp <= LT_O) {
-      // forward chunk: out[r][row0 + row] = sum_k Wc[row][k] in[k][r]
-      const int K = cur.grp == LT_A1 ? D : Hd;
-      const R* inT = sm + (cur.grp == LT_A1 ? C::ZT : cur.grp == LT_A2 ? C::H1 : C::H2);
-      const int row = tid & (LT_CH - 1), kq = tid / LT_CH;
-      const int nsg = K / VEC, spq = (nsg + LT_KQ - 1) / LT_KQ;
-      const int s0 = kq * spq, s1 = min(nsg, s0 + spq);
-      R2 acc[RT / 2];
+    // the warp's 4 staged rows, lane's columns (zero outside the chunk / row width)
+    R w[LT_RPW][NCL];
 #pragma unroll
-      for (int h = 0; h < RT / 2; ++h) acc[h] = R2{0, 0};
-      const R* wrow = Wc + row * LT_LDW;
-      for (int sg = s0; sg < s1; ++sg) {
-        R w[VEC];
-        lds_vec<R, VEC>(wrow + ((sg ^ (row & 7)) * VEC), w);
+    for (int i = 0; i < LT_RPW; ++i) {
+      const int row = warp * LT_RPW + i;
 #pragma unroll
-        for (int v = 0; v < VEC; ++v) {
-          const R2* in2 = reinterpret_cast<const R2*>(inT + (sg * VEC + v) * RT);
-#pragma unroll
-          for (int h = 0; h < RT / 2; ++h) acc[h] = fma2(R2{w[v], w[v]}, in2[h], acc[h]);
-        }
-      }
-#pragma unroll
-      for (int h = 0; h < RT / 2; ++h) {
-        sm[C::RED + (kq * RT + 2 * h) * LT_CH + row] = acc[h].x;
-        sm[C::RED + (kq * RT + 2 * h + 1) * LT_CH + row] = acc[h].y;
-      }
-      __syncthreads();
-      if (tid < RT * LT_CH) {
-        const int r = tid / LT_CH, rw = tid & (LT_CH - 1);
-        R o = 0;
-#pragma unroll
-        for (int q = 0; q < LT_KQ; ++q) o += sm[C::RED + (q * RT + r) * LT_CH + rw];
-        const int j = row0 + rw;
-        if (cur.grp == LT_A1) {
-          if (j < Hd) sm[C::H1 + j * RT + r] = tanh(o + sm[C::B1 + j]);
-        } else if (cur.grp == LT_A2) {
-          if (j < Hd) sm[C::H2 + j * RT + r] = tanh(o + sm[C::B2 + j]);
+      for (int j = 0; j < SPL; ++j) {
+        const int seg = lane + 32 * j;
+        if (row < nrow && seg * VEC < K) {
+          lds_vec<R, VEC>(Wc + row * LT_LDW + seg * VEC, &w[i][j * VEC]);
         } else {
-          // output layer + NLL gradient (dL/do of sum x~/y + log y)
-          const bool ok = j < F && r < nr;
-          R go = 0;
-          if (ok) {
-            const R rr = exp(o + sm[C::BS + buf * LT_CH + rw]);
-            if (refresh) {
-              a.r[((size_t)b * T + t0 + r) * F + j] = rr;
-            } else {
-              const R l0 = sm[C::US + buf * LT_CH + rw] * sm[C::VS + r] * rr;
-              const R* xr = sm + C::XS + buf * LT_CH * RT * M + (rw * RT + r) * M;
-              const R* ls = sm + C::LS + buf * (NMAX - 1) * LT_CH * RT + rw * RT + r;
-              const R* gs = sm + C::GS + buf * NMAX * LT_CH * M + rw * M;
-              R ln[NMAX];
 #pragma unroll
-              for (int n = 1; n < NMAX; ++n) {
-                ln[n] = R(0);
-                if (n >= N) break;
-                ln[n] = ls[(n - 1) * LT_CH * RT];
-              }
-              R s = 0;
-#pragma unroll
-              for (int m = 0; m < M; ++m) {
-                R rest = 0;
-#pragma unroll
-                for (int n = 1; n < NMAX; ++n) {
-                  if (n >= N) break;
-                  rest += ln[n] * gs[n * LT_CH * M + m];
-                }
-                const R g0 = gs[m];
-                R y = l0 * g0 + rest;
-                y = y > ::fm::RT<R>::tiny() ? y : ::fm::RT<R>::tiny();
-                const R iy = rcp_r(y);
-                s += g0 * (iy - xr[m] * iy * iy);
-              }
-              go = s * l0;
-            }
-          }
-          sm[C::GO + rw * RT + r] = go;
+          for (int v = 0; v < VEC; ++v) w[i][j * VEC + v] = 0;
         }
       }
-      if (cur.grp != LT_O || refresh) continue;
-      __syncthreads();
     }
 
-    // backward chunk: acc[col][r] += sum_i coef[i][r] Wc[i][col] over this
-    // thread's columns (one segment), frames (a pair) and chunk rows (a slice)
-    const int ncol = cur.grp == LT_C1 ? D : Hd;
-    const int nrow = min(LT_CH, (cur.grp == LT_O ? F : Hd) - row0);
-    const R* coef = cur.grp == LT_O ? sm + C::GO : sm + (cur.grp == LT_C2 ? C::D2 : C::D1) + row0 * RT;
-    if (cseg * VEC < ncol) {
-      for (int i = ciq; i < nrow; i += C::NIQ) {
-        R w[VEC];
-        lds_vec<R, VEC>(Wc + i * LT_LDW + ((cseg ^ (i & 7)) * VEC), w);
-        const R2 cf = *reinterpret_cast<const R2*>(coef + i * RT + crp * C::RP);
+    if (fwd) {
+      if (cur.idx == 0) {  // the layer input, in registers for the whole layer
+        const R* inT = sm + (cur.grp == LT_A1 ? C::ZT : cur.grp == LT_A2 ? C::H1 : C::H2);
 #pragma unroll
-        for (int v = 0; v < VEC; ++v) {
-          R2 t = R2{accC[v][0], accC[v][1]};
-          t = fma2(R2{w[v], w[v]}, cf, t);
-          accC[v][0] = t.x;
-          accC[v][1] = t.y;
+        for (int c = 0; c < NCL; ++c) {
+          const int k = colof(c);
+#pragma unroll
+          for (int h = 0; h < FR / 2; ++h)
+            xin[c][h] = k < K ? reinterpret_cast<const R2*>(inT + k * FR)[h] : R2{0, 0};
         }
+      }
+      R pv[LT_RPW * FR];
+#pragma unroll
+      for (int i = 0; i < LT_RPW; ++i) {
+        R2 s2[FR / 2];
+#pragma unroll
+        for (int h = 0; h < FR / 2; ++h) s2[h] = R2{0, 0};
+#pragma unroll
+        for (int c = 0; c < NCL; ++c)
+#pragma unroll
+          for (int h = 0; h < FR / 2; ++h) s2[h] = fma2(R2{w[i][c], w[i][c]}, xin[c][h], s2[h]);
+#pragma unroll
+        for (int h = 0; h < FR / 2; ++h) {
+          pv[i * FR + 2 * h] = s2[h].x;
+          pv[i * FR + 2 * h + 1] = s2[h].y;
+        }
+      }
+      const R o = lt_reduce16(pv, lane);
+      const int rl = warp * LT_RPW + qi, j = row0 + rl;  // chunk row, global row
+      if (cur.grp == LT_A1) {
+        if ((lane & 1) == 0 && j < Hd) sm[C::H1 + j * FR + qr] = tanh(o + sm[C::B1 + j]);
+        continue;
+      }
+      if (cur.grp == LT_A2) {
+        if ((lane & 1) == 0 && j < Hd) sm[C::H2 + j * FR + qr] = tanh(o + sm[C::B2 + j]);
+        continue;
+      }
+      // output layer + NLL gradient dL/do of sum x~/y + log y (both lanes of a pair)
+      const bool ok = j < F && qr < nr;
+      R go = 0;
+      if (ok) {
+        const R rr = exp(o + sm[C::BS + buf * LT_CH + rl]);
+        if (refresh) {
+          if ((lane & 1) == 0) a.r[((size_t)b * T + t0 + qr) * F + j] = rr;
+        } else {
+          const R l0 = sm[C::US + buf * LT_CH + rl] * sm[C::VS + qr] * rr;
+          const R* xr = sm + C::XS + buf * LT_CH * FR * M + (rl * FR + qr) * M;
+          const R* ls = sm + C::LS + buf * (NMAX - 1) * LT_CH * FR + rl * FR + qr;
+          const R* gs = sm + C::GS + buf * NMAX * LT_CH * M + rl * M;
+          R ln[NMAX];
+#pragma unroll
+          for (int n = 1; n < NMAX; ++n) {
+            ln[n] = R(0);
+            if (n >= N) break;
+            ln[n] = ls[(n - 1) * LT_CH * FR];
+          }
+          R s = 0;
+#pragma unroll
+          for (int m = 0; m < M; ++m) {
+            R rest = 0;
+#pragma unroll
+            for (int n = 1; n < NMAX; ++n) {
+              if (n >= N) break;
+              rest += ln[n] * gs[n * LT_CH * M + m];
+            }
+            const R g0 = gs[m];
+            R y = l0 * g0 + rest;
+            y = y > RT<R>::tiny() ? y : RT<R>::tiny();
+            const R iy = rcp_r(y);
+            s += g0 * (iy - xr[m] * iy * iy);
+          }
+          go = s * l0;
+        }
+      }
+      if (refresh) continue;
+      // backward part of the O chunk: acc[col][r] += go[row][r] W3[row][col]
+#pragma unroll
+      for (int qq = 0; qq < LT_RPW * FR; ++qq) {
+        const R gq = __shfl_sync(0xffffffffu, go, 2 * qq);
+        const int i = qq / FR, r = qq % FR;
+#pragma unroll
+        for (int c = 0; c < NCL / 2; ++c)
+          acc[c][r] = fma2(R2{w[i][2 * c], w[i][2 * c + 1]}, R2{gq, gq}, acc[c][r]);
+      }
+    } else {
+      // C2 / C1: acc[col][r] += coef[row][r] W[row][col]
+      const R* coef = sm + (cur.grp == LT_C2 ? C::D2 : C::D1) + (row0 + warp * LT_RPW) * FR;
+#pragma unroll
+      for (int i = 0; i < LT_RPW; ++i) {
+        R cf[FR];
+#pragma unroll
+        for (int h = 0; h < FR / 2; ++h) {
+          const R2 t = reinterpret_cast<const R2*>(coef + i * FR)[h];
+          cf[2 * h] = t.x;
+          cf[2 * h + 1] = t.y;
+        }
+#pragma unroll
+        for (int r = 0; r < FR; ++r)
+#pragma unroll
+          for (int c = 0; c < NCL / 2; ++c)
+            acc[c][r] = fma2(R2{w[i][2 * c], w[i][2 * c + 1]}, R2{cf[r], cf[r]}, acc[c][r]);
       }
     }
     if (!cur.last(nc1, nc3)) continue;
-    // group end: fixed-order sum over the chunk-row slices, then the epilogue
+
+    // layer end: warp partials -> the consumed weight buffer -> fixed-order sum
+    const int ncol = cur.grp == LT_C1 ? D : Hd;
+    __syncthreads();
+    R* red = Wc;  // [NW][FR][HMAX]
 #pragma unroll
-    for (int v = 0; v < VEC; ++v)
+    for (int c = 0; c < NCL / 2; ++c)
 #pragma unroll
-      for (int h = 0; h < C::RP; ++h) {
-        sm[C::RED + (ciq * RT + crp * C::RP + h) * DEC_HMAX + cseg * VEC + v] = accC[v][h];
-        accC[v][h] = 0;
+      for (int r = 0; r < FR; ++r) {
+        const int col = colof(2 * c);
+        red[(warp * FR + r) * DEC_HMAX + col] = acc[c][r].x;
+        red[(warp * FR + r) * DEC_HMAX + col + 1] = acc[c][r].y;
+        acc[c][r] = R2{0, 0};
       }
     __syncthreads();
     double c1 = 0, c2 = 0;
@@ -347,13 +400,13 @@ __global__ void __launch_bounds__(LT_NT) k_dp_latent(LatentArgs<R> a) {
       c1 = 1.0 - pow((double)a.b1a, tstep);
       c2 = 1.0 - pow((double)a.b2a, tstep);
     }
-    for (int e = tid; e < RT * DEC_HMAX; e += LT_NT) {
+    for (int e = tid; e < FR * DEC_HMAX; e += LT_NT) {
       const int r = e / DEC_HMAX, col = e % DEC_HMAX;
       if (col >= ncol) continue;
       R sum = 0;
 #pragma unroll
-      for (int q = 0; q < C::NIQ; ++q) sum += sm[C::RED + (q * RT + r) * DEC_HMAX + col];
-      const int i = col * RT + r;
+      for (int ww = 0; ww < LT_NW; ++ww) sum += red[(ww * FR + r) * DEC_HMAX + col];
+      const int i = col * FR + r;
       if (cur.grp == LT_O) {  // d2 = (W3^T go) (1 - h2^2)
         const R hv = sm[C::H2 + i];
         sm[C::D2 + i] = sum * (R(1) - hv * hv);
@@ -377,7 +430,7 @@ __global__ void __launch_bounds__(LT_NT) k_dp_latent(LatentArgs<R> a) {
   for (int e = tid; e < D * nr; e += LT_NT) {
     const int r = e / D, d = e - r * D;
     const size_t i = ((size_t)b * T + t0 + r) * D + d;
-    a.z[i] = sm[C::ZT + d * RT + r];
+    a.z[i] = sm[C::ZT + d * FR + r];
     a.m[i] = sm[C::AM + r * DEC_DMAX + d];
     a.v2[i] = sm[C::AV + r * DEC_DMAX + d];
   }

@@ -468,12 +468,11 @@ int Impl<R>::dp_latent(const fm_dims* d, const fm_state* s, const fm_dp* p, int 
   a.b1a = p->beta1;
   a.b2a = p->beta2;
   a.eps = p->eps;
-  constexpr int FR = 4;
-  dim3 grid((unsigned)((d->T + FR - 1) / FR), (unsigned)d->B);
+  dim3 grid((unsigned)((d->T + LT_FR - 1) / LT_FR), (unsigned)d->B);
   FM_DISPATCH_M(d->M, {
-    const size_t sm = sizeof(R) * LtCfg<R, MM, FR>::TOTAL;
-    if (int rc = ensure_smem(k_dp_latent<R, MM, FR>, sm)) return rc;
-    launch_pdl(k_dp_latent<R, MM, FR>, grid, dim3(LT_NT), sm, st, a);
+    const size_t sm = sizeof(R) * LtCfg<R, MM>::TOTAL;
+    if (int rc = ensure_smem(k_dp_latent<R, MM>, sm)) return rc;
+    launch_pdl(k_dp_latent<R, MM>, grid, dim3(LT_NT), sm, st, a);
     FM_CHECK_LAUNCH("k_dp_latent");
   });
   return FM_OK;
