@@ -6,8 +6,8 @@
 // gradient only involves frame t, so every frame's Adam trajectory is
 // independent: one CTA owns FR = 4 frames of one mixture and runs all steps,
 // forward and backward, with activations, Adam moments and the output-layer
-// gradient on chip. The decoder weights stream from L2 through a cp.async
-// double buffer in 32-row chunks; the output layer W3 is read ONCE per step:
+// gradient on chip. The decoder weights stream from L2 through an S-stage
+// cp.async pipeline (S = 2..4, as shared memory allows) in CH-row chunks; the output layer W3 is read ONCE per step:
 // each W3 chunk gives o[t, f-chunk] (forward), the NLL gradient dL/do for
 // those bins, and the chunk's contribution to W3^T dL/do (backward).
 //
@@ -19,10 +19,11 @@
 //   C1: gz += W1^T (d1 (1 - h1^2)); Adam(z, gz)
 // and the final refresh runs A1, A2, O writing r to HBM.
 //
-// Work split inside a chunk: warp w owns chunk rows 4w..4w+3, lane l owns the
-// 4 columns of 16-byte segment(s) l (+32). A forward row product is a lane
-// partial over the lane's columns, reduced across the warp by a 16-value
-// butterfly (lane l ends with output (row, frame) = ((l/2)/4, (l/2)%4)); the
+// Work split inside a chunk (CH = 64 rows fp32, 32 fp64): warp w owns CH/8
+// consecutive chunk rows, lane l owns the 4 columns of 16-byte segment(s)
+// l (+32). A forward row product is a lane partial over the lane's columns,
+// reduced across the warp by a 32- (16-) value butterfly that leaves lane l
+// with output (row, frame) = (l/4, l%4) (fp64: ((l/2)/4, (l/2)%4)); the
 // backward product reuses the same staged weights in registers
 // (acc[col][frame] += coef[row][frame] * W[row][col]), so an O chunk needs no
 // barrier between its forward, gradient and backward parts. Warp partials of
@@ -38,8 +39,6 @@ namespace fm {
 
 constexpr int LT_NT = 256;            // threads per CTA
 constexpr int LT_NW = LT_NT / 32;     // warps
-constexpr int LT_CH = 32;             // weight rows per chunk
-constexpr int LT_RPW = LT_CH / LT_NW; // chunk rows per warp (4)
 constexpr int LT_LDW = DEC_HMAX;      // row pitch of a staged chunk (elements)
 constexpr int LT_FR = 4;              // frames per CTA
 
@@ -52,7 +51,7 @@ template <typename R> struct LatentArgs {
   const R* xt;                           // (B, F, T, M)
   const R* g;                            // (B, N, F, M)
   const unsigned* iter;                  // device iteration counter (Adam step index)
-  int T, F, D, Hd, N, steps;
+  int T, F, D, Hd, N, steps, stages;
   float lr, b1a, b2a, eps;
 };
 
@@ -62,30 +61,48 @@ template <typename R, int M> struct LtCfg {
   static constexpr int SPL = DEC_HMAX / VEC / 32;           // segments per lane
   static constexpr int NCL = SPL * VEC;                     // columns per lane (4)
   static constexpr bool XVEC = (M * sizeof(R)) % 16 == 0;   // x~ / g rows in 16-byte segments
-  static_assert(LT_RPW * FR == 16, "butterfly is specialised to 16 outputs per warp");
+  static constexpr int CH = sizeof(R) == 4 ? 64 : 32;       // weight rows per chunk
+  static constexpr int RPW = CH / LT_NW;                    // chunk rows per warp (8 / 4)
+  static constexpr int WB = CH * LT_LDW;                    // one weight buffer
+  static constexpr int NV = RPW * FR;                       // forward outputs per warp
+  static constexpr int QSH = NV == 8 ? 2 : NV == 16 ? 1 : 0; // lane -> output shift
+  static_assert(NV == 8 || NV == 16 || NV == 32, "butterfly sizes");
   static_assert(NCL % 2 == 0, "column pairs");
-  // shared-memory carve (elements of R); the layer-end warp partials
-  // [NW][FR][HMAX] reuse the consumed weight buffer
-  static constexpr int WB = LT_CH * LT_LDW;                      // one weight buffer
-  static_assert(LT_NW * FR * DEC_HMAX <= WB, "partials fit a weight buffer");
-  static constexpr int W = 0;                                    // [2][LT_CH][LT_LDW]
-  static constexpr int XS = W + 2 * WB;                          // [2][LT_CH][FR][M]
-  static constexpr int LS = XS + 2 * LT_CH * FR * M;             // [2][NMAX-1][LT_CH][FR]
-  static constexpr int GS = LS + 2 * (NMAX - 1) * LT_CH * FR;    // [2][NMAX][LT_CH][M]
-  static constexpr int US = GS + 2 * NMAX * LT_CH * M;           // [2][LT_CH]
-  static constexpr int BS = US + 2 * LT_CH;                      // [2][LT_CH]
-  static constexpr int ZT = BS + 2 * LT_CH;                      // [DMAX][FR]
-  static constexpr int H1 = ZT + DEC_DMAX * FR;                  // [HMAX][FR]
-  static constexpr int H2 = H1 + DEC_HMAX * FR;
-  static constexpr int D1 = H2 + DEC_HMAX * FR;
-  static constexpr int D2 = D1 + DEC_HMAX * FR;
-  static constexpr int AM = D2 + DEC_HMAX * FR;                  // [FR][DMAX]
-  static constexpr int AV = AM + FR * DEC_DMAX;
-  static constexpr int B1 = AV + FR * DEC_DMAX;                  // [HMAX]
-  static constexpr int B2 = B1 + DEC_HMAX;
-  static constexpr int VS = B2 + DEC_HMAX;                       // [FR]
-  static constexpr int TOTAL = ((VS + FR) + 3) / 4 * 4;
+  static_assert(LT_NW * FR * DEC_HMAX <= WB, "layer-end partials fit a weight buffer");
 };
+
+// shared-memory carve (elements of R) for S pipeline stages and N sources;
+// the layer-end warp partials [NW][FR][HMAX] reuse the consumed weight buffer
+struct LtLayout {
+  int S, stage;                 // stages, elements per stage
+  int W, XS, LS, GS, US, BS;    // offsets inside a stage
+  int ZT, H1, H2, D1, D2, AM, AV, B1, B2, VS, total;
+};
+template <typename R, int M> __host__ __device__ inline LtLayout lt_layout(int S, int N) {
+  constexpr int FR = LT_FR, LT_CH = LtCfg<R, M>::CH;
+  auto up4 = [](int x) { return (x + 3) / 4 * 4; };
+  LtLayout L;
+  L.S = S;
+  L.W = 0;
+  L.XS = L.W + LT_CH * LT_LDW;
+  L.LS = L.XS + up4(LT_CH * FR * M);
+  L.GS = L.LS + up4((N - 1) * LT_CH * FR);
+  L.US = L.GS + up4(N * LT_CH * M);
+  L.BS = L.US + LT_CH;
+  L.stage = L.BS + LT_CH;
+  L.ZT = S * L.stage;
+  L.H1 = L.ZT + DEC_DMAX * FR;
+  L.H2 = L.H1 + DEC_HMAX * FR;
+  L.D1 = L.H2 + DEC_HMAX * FR;
+  L.D2 = L.D1 + DEC_HMAX * FR;
+  L.AM = L.D2 + DEC_HMAX * FR;
+  L.AV = L.AM + FR * DEC_DMAX;
+  L.B1 = L.AV + FR * DEC_DMAX;
+  L.B2 = L.B1 + DEC_HMAX;
+  L.VS = L.B2 + DEC_HMAX;
+  L.total = up4(L.VS + FR);
+  return L;
+}
 
 template <typename R> __device__ __forceinline__ void cp_async_el(R* s, const R* gp) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], %2;\n" ::"r"(
@@ -129,13 +146,18 @@ template <int HALF, int MASK, typename R> __device__ __forceinline__ void lt_fol
     v[j] = keep + __shfl_xor_sync(0xffffffffu, send, MASK);
   }
 }
-// warp sum of 16 per-lane partials; lane l returns the total of output l / 2
-template <typename R> __device__ __forceinline__ R lt_reduce16(R (&v)[16], int lane) {
-  lt_fold<8, 16>(v, lane);
-  lt_fold<4, 8>(v, lane);
-  lt_fold<2, 4>(v, lane);
-  lt_fold<1, 2>(v, lane);
-  return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 1);
+// warp sum of NV per-lane partials; lane l returns the total of output l >> (5 - log2 NV)
+template <int NV, typename R> __device__ __forceinline__ R lt_reduce(R (&v)[NV], int lane) {
+  if constexpr (NV >= 2) lt_fold<NV / 2, 16>(v, lane);
+  if constexpr (NV >= 4) lt_fold<NV / 4, 8>(v, lane);
+  if constexpr (NV >= 8) lt_fold<NV / 8, 4>(v, lane);
+  if constexpr (NV >= 16) lt_fold<NV / 16, 2>(v, lane);
+  if constexpr (NV >= 32) lt_fold<1, 1>(v, lane);
+  R x = v[0];
+  if constexpr (NV < 32) x += __shfl_xor_sync(0xffffffffu, x, 1);
+  if constexpr (NV < 16) x += __shfl_xor_sync(0xffffffffu, x, 2);
+  if constexpr (NV < 8) x += __shfl_xor_sync(0xffffffffu, x, 4);
+  return x;
 }
 
 template <typename R, int M>
@@ -143,6 +165,9 @@ __global__ void __launch_bounds__(LT_NT) k_dp_latent(LatentArgs<R> a) {
   pdl_entry();
   using C = LtCfg<R, M>;
   constexpr int FR = C::FR, VEC = C::VEC, NCL = C::NCL, SPL = C::SPL;
+  const LtLayout L = lt_layout<R, M>(a.stages, a.N);
+  const int S = L.S;
+  constexpr int LT_CH = C::CH, LT_RPW = C::RPW;
   using R2 = typename RT<R>::C;
   extern __shared__ __align__(16) unsigned char lt_raw[];
   R* sm = reinterpret_cast<R*>(lt_raw);
@@ -158,15 +183,15 @@ __global__ void __launch_bounds__(LT_NT) k_dp_latent(LatentArgs<R> a) {
     const int d = e / FR, r = e % FR;
     const bool ok = d < D && r < nr;
     const size_t i = ((size_t)b * T + t0 + r) * D + d;
-    sm[C::ZT + e] = ok ? a.z[i] : R(0);
-    sm[C::AM + r * DEC_DMAX + d] = ok ? a.m[i] : R(0);
-    sm[C::AV + r * DEC_DMAX + d] = ok ? a.v2[i] : R(0);
+    sm[L.ZT + e] = ok ? a.z[i] : R(0);
+    sm[L.AM + r * DEC_DMAX + d] = ok ? a.m[i] : R(0);
+    sm[L.AV + r * DEC_DMAX + d] = ok ? a.v2[i] : R(0);
   }
   for (int j = tid; j < DEC_HMAX; j += LT_NT) {
-    sm[C::B1 + j] = j < Hd ? a.b1[j] : R(0);
-    sm[C::B2 + j] = j < Hd ? a.b2[j] : R(0);
+    sm[L.B1 + j] = j < Hd ? a.b1[j] : R(0);
+    sm[L.B2 + j] = j < Hd ? a.b2[j] : R(0);
   }
-  if (tid < FR) sm[C::VS + tid] = tid < nr ? a.v[(size_t)b * T + t0 + tid] : R(0);
+  if (tid < FR) sm[L.VS + tid] = tid < nr ? a.v[(size_t)b * T + t0 + tid] : R(0);
 
   // per-thread weight-staging maps for the two row widths (D and Hd)
   const int sgD = D / VEC, sgH = Hd / VEC;
@@ -179,14 +204,14 @@ __global__ void __launch_bounds__(LT_NT) k_dp_latent(LatentArgs<R> a) {
     const R* Wm = narrow ? a.W1 : c.grp == LT_O ? a.W3 : a.W2;
     const int rows = c.grp == LT_O ? F : Hd, K = narrow ? D : Hd;
     const int row0 = c.idx * LT_CH, nrow = min(LT_CH, rows - row0);
-    R* Wc = sm + C::W + buf * C::WB;
+    R* Wc = sm + buf * L.stage + L.W;
     const R* Wg = Wm + (size_t)row0 * K;
     const int i0 = narrow ? iD0 : iH0, sg = narrow ? sD : sH, st = narrow ? stD : stH;
     for (int i = i0; i < nrow; i += st)
       cp_async16(Wc + i * LT_LDW + sg * VEC, Wg + (size_t)i * K + sg * VEC, true);
     if (c.grp != LT_O) return;
     const int f0 = row0;
-    R* xs = sm + C::XS + buf * LT_CH * FR * M;
+    R* xs = sm + buf * L.stage + L.XS;
     if constexpr (C::XVEC) {
       constexpr int MS = M / VEC;
       for (int e = tid; e < LT_CH * FR * MS; e += LT_NT) {
@@ -202,13 +227,13 @@ __global__ void __launch_bounds__(LT_NT) k_dp_latent(LatentArgs<R> a) {
           cp_async_el(xs + fl * FR * M + q, a.xt + (((size_t)b * F + f0 + fl) * T + t0) * M + q);
       }
     }
-    R* ls = sm + C::LS + buf * (NMAX - 1) * LT_CH * FR;
+    R* ls = sm + buf * L.stage + L.LS;
     for (int e = tid; e < (N - 1) * LT_CH * FR; e += LT_NT) {
       const int n = e / (LT_CH * FR), q = e % (LT_CH * FR), fl = q / FR, r = q % FR;
       if (fl < nrow && r < nr)
         cp_async_el(ls + e, a.lam + ((size_t)b * N + n + 1) * FT + (size_t)(f0 + fl) * T + t0 + r);
     }
-    R* gs = sm + C::GS + buf * NMAX * LT_CH * M;
+    R* gs = sm + buf * L.stage + L.GS;
     if constexpr (C::XVEC) {
       constexpr int GSG = LT_CH * M / VEC;
       for (int e = tid; e < N * GSG; e += LT_NT) {
@@ -224,14 +249,15 @@ __global__ void __launch_bounds__(LT_NT) k_dp_latent(LatentArgs<R> a) {
       }
     }
     if (tid < nrow) {
-      cp_async_el(sm + C::US + buf * LT_CH + tid, a.u + (size_t)b * F + f0 + tid);
-      cp_async_el(sm + C::BS + buf * LT_CH + tid, a.b3 + f0 + tid);
+      cp_async_el(sm + buf * L.stage + L.US + tid, a.u + (size_t)b * F + f0 + tid);
+      cp_async_el(sm + buf * L.stage + L.BS + tid, a.b3 + f0 + tid);
     }
   };
 
   // lane's columns: segment (lane + 32 j) of a staged row, j < SPL
   auto colof = [&](int c) { return (lane + 32 * (c / VEC)) * VEC + (c % VEC); };
-  const int q = lane >> 1, qi = q / FR, qr = q % FR;  // lane's output after the butterfly
+  const int q = lane >> C::QSH, qi = q / FR, qr = q % FR;  // lane's output after the butterfly
+  const bool qlead = (lane & ((1 << C::QSH) - 1)) == 0;       // one writer per output
 
   R2 acc[NCL / 2][FR];   // backward partials: (column pair, frame)
   R2 xin[NCL][FR / 2];   // forward input rows of the lane's k columns, per frame pair
@@ -240,18 +266,29 @@ __global__ void __launch_bounds__(LT_NT) k_dp_latent(LatentArgs<R> a) {
 #pragma unroll
     for (int r = 0; r < FR; ++r) acc[c][r] = R2{0, 0};
 
+  // S-stage cp.async pipeline: chunk gi lives in stage gi % S; loads run S-1 chunks ahead
   LtIt cur{LT_A1, 0, 0};
-  LtIt nxt = cur;
-  load(cur, 0);
-  cp_async_commit();
-  for (int gi = 0; cur.grp != LT_END; ++gi, cur = nxt) {
-    cp_async_wait<0>();
-    __syncthreads();
-    nxt.next(nc1, nc3, a.steps);
-    if (nxt.grp != LT_END) load(nxt, (gi + 1) & 1);
+  LtIt ld = cur;
+  for (int p = 0; p < S - 1; ++p) {
+    if (ld.grp != LT_END) {
+      load(ld, p);
+      ld.next(nc1, nc3, a.steps);
+    }
     cp_async_commit();
-    const int buf = gi & 1;
-    R* Wc = sm + C::W + buf * C::WB;
+  }
+  int buf = 0, bld = S - 1;  // stage of the current chunk / of the next load
+  for (; cur.grp != LT_END; cur.next(nc1, nc3, a.steps), buf = buf + 1 == S ? 0 : buf + 1,
+                            bld = bld + 1 == S ? 0 : bld + 1) {
+    if (S == 2) cp_async_wait<0>();
+    else if (S == 3) cp_async_wait<1>();
+    else cp_async_wait<2>();
+    __syncthreads();
+    if (ld.grp != LT_END) {
+      load(ld, bld);
+      ld.next(nc1, nc3, a.steps);
+    }
+    cp_async_commit();
+    R* Wc = sm + buf * L.stage + L.W;
     const bool refresh = cur.s == a.steps;
     const bool fwd = cur.grp <= LT_O;
     const int row0 = cur.idx * LT_CH;
@@ -277,7 +314,7 @@ __global__ void __launch_bounds__(LT_NT) k_dp_latent(LatentArgs<R> a) {
 
     if (fwd) {
       if (cur.idx == 0) {  // the layer input, in registers for the whole layer
-        const R* inT = sm + (cur.grp == LT_A1 ? C::ZT : cur.grp == LT_A2 ? C::H1 : C::H2);
+        const R* inT = sm + (cur.grp == LT_A1 ? L.ZT : cur.grp == LT_A2 ? L.H1 : L.H2);
 #pragma unroll
         for (int c = 0; c < NCL; ++c) {
           const int k = colof(c);
@@ -286,7 +323,7 @@ __global__ void __launch_bounds__(LT_NT) k_dp_latent(LatentArgs<R> a) {
             xin[c][h] = k < K ? reinterpret_cast<const R2*>(inT + k * FR)[h] : R2{0, 0};
         }
       }
-      R pv[LT_RPW * FR];
+      R pv[C::NV];
 #pragma unroll
       for (int i = 0; i < LT_RPW; ++i) {
         R2 s2[FR / 2];
@@ -302,28 +339,28 @@ __global__ void __launch_bounds__(LT_NT) k_dp_latent(LatentArgs<R> a) {
           pv[i * FR + 2 * h + 1] = s2[h].y;
         }
       }
-      const R o = lt_reduce16(pv, lane);
+      const R o = lt_reduce<C::NV>(pv, lane);
       const int rl = warp * LT_RPW + qi, j = row0 + rl;  // chunk row, global row
       if (cur.grp == LT_A1) {
-        if ((lane & 1) == 0 && j < Hd) sm[C::H1 + j * FR + qr] = tanh(o + sm[C::B1 + j]);
+        if (qlead && j < Hd) sm[L.H1 + j * FR + qr] = tanh(o + sm[L.B1 + j]);
         continue;
       }
       if (cur.grp == LT_A2) {
-        if ((lane & 1) == 0 && j < Hd) sm[C::H2 + j * FR + qr] = tanh(o + sm[C::B2 + j]);
+        if (qlead && j < Hd) sm[L.H2 + j * FR + qr] = tanh(o + sm[L.B2 + j]);
         continue;
       }
-      // output layer + NLL gradient dL/do of sum x~/y + log y (both lanes of a pair)
+      // output layer + NLL gradient dL/do of sum x~/y + log y (all copies of an output)
       const bool ok = j < F && qr < nr;
       R go = 0;
       if (ok) {
-        const R rr = exp(o + sm[C::BS + buf * LT_CH + rl]);
+        const R rr = exp(o + sm[buf * L.stage + L.BS + rl]);
         if (refresh) {
-          if ((lane & 1) == 0) a.r[((size_t)b * T + t0 + qr) * F + j] = rr;
+          if (qlead) a.r[((size_t)b * T + t0 + qr) * F + j] = rr;
         } else {
-          const R l0 = sm[C::US + buf * LT_CH + rl] * sm[C::VS + qr] * rr;
-          const R* xr = sm + C::XS + buf * LT_CH * FR * M + (rl * FR + qr) * M;
-          const R* ls = sm + C::LS + buf * (NMAX - 1) * LT_CH * FR + rl * FR + qr;
-          const R* gs = sm + C::GS + buf * NMAX * LT_CH * M + rl * M;
+          const R l0 = sm[buf * L.stage + L.US + rl] * sm[L.VS + qr] * rr;
+          const R* xr = sm + buf * L.stage + L.XS + (rl * FR + qr) * M;
+          const R* ls = sm + buf * L.stage + L.LS + rl * FR + qr;
+          const R* gs = sm + buf * L.stage + L.GS + rl * M;
           R ln[NMAX];
 #pragma unroll
           for (int n = 1; n < NMAX; ++n) {
@@ -353,7 +390,7 @@ __global__ void __launch_bounds__(LT_NT) k_dp_latent(LatentArgs<R> a) {
       // backward part of the O chunk: acc[col][r] += go[row][r] W3[row][col]
 #pragma unroll
       for (int qq = 0; qq < LT_RPW * FR; ++qq) {
-        const R gq = __shfl_sync(0xffffffffu, go, 2 * qq);
+        const R gq = __shfl_sync(0xffffffffu, go, qq << C::QSH);
         const int i = qq / FR, r = qq % FR;
 #pragma unroll
         for (int c = 0; c < NCL / 2; ++c)
@@ -361,7 +398,7 @@ __global__ void __launch_bounds__(LT_NT) k_dp_latent(LatentArgs<R> a) {
       }
     } else {
       // C2 / C1: acc[col][r] += coef[row][r] W[row][col]
-      const R* coef = sm + (cur.grp == LT_C2 ? C::D2 : C::D1) + (row0 + warp * LT_RPW) * FR;
+      const R* coef = sm + (cur.grp == LT_C2 ? L.D2 : L.D1) + (row0 + warp * LT_RPW) * FR;
 #pragma unroll
       for (int i = 0; i < LT_RPW; ++i) {
         R cf[FR];
@@ -408,19 +445,19 @@ __global__ void __launch_bounds__(LT_NT) k_dp_latent(LatentArgs<R> a) {
       for (int ww = 0; ww < LT_NW; ++ww) sum += red[(ww * FR + r) * DEC_HMAX + col];
       const int i = col * FR + r;
       if (cur.grp == LT_O) {  // d2 = (W3^T go) (1 - h2^2)
-        const R hv = sm[C::H2 + i];
-        sm[C::D2 + i] = sum * (R(1) - hv * hv);
+        const R hv = sm[L.H2 + i];
+        sm[L.D2 + i] = sum * (R(1) - hv * hv);
       } else if (cur.grp == LT_C2) {  // d1 = (W2^T d2) (1 - h1^2)
-        const R hv = sm[C::H1 + i];
-        sm[C::D1 + i] = sum * (R(1) - hv * hv);
+        const R hv = sm[L.H1 + i];
+        sm[L.D1 + i] = sum * (R(1) - hv * hv);
       } else if (r < nr) {  // gz = W1^T d1; Adam on z
-        R* mp = sm + C::AM + r * DEC_DMAX + col;
-        R* vp = sm + C::AV + r * DEC_DMAX + col;
+        R* mp = sm + L.AM + r * DEC_DMAX + col;
+        R* vp = sm + L.AV + r * DEC_DMAX + col;
         const R mi = R(a.b1a) * *mp + R(1 - a.b1a) * sum;
         const R vi = R(a.b2a) * *vp + R(1 - a.b2a) * sum * sum;
         *mp = mi;
         *vp = vi;
-        sm[C::ZT + i] -= R(a.lr) * (mi / (R)c1) / (sqrt_r(vi / (R)c2) + R(a.eps));
+        sm[L.ZT + i] -= R(a.lr) * (mi / (R)c1) / (sqrt_r(vi / (R)c2) + R(a.eps));
       }
     }
   }
@@ -430,9 +467,9 @@ __global__ void __launch_bounds__(LT_NT) k_dp_latent(LatentArgs<R> a) {
   for (int e = tid; e < D * nr; e += LT_NT) {
     const int r = e / D, d = e - r * D;
     const size_t i = ((size_t)b * T + t0 + r) * D + d;
-    a.z[i] = sm[C::ZT + d * FR + r];
-    a.m[i] = sm[C::AM + r * DEC_DMAX + d];
-    a.v2[i] = sm[C::AV + r * DEC_DMAX + d];
+    a.z[i] = sm[L.ZT + d * FR + r];
+    a.m[i] = sm[L.AM + r * DEC_DMAX + d];
+    a.v2[i] = sm[L.AV + r * DEC_DMAX + d];
   }
 }
 

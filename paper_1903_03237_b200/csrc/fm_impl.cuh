@@ -6,6 +6,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -435,6 +436,8 @@ inline int mlp_gemm(const R* A, const R* Bm, const R* bias, const R* aux, R* Cm,
   return FM_OK;
 }
 
+constexpr size_t LT_SMEM_MAX = 226 * 1024;  // opt-in dynamic limit less the static kernel smem
+
 // The latent hook in one launch (fm_dp_latent.cuh): `steps` Adam steps and the
 // refresh r = exp(dec(z)); steps = 0 is the refresh alone.
 template <typename R>
@@ -470,7 +473,21 @@ int Impl<R>::dp_latent(const fm_dims* d, const fm_state* s, const fm_dp* p, int 
   a.eps = p->eps;
   dim3 grid((unsigned)((d->T + LT_FR - 1) / LT_FR), (unsigned)d->B);
   FM_DISPATCH_M(d->M, {
-    const size_t sm = sizeof(R) * LtCfg<R, MM>::TOTAL;
+    size_t sm = 0;
+    static const int max_stages = [] {  // FM_LT_STAGES: pipeline-depth tuning knob (2..4)
+      const char* e = getenv("FM_LT_STAGES");
+      const int v = e ? atoi(e) : 3;
+      return v < 2 ? 2 : v > 4 ? 4 : v;
+    }();
+    for (a.stages = max_stages; a.stages > 2; --a.stages) {  // deepest pipeline that fits
+      sm = sizeof(R) * lt_layout<R, MM>(a.stages, a.N).total;
+      if (sm <= LT_SMEM_MAX) break;
+    }
+    sm = sizeof(R) * lt_layout<R, MM>(a.stages, a.N).total;
+    if (sm > LT_SMEM_MAX) {
+      set_error("latent kernel needs %zu B shared memory (N=%d M=%d)", sm, a.N, (int)MM);
+      return FM_EINVAL;
+    }
     if (int rc = ensure_smem(k_dp_latent<R, MM>, sm)) return rc;
     launch_pdl(k_dp_latent<R, MM>, grid, dim3(LT_NT), sm, st, a);
     FM_CHECK_LAUNCH("k_dp_latent");
