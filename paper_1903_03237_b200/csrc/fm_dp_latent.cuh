@@ -37,8 +37,6 @@
 
 namespace fm {
 
-constexpr int LT_NT = 256;            // threads per CTA
-constexpr int LT_NW = LT_NT / 32;     // warps
 constexpr int LT_LDW = DEC_HMAX;      // row pitch of a staged chunk (elements)
 constexpr int LT_FR = 4;              // frames per CTA
 
@@ -62,13 +60,15 @@ template <typename R, int M> struct LtCfg {
   static constexpr int NCL = SPL * VEC;                     // columns per lane (4)
   static constexpr bool XVEC = (M * sizeof(R)) % 16 == 0;   // x~ / g rows in 16-byte segments
   static constexpr int CH = sizeof(R) == 4 ? 64 : 32;       // weight rows per chunk
-  static constexpr int RPW = CH / LT_NW;                    // chunk rows per warp (8 / 4)
+  static constexpr int NT = 256;                             // threads per CTA
+  static constexpr int NW = NT / 32;                        // warps
+  static constexpr int RPW = CH / NW;                       // chunk rows per warp (4)
   static constexpr int WB = CH * LT_LDW;                    // one weight buffer
   static constexpr int NV = RPW * FR;                       // forward outputs per warp
   static constexpr int QSH = NV == 8 ? 2 : NV == 16 ? 1 : 0; // lane -> output shift
   static_assert(NV == 8 || NV == 16 || NV == 32, "butterfly sizes");
   static_assert(NCL % 2 == 0, "column pairs");
-  static_assert(LT_NW * FR * DEC_HMAX <= WB, "layer-end partials fit a weight buffer");
+  static_assert(NW * FR * DEC_HMAX <= WB, "layer-end partials fit a weight buffer");
 };
 
 // shared-memory carve (elements of R) for S pipeline stages and N sources;
@@ -161,13 +161,13 @@ template <int NV, typename R> __device__ __forceinline__ R lt_reduce(R (&v)[NV],
 }
 
 template <typename R, int M>
-__global__ void __launch_bounds__(LT_NT) k_dp_latent(LatentArgs<R> a) {
+__global__ void __launch_bounds__(LtCfg<R, M>::NT) k_dp_latent(LatentArgs<R> a) {
   pdl_entry();
   using C = LtCfg<R, M>;
   constexpr int FR = C::FR, VEC = C::VEC, NCL = C::NCL, SPL = C::SPL;
   const LtLayout L = lt_layout<R, M>(a.stages, a.N);
   const int S = L.S;
-  constexpr int LT_CH = C::CH, LT_RPW = C::RPW;
+  constexpr int LT_CH = C::CH, LT_RPW = C::RPW, LT_NT = C::NT, LT_NW = C::NW;
   using R2 = typename RT<R>::C;
   extern __shared__ __align__(16) unsigned char lt_raw[];
   R* sm = reinterpret_cast<R*>(lt_raw);
@@ -199,16 +199,20 @@ __global__ void __launch_bounds__(LT_NT) k_dp_latent(LatentArgs<R> a) {
   const int iD0 = tid < stD * sgD ? tid / sgD : LT_CH, sD = tid % sgD;
   const int iH0 = tid < stH * sgH ? tid / sgH : LT_CH, sH = tid % sgH;
 
+  const unsigned sbase = (unsigned)__cvta_generic_to_shared(sm);
   auto load = [&](const LtIt& c, int buf) {
     const bool narrow = c.grp == LT_A1 || c.grp == LT_C1;
     const R* Wm = narrow ? a.W1 : c.grp == LT_O ? a.W3 : a.W2;
     const int rows = c.grp == LT_O ? F : Hd, K = narrow ? D : Hd;
     const int row0 = c.idx * LT_CH, nrow = min(LT_CH, rows - row0);
-    R* Wc = sm + buf * L.stage + L.W;
-    const R* Wg = Wm + (size_t)row0 * K;
     const int i0 = narrow ? iD0 : iH0, sg = narrow ? sD : sH, st = narrow ? stD : stH;
-    for (int i = i0; i < nrow; i += st)
-      cp_async16(Wc + i * LT_LDW + sg * VEC, Wg + (size_t)i * K + sg * VEC, true);
+    unsigned dst = sbase + (unsigned)((buf * L.stage + L.W + i0 * LT_LDW + sg * VEC) * sizeof(R));
+    const R* src = Wm + ((size_t)row0 + i0) * K + sg * VEC;
+    const unsigned dstep = (unsigned)(st * LT_LDW * sizeof(R));
+    const size_t sstep = (size_t)st * K;
+#pragma unroll 4
+    for (int i = i0; i < nrow; i += st, dst += dstep, src += sstep)
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src));
     if (c.grp != LT_O) return;
     const int f0 = row0;
     R* xs = sm + buf * L.stage + L.XS;

@@ -93,8 +93,10 @@ inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
 // Workspace plan for the fused iteration.
 struct Plan {
   int FT, TT;    // k_wstats bins per CTA, k_hstats frames per CTA
+  int HS, HFR;   // k_hstats bin splits and bins per split
   int TR, nseg;  // k_gain / k_vacc frames per CTA segment and segments per bin
-  size_t off_lam, off_phi, off_gpart, off_vpart, off_gnew, off_llp, off_ldp, off_cs, off_cnt, total;
+  size_t off_lam, off_phi, off_gpart, off_vpart, off_gnew, off_llp, off_ldp, off_cs, off_hpart;
+  size_t off_cnt, off_hcnt, total;
 };
 
 inline Plan make_plan(const fm_dims* d) {
@@ -107,6 +109,13 @@ inline Plan make_plan(const fm_dims* d) {
   while (p.FT > 8 && ((F + p.FT - 1) / p.FT) * B * N < target) p.FT /= 2;
   p.TT = 64;
   while (p.TT > 16 && ((T + p.TT - 1) / p.TT) * B * N < target) p.TT /= 2;
+  // k_hstats bin splits: fill the SMs when T-tiles x sources are few (each
+  // split keeps >= 64 bins, a multiple of the 32-bin staging chunk)
+  const long long htiles = ((T + p.TT - 1) / p.TT) * B * N;
+  long long hs = std::max<long long>(1, (target + htiles - 1) / htiles);
+  hs = std::min<long long>(hs, std::max<long long>(1, F / 64));
+  p.HFR = (int)((((F + hs - 1) / hs) + 31) / 32 * 32);
+  p.HS = (int)((F + p.HFR - 1) / p.HFR);
   // k_gain / k_vacc: segments per bin so that bins x segments >= ~4 CTAs per SM,
   // each segment a multiple of 256 frames (the fp32 chunk; 64/128 divide it)
   long long segs = std::max<long long>(1, (4 * 148 + F * B - 1) / (F * B));
@@ -126,7 +135,9 @@ inline Plan make_plan(const fm_dims* d) {
   p.off_llp = o; o = align256(o + (size_t)B * F * ((T + 255) / 256) * 8);
   p.off_ldp = o; o = align256(o + (size_t)B * F * 8);
   p.off_cs = o; o = align256(o + (size_t)B * F * NMAX * rs);
+  p.off_hpart = o; o = align256(o + (size_t)htiles * p.HS * 2 * 64 * 64 * rs);
   p.off_cnt = o; o = align256(o + 64);
+  p.off_hcnt = o; o = align256(o + (size_t)htiles * 4);
   p.total = o;
   return p;
 }
@@ -361,9 +372,10 @@ int Impl<R>::iterate_phase(const fm_dims* d, const fm_state* s, int phase, void*
         if constexpr (TTT >= 16) {
           const size_t smh = HsCfg<R, KB, TTT>::bytes;
           if (int rc = ensure_smem(k_hstats<R, KB, TTT>, smh)) return rc;
-          launch_pdl(k_hstats<R, KB, TTT>, dim3((unsigned)((T + TTT - 1) / TTT), BN), dim3(256),
-                     smh, st, phi, W, H, reinterpret_cast<R*>(hstat), N, F, T, K,
-                     phase == 0 ? 1 : 0, 0);
+          launch_pdl(k_hstats<R, KB, TTT>, dim3((unsigned)((T + TTT - 1) / TTT), BN, (unsigned)p.HS),
+                     dim3(256), smh, st, phi, W, H, reinterpret_cast<R*>(hstat), N, F, T, K,
+                     phase == 0 ? 1 : 0, 0, p.HFR, reinterpret_cast<R*>(w + p.off_hpart),
+                     reinterpret_cast<unsigned*>(w + p.off_hcnt));
           FM_CHECK_LAUNCH("k_hstats");
         }
       });
@@ -489,7 +501,7 @@ int Impl<R>::dp_latent(const fm_dims* d, const fm_state* s, const fm_dp* p, int 
       return FM_EINVAL;
     }
     if (int rc = ensure_smem(k_dp_latent<R, MM>, sm)) return rc;
-    launch_pdl(k_dp_latent<R, MM>, grid, dim3(LT_NT), sm, st, a);
+    launch_pdl(k_dp_latent<R, MM>, grid, dim3(LtCfg<R, MM>::NT), sm, st, a);
     FM_CHECK_LAUNCH("k_dp_latent");
   });
   return FM_OK;
@@ -594,8 +606,10 @@ int Impl<R>::iterate_dp(const fm_dims* d, const fm_state* s, const fm_dp* p, cud
       if constexpr (TTT >= 16) {
         const size_t smh = HsCfg<R, KB, TTT>::bytes;
         if (int rc = ensure_smem(k_hstats<R, KB, TTT>, smh)) return rc;
-        launch_pdl(k_hstats<R, KB, TTT>, dim3((unsigned)((T + TTT - 1) / TTT), BN), dim3(256), smh,
-                   st, (const R*)phi, (const R*)W, H, (R*)nullptr, N, F, T, K, 0, 1);
+        launch_pdl(k_hstats<R, KB, TTT>, dim3((unsigned)((T + TTT - 1) / TTT), BN, (unsigned)pl.HS),
+                   dim3(256), smh, st, (const R*)phi, (const R*)W, H, (R*)nullptr, N, F, T, K, 0, 1,
+                   pl.HFR, reinterpret_cast<R*>(w + pl.off_hpart),
+                   reinterpret_cast<unsigned*>(w + pl.off_hcnt));
         FM_CHECK_LAUNCH("k_hstats");
       }
     });

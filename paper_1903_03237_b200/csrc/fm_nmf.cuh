@@ -180,8 +180,10 @@ __global__ void __launch_bounds__(256) k_wstats(const R* __restrict__ phi, const
 // (b, n) and reduces over all local F itself; W rows and phi rows stream
 // through a cp.async double buffer in FCH-bin chunks; thread tile 4 k x 4 t
 // (x2). mode 0 applies the MU; mode 1 writes the (num, den) sums to hout
-// (B, 2, N, K, T) for the cross-shard all-reduce.
-// grid (ceil(T/TT), B*N), block 256.
+// (B, 2, N, K, T) for the cross-shard all-reduce. When T-tiles alone leave
+// SMs idle the bins split FS ways (grid z): each CTA publishes its partial
+// sums and the last one of the tile adds them in split order.
+// grid (ceil(T/TT), B*N, FS), block 256.
 // ---------------------------------------------------------------------------
 template <typename R, int KB, int TT> struct HsCfg {
   static constexpr int FCH = sizeof(R) == 4 ? 32 : 16;   // bins per staged chunk
@@ -196,7 +198,8 @@ template <typename R, int KB, int TT> struct HsCfg {
 template <typename R, int KB, int TT>
 __global__ void __launch_bounds__(256) k_hstats(const R* __restrict__ phi, const R* __restrict__ W,
                                                 R* __restrict__ H, R* __restrict__ hout, int N,
-                                                int F, int T, int K, int mode, int n0) {
+                                                int F, int T, int K, int mode, int n0, int frange,
+                                                R* __restrict__ part, unsigned* __restrict__ cnt) {
   pdl_entry();
   using Cf = HsCfg<R, KB, TT>;
   constexpr int FCH = Cf::FCH, NTH = Cf::NTH, S = Cf::S, LDW = Cf::LDW, LDP = Cf::LDP;
@@ -248,9 +251,10 @@ __global__ void __launch_bounds__(256) k_hstats(const R* __restrict__ phi, const
 #pragma unroll
     for (int j = 0; j < 4; ++j) a1[i][j] = a2[i][j] = 0;
   int st = 0;
-  load(0, 0);
-  for (int c0 = 0; c0 < F; c0 += FCH, st ^= 1) {
-    if (c0 + FCH < F) {
+  const int fbeg = blockIdx.z * frange, fend = min(F, fbeg + frange);  // this CTA's bin range
+  load(0, fbeg);
+  for (int c0 = fbeg; c0 < fend; c0 += FCH, st ^= 1) {
+    if (c0 + FCH < fend) {
       load(st ^ 1, c0 + FCH);
       cp_async_wait<1>();
     } else {
@@ -260,7 +264,7 @@ __global__ void __launch_bounds__(256) k_hstats(const R* __restrict__ phi, const
     const R* ws = stage(st);
     const R* p1s = ws + FCH * LDW;
     const R* p2s = p1s + FCH * LDP;
-    const int fe = min(FCH, F - c0);
+    const int fe = min(FCH, fend - c0);
     for (int fl = s; fl < fe; fl += S) {
       R w[4], x1[4], x2[4];
       lds4(ws + fl * LDW + kg * 4, w);
@@ -287,13 +291,43 @@ __global__ void __launch_bounds__(256) k_hstats(const R* __restrict__ phi, const
     }
   __syncthreads();
   R* Hn = H + (size_t)bn * K * T;
-  for (int e = tid; e < KB * TT; e += 256) {
-    const int k = e / TT, tl = e % TT, t = t0 + tl;
-    if (k < K && t < T) {
+  const int FS = gridDim.z;
+  R* pt = part + ((size_t)(bn * gridDim.x + blockIdx.x) * FS) * 2 * KB * TT;  // [FS][2][KB][TT]
+  if (FS > 1) {
+    // bin-split: publish this CTA's sums; the last CTA of the T-tile adds the
+    // FS partials in split order (deterministic) and finishes the update
+    for (int e = tid; e < KB * TT; e += 256) {
       R sn = 0, sd = 0;
       for (int q = 0; q < S; ++q) {
         sn += red[(q * 2) * KB * TT + e];
         sd += red[(q * 2 + 1) * KB * TT + e];
+      }
+      pt[((size_t)blockIdx.z * 2) * KB * TT + e] = sn;
+      pt[((size_t)blockIdx.z * 2 + 1) * KB * TT + e] = sd;
+    }
+    __threadfence();
+    __syncthreads();
+    __shared__ unsigned last;
+    if (tid == 0) last = atomicAdd(cnt + bn * gridDim.x + blockIdx.x, 1u) == (unsigned)FS - 1;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    if (tid == 0) cnt[bn * gridDim.x + blockIdx.x] = 0;  // re-armed for the next launch
+  }
+  for (int e = tid; e < KB * TT; e += 256) {
+    const int k = e / TT, tl = e % TT, t = t0 + tl;
+    if (k < K && t < T) {
+      R sn = 0, sd = 0;
+      if (FS > 1) {
+        for (int z = 0; z < FS; ++z) {
+          sn += __ldcg(pt + ((size_t)z * 2) * KB * TT + e);
+          sd += __ldcg(pt + ((size_t)z * 2 + 1) * KB * TT + e);
+        }
+      } else {
+        for (int q = 0; q < S; ++q) {
+          sn += red[(q * 2) * KB * TT + e];
+          sd += red[(q * 2 + 1) * KB * TT + e];
+        }
       }
       if (mode == 0) {
         Hn[(size_t)k * T + t] *= mu_factor(sn, sd);  // sources.py:198
