@@ -419,35 +419,6 @@ int Impl<R>::iterate_phase(const fm_dims* d, const fm_state* s, int phase, void*
 // ---------------------------------------------------------------------------
 // FastMNMF-DP (config 4)
 // ---------------------------------------------------------------------------
-struct DpWs {
-  size_t h1, h2, d1, d2, go, gz, total;
-};
-inline DpWs dp_ws(const fm_dims* d, const fm_dp* p) {
-  const size_t rs = d->dtype == FM_F64 ? 8 : 4;
-  const size_t BT = (size_t)d->B * d->T;
-  DpWs w;
-  size_t o = 0;
-  w.h1 = o; o = align256(o + BT * p->Hd * rs);
-  w.h2 = o; o = align256(o + BT * p->Hd * rs);
-  w.d1 = o; o = align256(o + BT * p->Hd * rs);
-  w.d2 = o; o = align256(o + BT * p->Hd * rs);
-  w.go = o; o = align256(o + BT * d->F * rs);
-  w.gz = o; o = align256(o + BT * p->D * rs);
-  w.total = o;
-  return w;
-}
-
-template <typename R, bool BT, int EPI, int TM = 32, int TN = 32>
-inline int mlp_gemm(const R* A, const R* Bm, const R* bias, const R* aux, R* Cm, int Rows, int Ncol,
-                    int K, long long sA, long long sC, int B, cudaStream_t st,
-                    AdamEpi<R> ad = AdamEpi<R>{}) {
-  dim3 grid((unsigned)((Ncol + TN - 1) / TN), (unsigned)((Rows + TM - 1) / TM), (unsigned)B);
-  launch_pdl(k_mlp_gemm<R, BT, EPI, TM, TN>, grid, dim3(256), 0, st, A, Bm, bias, aux, Cm, Rows, Ncol,
-             K, sA, sC, ad);
-  FM_CHECK_LAUNCH("k_mlp_gemm");
-  return FM_OK;
-}
-
 constexpr size_t LT_SMEM_MAX = 226 * 1024;  // opt-in dynamic limit less the static kernel smem
 
 // The latent hook in one launch (fm_dp_latent.cuh): `steps` Adam steps and the
