@@ -15,6 +15,7 @@
 #include "fm_kernels.cuh"
 #include "fm_ops.cuh"
 #include "fm_dp_latent.cuh"
+#include "fm_vacc_tc.cuh"
 
 namespace fm {
 
@@ -246,8 +247,25 @@ int Impl<R>::vacc(const fm_dims* d, const fm_state* s, cudaStream_t st) {
   a.gnew = reinterpret_cast<R*>(w + p.off_gnew);
   a.part = reinterpret_cast<R*>(w + p.off_vpart);
   a.F = (int)d->F; a.T = (int)d->T; a.N = (int)d->N; a.TR = p.TR;
+  static const int dbg = [] { const char* e = getenv("FM_VTC_DBG"); return e ? atoi(e) : 0; }();
+  a.dbg = dbg;
   dim3 grid((unsigned)p.nseg, (unsigned)d->F, (unsigned)d->B);
+  static const bool simt = [] {  // FM_VACC=simt: the SIMT accumulation (A/B comparisons)
+    const char* e = getenv("FM_VACC");
+    return e && strcmp(e, "simt") == 0;
+  }();
   FM_DISPATCH_M(d->M, {
+    if constexpr (sizeof(R) == 4 && MM >= 12) {
+      // complex64, M >= 12: tensor-core accumulation (fm_vacc_tc.cuh); at
+      // M <= 8 the SS-mode MMAs (N = M) are smem-read bound and SIMT wins
+      if (!simt) {
+        const size_t smv = VtcCfg<MM>::SMEM;
+        if (int rc = ensure_smem(k_vacc_tc<MM>, smv)) return rc;
+        launch_pdl(k_vacc_tc<MM>, grid, dim3(VtcCfg<MM>::BS), smv, st, a);
+        FM_CHECK_LAUNCH("k_vacc_tc");
+        return FM_OK;
+      }
+    }
     launch_pdl(k_vacc<R, MM>, grid, dim3(VaCfg<R, MM>::BS), 0, st, a);
     FM_CHECK_LAUNCH("k_vacc");
   });

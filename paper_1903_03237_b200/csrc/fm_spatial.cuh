@@ -175,6 +175,7 @@ template <typename R> struct VaccArgs {
   R* gnew;         // (B, N, F, M) gains after the MU (written by segment 0)
   R* part;         // (B, F, nseg, M, P) complex partial V sums
   int F, T, N, TR;
+  int dbg;         // timing experiments only (k_vacc_tc): 1 skip MMAs, 2 skip operand builds
 };
 
 // g MU (separate.py:218-220) + V_fm = (1/T) sum_t x x^H / y_ftm with y from
