@@ -26,24 +26,30 @@ namespace fm {
 template <int M> struct VtcCfg {
   static constexpr int P = M * (M + 1) / 2;
   static constexpr int J = M * M;                  // real rows of A
-  static constexpr int NTILE = (J + 127) / 128;    // 128-lane accumulator tiles
-  static constexpr int JP = NTILE * 128;
+  static constexpr int NTILE = (J + 127) / 128;    // 128-lane tiles (A and accumulator)
   static constexpr int NB = (M + 7) / 8 * 8;       // MMA N (weights per m, padded)
-  static constexpr int KC = 32;                    // frames per chunk (KC/8 MMA k-steps)
+  static constexpr int KC = 16;                    // frames per chunk (KC/8 MMA k-steps)
   static constexpr int BS = 256;
-  static constexpr int SBO = (KC / 4) * 128;       // bytes between 8-row core groups
-  static constexpr int ABYTES = JP * KC * 4;       // one A plane (hi or lo)
-  static constexpr int BBYTES = NB * KC * 4;
+  static constexpr int WG = 8 / (4 * NTILE);       // warp groups sharing a tile's rows (split frames)
+  static constexpr int KW = KC / WG;               // frames per thread per chunk
+  static constexpr int SBO = (KC / 4) * 128;       // B plane: bytes between 8-row core groups
+  static constexpr int BBYTES = NB * KC * 4;       // one B plane (hi or lo)
   static constexpr int TBLK = M <= 8 ? 256 : 128;  // frames staged per block (x, 1/y)
-  static constexpr int STAGE = 2 * ABYTES + 2 * BBYTES;
-  static constexpr int XS = 2 * STAGE;             // x block (TBLK x M complex)
+  static constexpr int STAGE = 2 * BBYTES;
+  static constexpr int XS = 2 * STAGE;             // x block (M x TBLK complex, padded rows)
   static constexpr int XLD = TBLK + 2;             // x row pitch (complex): rows land on distinct banks
   static constexpr int IYS = XS + XLD * M * 8;     // 1/y block (M x TBLK)
   static constexpr int SMEM = IYS + TBLK * M * 4;
-  static constexpr int TCOLS = 32;                 // TMEM columns allocated (>= NTILE * NB)
-  static_assert(NTILE * NB <= TCOLS, "accumulator columns");
-  static_assert(STAGE % 128 == 0 || true, "");
+  // TMEM columns: accumulator [0, NTILE*NB), then per stage, tile and plane (hi, lo) KC columns
+  static constexpr int ACOL = 32;
+  static constexpr int TCOLS_USED = ACOL + 2 * NTILE * 2 * KC;
+  static constexpr int TCOLS = TCOLS_USED <= 128 ? 128 : TCOLS_USED <= 256 ? 256 : 512;
+  static_assert(NTILE * NB <= ACOL, "accumulator columns");
+  static_assert(WG >= 1 && KC % WG == 0, "warp groups");
 };
+__host__ __device__ constexpr int vtc_acol(int stage, int tile, int plane, int ntile, int kc) {
+  return 32 + ((stage * ntile + tile) * 2 + plane) * kc;
+}
 
 // byte offset of element (row, k) in a K-major no-swizzle operand plane
 template <int M> __device__ __forceinline__ uint32_t vtc_off(int row, int k) {
@@ -87,6 +93,40 @@ __device__ __forceinline__ void umma_tf32(uint32_t tmem_d, uint64_t adesc, uint6
       "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
 }
+// A operand from tensor memory (rows = lanes, K along columns)
+__device__ __forceinline__ void umma_tf32_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
+                                             uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+// registers -> TMEM: lane (warp quadrant) x NC consecutive columns
+template <int NC> __device__ __forceinline__ void tmem_st_row(uint32_t taddr, const float (&v)[NC]);
+template <> __device__ __forceinline__ void tmem_st_row<8>(uint32_t taddr, const float (&v)[8]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr),
+               "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7])
+               : "memory");
+}
+template <> __device__ __forceinline__ void tmem_st_row<16>(uint32_t taddr, const float (&v)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+          taddr),
+      "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]), "f"(v[8]),
+      "f"(v[9]), "f"(v[10]), "f"(v[11]), "f"(v[12]), "f"(v[13]), "f"(v[14]), "f"(v[15])
+      : "memory");
+}
+template <> __device__ __forceinline__ void tmem_st_row<32>(uint32_t taddr, const float (&v)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]), "f"(v[8]),
+      "f"(v[9]), "f"(v[10]), "f"(v[11]), "f"(v[12]), "f"(v[13]), "f"(v[14]), "f"(v[15]), "f"(v[16]),
+      "f"(v[17]), "f"(v[18]), "f"(v[19]), "f"(v[20]), "f"(v[21]), "f"(v[22]), "f"(v[23]), "f"(v[24]),
+      "f"(v[25]), "f"(v[26]), "f"(v[27]), "f"(v[28]), "f"(v[29]), "f"(v[30]), "f"(v[31])
+      : "memory");
+}
 
 template <int NB> __device__ __forceinline__ void tmem_ld_row(uint32_t taddr, float (&v)[NB]) {
   uint32_t r[NB];
@@ -115,6 +155,7 @@ __global__ void __launch_bounds__(256) k_vacc_tc(VaccArgs<float> a) {
   using Cf = VtcCfg<M>;
   using C = float2;
   constexpr int P = Cf::P, J = Cf::J, NTILE = Cf::NTILE, NB = Cf::NB, KC = Cf::KC, BS = Cf::BS;
+  constexpr int KW = Cf::KW;
   extern __shared__ __align__(1024) unsigned char smv[];
   __shared__ __align__(8) uint64_t mbar[2];
   __shared__ uint32_t tmem_base;
@@ -171,8 +212,32 @@ __global__ void __launch_bounds__(256) k_vacc_tc(VaccArgs<float> a) {
   const uint32_t sbase = (unsigned)__cvta_generic_to_shared(smv);
   // operand descriptors of stage 0 (A hi plane, B hi plane); per-MMA offsets are
   // added to the 14-bit start-address field (16-byte units, no carry out: < 256 KB)
-  const uint64_t dA = umma_desc(sbase, 128, Cf::SBO);
-  const uint64_t dB = umma_desc(sbase + 2 * Cf::ABYTES, 128, Cf::SBO);
+  const uint64_t dB = umma_desc(sbase, 128, Cf::SBO);
+  // this thread's A row: tile (warp / 4 when two tiles), lane quadrant (warp % 4), frame group
+  const int tile = NTILE == 2 ? warp >> 2 : 0, wg = NTILE == 2 ? 0 : warp >> 2;
+  const int arow = tile * 128 + (warp & 3) * 32 + lane;  // A row j (rows >= J are padding)
+  int ai = 0, ak = 0;
+  {
+    const int j = arow < J ? arow : 0;
+    int p = j, q = j - P;
+    if (j >= P) {  // Im of the q-th off-diagonal pair
+      int i = 0, rem = q;
+      while (rem >= M - 1 - i) {
+        rem -= M - 1 - i;
+        ++i;
+      }
+      ai = i;
+      ak = i + 1 + rem;
+    } else {
+      int i = 0, rem = p;
+      while (rem >= M - i) {
+        rem -= M - i;
+        ++i;
+      }
+      ai = i;
+      ak = i + rem;
+    }
+  }
   constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(NB >> 3) << 17) |
                              ((uint32_t)(128 >> 4) << 24);
 
@@ -226,14 +291,11 @@ __global__ void __launch_bounds__(256) k_vacc_tc(VaccArgs<float> a) {
     const int nchb = min(TBLK, tb - b0 + KC - 1) / KC;
     for (int cb = 0; cb < nchb; ++cb, ++c) {
       const int s = c & 1;
-      unsigned char* st = smv + s * Cf::STAGE;
-      unsigned char* Ahi = st;
-      unsigned char* Alo = st + Cf::ABYTES;
-      unsigned char* Bhi = st + 2 * Cf::ABYTES;
+      unsigned char* Bhi = smv + s * Cf::STAGE;
       unsigned char* Blo = Bhi + Cf::BBYTES;
       if (c >= 2) mbar_wait(&mbar[s], (unsigned)(((c >> 1) - 1) & 1));  // MMAs of chunk c-2 done
       const int k0 = cb * KC;  // chunk's first frame inside the block
-      // B rows: 1/y of the chunk's frames, 4 frames per item
+      // B rows: 1/y of the chunk's frames, 4 frames per item (smem, UMMA K-major)
       for (int e = a.dbg == 2 ? BS : tid; e < M * (KC / 4); e += BS) {
         const int m = e / (KC / 4), kq = e % (KC / 4);
         const float4 v = *reinterpret_cast<const float4*>(Ys + m * TBLK + k0 + kq * 4);
@@ -243,33 +305,30 @@ __global__ void __launch_bounds__(256) k_vacc_tc(VaccArgs<float> a) {
         *reinterpret_cast<float4*>(Bhi + o) = h;
         *reinterpret_cast<float4*>(Blo + o) = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
       }
-      // A rows: one pair x 4 consecutive frames per item -> its Re row and its Im row
-      for (int e = a.dbg == 2 ? P * KC : tid; e < P * (KC / 4); e += BS) {
-        const int p = e % P, kq = e / P;
-        const int i = pairI[p], k = pairK[p], jm = pairIm[p];
-        const float4* pi = reinterpret_cast<const float4*>(Xs + i * Cf::XLD + k0 + kq * 4);
-        const float4* pk = reinterpret_cast<const float4*>(Xs + k * Cf::XLD + k0 + kq * 4);
-        const float4 i01 = pi[0], i23 = pi[1], k01 = pk[0], k23 = pk[1];
-        float re[4], im[4];
-        re[0] = i01.x * k01.x + i01.y * k01.y;  im[0] = i01.y * k01.x - i01.x * k01.y;
-        re[1] = i01.z * k01.z + i01.w * k01.w;  im[1] = i01.w * k01.z - i01.z * k01.w;
-        re[2] = i23.x * k23.x + i23.y * k23.y;  im[2] = i23.y * k23.x - i23.x * k23.y;
-        re[3] = i23.z * k23.z + i23.w * k23.w;  im[3] = i23.w * k23.z - i23.z * k23.w;
-        float4 h, w;
-        h.x = tf32_rna(re[0]); h.y = tf32_rna(re[1]); h.z = tf32_rna(re[2]); h.w = tf32_rna(re[3]);
-        w.x = re[0] - h.x; w.y = re[1] - h.y; w.z = re[2] - h.z; w.w = re[3] - h.w;
-        uint32_t o = vtc_off<M>(p, kq * 4);
-        *reinterpret_cast<float4*>(Ahi + o) = h;
-        *reinterpret_cast<float4*>(Alo + o) = w;
-        if (jm >= 0) {
-          h.x = tf32_rna(im[0]); h.y = tf32_rna(im[1]); h.z = tf32_rna(im[2]); h.w = tf32_rna(im[3]);
-          w.x = im[0] - h.x; w.y = im[1] - h.y; w.z = im[2] - h.z; w.w = im[3] - h.w;
-          o = vtc_off<M>(jm, kq * 4);
-          *reinterpret_cast<float4*>(Ahi + o) = h;
-          *reinterpret_cast<float4*>(Alo + o) = w;
+      // A rows -> TMEM: this thread's row (lane) for its KW frames, hi and lo planes
+      if (a.dbg != 2) {
+        const bool im = arow >= P;
+        const C* xi = Xs + ai * Cf::XLD + k0 + wg * KW;
+        const C* xk = Xs + ak * Cf::XLD + k0 + wg * KW;
+        float hv[KW], lv[KW];
+#pragma unroll
+        for (int u = 0; u < KW; u += 2) {
+          const float4 pi = *reinterpret_cast<const float4*>(xi + u);
+          const float4 pk = *reinterpret_cast<const float4*>(xk + u);
+          const float v0 = im ? (pi.y * pk.x - pi.x * pk.y) : (pi.x * pk.x + pi.y * pk.y);
+          const float v1 = im ? (pi.w * pk.z - pi.z * pk.w) : (pi.z * pk.z + pi.w * pk.w);
+          hv[u] = tf32_rna(v0);
+          hv[u + 1] = tf32_rna(v1);
+          lv[u] = v0 - hv[u];
+          lv[u + 1] = v1 - hv[u + 1];
         }
+        const uint32_t lanes = (uint32_t)((warp & 3) * 32) << 16;
+        tmem_st_row<KW>(tmem + lanes + vtc_acol(s, tile, 0, NTILE, KC) + wg * KW, hv);
+        tmem_st_row<KW>(tmem + lanes + vtc_acol(s, tile, 1, NTILE, KC) + wg * KW, lv);
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncthreads();
       if (tid == 0) {
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -279,13 +338,13 @@ __global__ void __launch_bounds__(256) k_vacc_tc(VaccArgs<float> a) {
           const uint64_t dbh = dB + so + ks * 16, dbl = dB + so + (Cf::BBYTES >> 4) + ks * 16;
 #pragma unroll
           for (int tt = 0; tt < NTILE; ++tt) {
-            const uint64_t dah = dA + so + tt * Cf::SBO + ks * 16;  // tt*16*SBO bytes >> 4
-            const uint64_t dal = dah + (Cf::ABYTES >> 4);
+            const uint32_t tah = tmem + (uint32_t)(vtc_acol(s, tt, 0, NTILE, KC) + ks * 8);
+            const uint32_t tal = tmem + (uint32_t)(vtc_acol(s, tt, 1, NTILE, KC) + ks * 8);
             const uint32_t td = tmem + (uint32_t)(tt * NB);
             if (a.dbg == 1) continue;
-            umma_tf32(td, dah, dbh, IDESC, (c > 0 || ks > 0) ? 1u : 0u);
-            umma_tf32(td, dah, dbl, IDESC, 1u);
-            umma_tf32(td, dal, dbh, IDESC, 1u);
+            umma_tf32_ts(td, tah, dbh, IDESC, (c > 0 || ks > 0) ? 1u : 0u);
+            umma_tf32_ts(td, tah, dbl, IDESC, 1u);
+            umma_tf32_ts(td, tal, dbh, IDESC, 1u);
           }
         }
         asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
