@@ -360,10 +360,21 @@ def main():
         run(scfg, Xh, init=tuple(a[0].numpy() for a in init))  # warm
         torch.cuda.synchronize()
         reps = 3
+        prof = None
+        if os.environ.get("BENCH_E2E_PROFILE"):
+            import cProfile
+
+            prof = cProfile.Profile()
+            prof.enable()
         t0 = time.perf_counter()
         for _ in range(reps):
             res = run(scfg, Xh, init=tuple(a[0].numpy() for a in init))
         dt = (time.perf_counter() - t0) / reps
+        if prof is not None:
+            import pstats
+
+            prof.disable()
+            pstats.Stats(prof, stream=sys.stderr).sort_stats("cumulative").print_stats(20)
         cb = 8 if cfg["precision"] == "complex64" else 16
         h2d = F * T * M * cb + F * M * M * 16 + N * F * M * 8 + N * F * K * 8 + N * K * T * 8
         d2h = N * F * T * M * cb + iters * 8

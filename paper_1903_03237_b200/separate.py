@@ -324,11 +324,12 @@ def _prepare_observation(X, cfg, torch):
     cdt = torch.complex64 if cfg.precision == "complex64" else torch.complex128
     if isinstance(X, torch.Tensor):
         Xd = X.to(device=cfg.device, dtype=cdt).contiguous()
-    else:
-        Xn = np.asarray(X)
-        if not np.all(np.isfinite(Xn)):
-            raise InvalidInputError("observation contains non-finite values")
-        Xd = torch.from_numpy(np.ascontiguousarray(Xn.astype(np.complex128))).to(cfg.device, cdt)
+    else:  # host numpy: copy at its own width, convert on the device (non-finite values
+        # surface in the device power statistics below)
+        Xn = np.ascontiguousarray(np.asarray(X))
+        if not np.iscomplexobj(Xn):
+            Xn = Xn.astype(np.complex128)
+        Xd = torch.from_numpy(Xn).to(cfg.device).to(cdt).contiguous()
     if Xd.dim() == 3:
         Xd = Xd.unsqueeze(0)
     B, F, T, M = Xd.shape
@@ -352,6 +353,27 @@ def _prepare_observation(X, cfg, torch):
                                         _lib.stream_ptr()), "fm_observation_stats")
     floor = torch.tensor([1e-12 * v for v in maxsq[:]], dtype=torch.float64)  # spatial.py:64-66
     return Xd, scale, floor.to(cfg.device)
+
+
+_STAGING = {}
+
+
+def _to_host(t):
+    """Device tensor -> fresh host tensor: async copy into a cached pinned
+    staging buffer, then a multi-threaded host copy into pageable memory
+    (a plain .cpu() of a large tensor runs at pageable-DMA speed)."""
+    torch = _torch()
+    n = t.numel() * t.element_size()
+    buf = _STAGING.get("buf")
+    if buf is None or buf.numel() < n:
+        buf = torch.empty((max(n, 1),), dtype=torch.uint8, pin_memory=True)
+        _STAGING["buf"] = buf
+    st = buf[:n].view(t.dtype).view(t.shape)
+    st.copy_(t.contiguous(), non_blocking=True)
+    torch.cuda.current_stream().synchronize()
+    out = torch.empty(t.shape, dtype=t.dtype)
+    out.copy_(st)
+    return out
 
 
 def _as_batch(a, torch, B):
@@ -430,7 +452,8 @@ def run(cfg: SeparatorConfig, X_FTM, on_iteration=None, init=None) -> Separation
         time_trace.append(prev.elapsed_time(e) / 1e3)
         prev = e
     ll = loop.trace[:, 0].cpu().numpy().copy() if cfg.record_likelihood else np.zeros(0)
-    images = loop.images(scale)[0].cpu().numpy().astype(np.complex128)
+    # images at the run's precision (complex64 runs return complex64), through pinned staging
+    images = _to_host(loop.images(scale)[0]).numpy()
     res = SeparationResult(images_NFTM=images, likelihood_trace=np.asarray(ll),
                            time_trace=np.asarray(time_trace), method=cfg.method,
                            config=replace(cfg))

@@ -1,0 +1,65 @@
+"""Wall-clock breakdown of one public run() call at config 1 (e2e leg of bench.py)."""
+import time
+
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+from paper_1903_03237_b200 import SeparatorConfig, separate as S
+from paper_1903_03237_b200.synth import CONFIGS, baseline_init, make_mixture_torch
+
+cfg = CONFIGS["c1"]
+F, T, M, N, K = (cfg[k] for k in ("F", "T", "M", "N", "K"))
+X = make_mixture_torch(F, T, M, N, K, seed=0, device="cuda").to(torch.complex64).unsqueeze(0)
+Xh = X[0].cpu().pin_memory()
+init = baseline_init(F, T, M, N, K, 0)
+scfg = SeparatorConfig(method="fast-mnmf", n_sources=N, n_basis=K, n_iterations=100, precision="complex64")
+S.run(scfg, Xh, init=init)
+torch.cuda.synchronize()
+
+
+def tick(tag, t):
+    torch.cuda.synchronize()
+    now = time.perf_counter()
+    print(f"{tag:28s} {1e3 * (now - t):8.2f} ms", flush=True)
+    return now
+
+
+for rep in range(2):
+    t = time.perf_counter()
+    t00 = t
+    Xs, scale, floor = S._prepare_observation(Xh, scfg, torch)
+    t = tick("prepare_observation", t)
+    loop = S.DeviceLoop(Xs, S._as_batch(init[0], torch, 1), S._as_batch(init[1], torch, 1),
+                        S._as_batch(init[2], torch, 1), S._as_batch(init[3], torch, 1), floor,
+                        True, 1, n_trace=100)
+    t = tick("DeviceLoop()", t)
+    loop.prologue()
+    t = tick("prologue", t)
+    loop.run(1, use_graph=True)
+    t = tick("iteration 1 (graph capture)", t)
+    for _ in range(99):
+        loop.run(1, use_graph=True)
+    t = tick("iterations 2..100", t)
+    img = loop.images(scale)[0]
+    t = tick("images (device)", t)
+    n = img.numel() * img.element_size()
+    if "buf" not in S._STAGING or S._STAGING["buf"].numel() < n:
+        S._STAGING["buf"] = torch.empty((n,), dtype=torch.uint8, pin_memory=True)
+    t = tick("pinned alloc (cached)", t)
+    st = S._STAGING["buf"][:n].view(img.dtype).view(img.shape)
+    st.copy_(img, non_blocking=True)
+    t = tick("D2H into pinned", t)
+    out = torch.empty(img.shape, dtype=img.dtype)
+    t = tick("host empty", t)
+    out.copy_(st)
+    t = tick("host copy (torch)", t)
+    o2 = np.empty(tuple(img.shape), dtype=np.complex64)
+    np.copyto(o2, st.numpy())
+    t = tick("host copy (numpy)", t)
+    print("torch threads", torch.get_num_threads())
+    print(f"{'total':28s} {1e3 * (t - t00):8.2f} ms")
