@@ -8,6 +8,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -740,20 +741,51 @@ int Impl<R>::wiener(int64_t N, int64_t F, int64_t T, int64_t M, const void* lam,
   return FM_OK;
 }
 
+// Small persistent device + pinned host scratch for the synchronous prologue
+// helpers (observation statistics, scaling): a per-call cudaMallocAsync /
+// cudaFreeAsync re-mapped pool memory on every run() (~10 ms per call).
+struct HostSync {
+  std::mutex mu;
+  double* dev = nullptr;
+  double* host = nullptr;
+  size_t n = 0;
+  int grow(size_t need) {
+    if (need <= n) return FM_OK;
+    if (dev) cudaFree(dev);
+    if (host) cudaFreeHost(host);
+    dev = nullptr;
+    host = nullptr;
+    n = 0;
+    if (cudaMalloc(&dev, need * sizeof(double)) != cudaSuccess ||
+        cudaMallocHost(&host, need * sizeof(double)) != cudaSuccess) {
+      set_error("scratch allocation of %zu doubles failed", need);
+      return FM_ECUDA;
+    }
+    n = need;
+    return FM_OK;
+  }
+};
+inline HostSync& host_sync() {
+  static HostSync h;
+  return h;
+}
+
 template <typename R>
 int Impl<R>::obs_stats(const fm_dims* d, const void* X, double* sumsq, double* maxsq,
                        cudaStream_t st) {
   const long long per_b = d->F * d->T * d->M;
   const unsigned nblk = (unsigned)std::max<long long>(1, std::min<long long>(256, (per_b + 4095) / 4096));
-  double* buf = nullptr;
-  FM_CUDA(cudaMallocAsync(&buf, sizeof(double) * 2 * nblk * d->B, st));
+  HostSync& hs = host_sync();
+  std::lock_guard<std::mutex> lock(hs.mu);
+  const size_t nv = (size_t)2 * nblk * d->B;
+  if (int rc = hs.grow(nv)) return rc;
+  double* buf = hs.dev;
   k_obs_stats<R><<<dim3(nblk, (unsigned)d->B), 256, 0, st>>>(reinterpret_cast<const C*>(X), per_b,
                                                              buf, buf + (size_t)nblk * d->B);
   FM_CHECK_LAUNCH("k_obs_stats");
-  std::vector<double> h((size_t)2 * nblk * d->B);
-  FM_CUDA(cudaMemcpyAsync(h.data(), buf, sizeof(double) * h.size(), cudaMemcpyDeviceToHost, st));
-  FM_CUDA(cudaFreeAsync(buf, st));
+  FM_CUDA(cudaMemcpyAsync(hs.host, buf, sizeof(double) * nv, cudaMemcpyDeviceToHost, st));
   FM_CUDA(cudaStreamSynchronize(st));
+  const double* h = hs.host;
   for (long long b = 0; b < d->B; ++b) {
     double s = 0.0, m = 0.0;
     for (unsigned i = 0; i < nblk; ++i) {
@@ -769,13 +801,15 @@ int Impl<R>::obs_stats(const fm_dims* d, const void* X, double* sumsq, double* m
 template <typename R>
 int Impl<R>::scale(const fm_dims* d, void* X, const double* scale_host, cudaStream_t st) {
   const long long per_b = d->F * d->T * d->M;
-  double* sc = nullptr;
-  FM_CUDA(cudaMallocAsync(&sc, sizeof(double) * d->B, st));
-  FM_CUDA(cudaMemcpyAsync(sc, scale_host, sizeof(double) * d->B, cudaMemcpyHostToDevice, st));
+  HostSync& hs = host_sync();
+  std::lock_guard<std::mutex> lock(hs.mu);
+  if (int rc = hs.grow((size_t)d->B)) return rc;
+  double* sc = hs.dev;
+  memcpy(hs.host, scale_host, sizeof(double) * d->B);
+  FM_CUDA(cudaMemcpyAsync(sc, hs.host, sizeof(double) * d->B, cudaMemcpyHostToDevice, st));
   const long long n = per_b * d->B;
   k_scale<R><<<(unsigned)((n + 255) / 256), 256, 0, st>>>(reinterpret_cast<C*>(X), per_b, sc, (int)d->B);
   FM_CHECK_LAUNCH("k_scale");
-  FM_CUDA(cudaFreeAsync(sc, st));
   FM_CUDA(cudaStreamSynchronize(st));
   return FM_OK;
 }

@@ -18,6 +18,9 @@ X = make_mixture_torch(F, T, M, N, K, seed=0, device="cuda").to(torch.complex64)
 Xh = X[0].cpu().pin_memory()
 init = baseline_init(F, T, M, N, K, 0)
 scfg = SeparatorConfig(method="fast-mnmf", n_sources=N, n_basis=K, n_iterations=100, precision="complex64")
+if "--bench-like" in sys.argv:  # the bench process also holds its own loop and a 256 MiB flush buffer
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    keep = S.run(scfg, Xh, init=init)
 S.run(scfg, Xh, init=init)
 torch.cuda.synchronize()
 
@@ -32,6 +35,8 @@ def tick(tag, t):
 for rep in range(2):
     t = time.perf_counter()
     t00 = t
+    Xd = Xh.to("cuda")
+    t = tick("H2D X", t)
     Xs, scale, floor = S._prepare_observation(Xh, scfg, torch)
     t = tick("prepare_observation", t)
     loop = S.DeviceLoop(Xs, S._as_batch(init[0], torch, 1), S._as_batch(init[1], torch, 1),
