@@ -197,6 +197,16 @@ int fm_observation_stats(const fm_dims* d, const void* X, double* sumsq_host,
                          double* maxsq_host, void* stream);
 int fm_scale_observation(const fm_dims* d, void* X, const double* scale_host, void* stream);
 
+/* The reference's default spatial initialisation, per mixture and bin
+ * (spatial.py:109-121 circular_init -> init_spatial(..., "diagonalizable")
+ * spatial.py:93-105, clamp_psd linalg.py:85-94, hermitian_eig
+ * linalg.py:23-33): G1 = clamp_psd(sum_t x x^H / T), w, U = eig descending,
+ * Q = U^H. X is the SCALED observation (B, F, T, M) on the device; Q
+ * (B, F, M, M) complex of d->dtype; w (B, F, M) fp64 clamped eigenvalues,
+ * descending (may be NULL). Only d->B, F, T, M, dtype are read. fp64
+ * throughout; eigenvector phases are arbitrary (as in LAPACK). */
+int fm_spatial_init(const fm_dims* d, const void* X, void* Q, double* w, void* stream);
+
 const char* fm_last_error(void);
 int fm_version(void);
 

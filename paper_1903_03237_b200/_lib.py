@@ -83,6 +83,7 @@ SIGNATURES = [
      [ctypes.POINTER(FmDims), ctypes.POINTER(FmState), ctypes.c_int, ctypes.c_int, _vp]),
     ("fm_observation_stats", ctypes.c_int, [ctypes.POINTER(FmDims), _vp, _dp, _dp, _vp]),
     ("fm_scale_observation", ctypes.c_int, [ctypes.POINTER(FmDims), _vp, _dp, _vp]),
+    ("fm_spatial_init", ctypes.c_int, [ctypes.POINTER(FmDims), _vp, _vp, _vp, _vp]),
     ("fm_last_error", ctypes.c_char_p, []),
     ("fm_version", ctypes.c_int, []),
 ]

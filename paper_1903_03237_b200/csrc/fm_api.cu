@@ -252,4 +252,14 @@ int fm_scale_observation(const fm_dims* d, void* X, const double* scale_host, vo
   return FM_BY_DTYPE(d->dtype, scale(d, X, scale_host, (cudaStream_t)stream));
 }
 
+int fm_spatial_init(const fm_dims* d, const void* X, void* Q, double* w, void* stream) {
+  if (!d) { set_error("null dims"); return FM_EINVAL; }
+  if (d->dtype != FM_F32 && d->dtype != FM_F64) { set_error("dtype %d", d->dtype); return FM_EINVAL; }
+  if (d->B < 1 || d->F < 1 || d->T < 1) { set_error("empty problem"); return FM_EINVAL; }
+  if (d->F > 65535 || d->B > 65535) { set_error("F and B must be <= 65535"); return FM_EINVAL; }
+  if (int rc = check_m(d->M)) return rc;
+  if (!X || !Q) { set_error("null X or Q"); return FM_EINVAL; }
+  return FM_BY_DTYPE(d->dtype, spatial_init(d, X, Q, w, (cudaStream_t)stream));
+}
+
 }  // extern "C"

@@ -17,6 +17,7 @@
 #include "fm_ops.cuh"
 #include "fm_dp_latent.cuh"
 #include "fm_vacc_tc.cuh"
+#include "fm_init.cuh"
 
 namespace fm {
 
@@ -191,6 +192,7 @@ template <typename R> struct Impl {
   static int obs_stats(const fm_dims* d, const void* X, double* sumsq, double* maxsq,
                        cudaStream_t st);
   static int scale(const fm_dims* d, void* X, const double* scale_host, cudaStream_t st);
+  static int spatial_init(const fm_dims* d, const void* X, void* Q, double* w, cudaStream_t st);
 };
 
 template <typename Kern>
@@ -811,6 +813,21 @@ int Impl<R>::scale(const fm_dims* d, void* X, const double* scale_host, cudaStre
   k_scale<R><<<(unsigned)((n + 255) / 256), 256, 0, st>>>(reinterpret_cast<C*>(X), per_b, sc, (int)d->B);
   FM_CHECK_LAUNCH("k_scale");
   FM_CUDA(cudaStreamSynchronize(st));
+  return FM_OK;
+}
+
+template <typename R>
+int Impl<R>::spatial_init(const fm_dims* d, const void* X, void* Q, double* w, cudaStream_t st) {
+  InitArgs<R> a;
+  a.X = reinterpret_cast<const C*>(X);
+  a.Q = reinterpret_cast<C*>(Q);
+  a.w = w;
+  a.F = (int)d->F;
+  a.T = (int)d->T;
+  FM_DISPATCH_M(d->M, {
+    k_spatial_init<R, MM><<<dim3((unsigned)d->F, (unsigned)d->B), 256, 0, st>>>(a);
+    FM_CHECK_LAUNCH("k_spatial_init");
+  });
   return FM_OK;
 }
 

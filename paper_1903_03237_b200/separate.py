@@ -274,32 +274,30 @@ def default_init(cfg, Xs, rng, n_nmf=None):
     """Reference default init: circular spatial init (spatial.py:109-121) and
     NmfSource.random (sources.py:177-182) drawn from the run's rng.
 
-    The spatial part (time-averaged SCM, PSD clamp and descending Hermitian
-    eigendecomposition, linalg.py:23-33, 85-94) runs on the device through
-    torch.linalg.eigh (cuSOLVER); see DESIGN.md §8(f) for the planned native
-    batched-Jacobi kernel.
+    The spatial part -- time-averaged SCM, clamp_psd and the descending
+    Hermitian eigendecomposition (spatial.py:93-105, linalg.py:23-33, 85-94)
+    -- is one native kernel (fm_spatial_init: fp64 SCM + warp-level cyclic
+    complex Jacobi per bin).
     """
     torch = _torch()
     F, T, M = Xs.shape
     N = cfg.n_sources
-    Xd = Xs.to(torch.complex128)
     init = cfg.spatial_init
     if init == "auto":
         init = "observed" if cfg.method in DP_METHODS else "circular"
-    G1 = torch.einsum("fti,ftj->fij", Xd, Xd.conj()) / T  # spatial.py:93
-    G1 = 0.5 * (G1 + G1.conj().transpose(-1, -2))  # clamp_psd (linalg.py:85-94)
-    w, v = torch.linalg.eigh(G1)
-    w = torch.maximum(w, 1e-12 * torch.clamp(w.max(dim=-1, keepdim=True).values, min=0.0))
-    G1 = (v * w[..., None, :].to(v.dtype)) @ v.conj().transpose(-1, -2)
-    w, U = torch.linalg.eigh(G1)  # hermitian_eig: descending (linalg.py:23-33)
-    w, U = w.flip(-1), U.flip(-1)
-    Q = U.conj_physical().transpose(-1, -2).contiguous()
+    X1 = Xs.contiguous()
+    dims = _lib.FmDims(1, F, T, M, 1, 1, 0,
+                       _lib.FM_F32 if X1.dtype == torch.complex64 else _lib.FM_F64, 1, 1, 0)
+    Q = torch.empty((F, M, M), device=X1.device, dtype=X1.dtype)
+    w = torch.empty((F, M), device=X1.device, dtype=torch.float64)
+    _lib.check(_lib.load().fm_spatial_init(ctypes.byref(dims), _lib.ptr(X1), _lib.ptr(Q), _lib.ptr(w),
+                                           _lib.stream_ptr()), "fm_spatial_init")
     if init == "circular":  # spatial.py:109-121
-        g = torch.full((N, F, M), 1e-2, dtype=torch.float64, device=Xd.device)
+        g = torch.full((N, F, M), 1e-2, dtype=torch.float64, device=X1.device)
         for m in range(M):
             g[m % N, :, m] = 1.0
     else:  # "observed": init_spatial diagonalizable (spatial.py:100-105)
-        g = torch.ones((N, F, M), dtype=torch.float64, device=Xd.device)
+        g = torch.ones((N, F, M), dtype=torch.float64, device=X1.device)
         g[0] = torch.maximum(w, w.max(dim=-1, keepdim=True).values * 1e-12)
     Nn = N if n_nmf is None else n_nmf  # DP: the noise NMF holds n_sources - 1
     Wn = rng.uniform(0.1, 1.1, (Nn, F, cfg.n_basis))  # sources.py:180-181

@@ -153,3 +153,45 @@ def test_all_channel_counts_c64(M):
     if T >= M:
         Qn = K.update_diagonalizer(_t(Q, torch.complex64), Xt, _t(y, torch.float32)).cpu().numpy()
         assert rel(Qn, O.update_diagonalizer(Q.astype(np.complex64), X, y.astype(np.float32))) < 1e-4
+
+
+@pytest.mark.parametrize("M,T", [(1, 20), (3, 40), (8, 64), (16, 200), (6, 4)])
+@pytest.mark.parametrize("precision", ["complex128", "complex64"])
+def test_spatial_init_vs_numpy(M, T, precision):
+    """fm_spatial_init (SCM + Jacobi, descending, clamp_psd) against numpy's
+    eigh: eigenvalues, |Q| (eigenvector phases are arbitrary), unitarity and
+    Q G1 Q^H diagonal. T < M gives a rank-deficient SCM (clamped eigenvalues)."""
+    import ctypes
+
+    import torch
+
+    from paper_1903_03237_b200 import _lib
+    F = 5
+    rng = np.random.default_rng(M * 100 + T)
+    X = (rng.standard_normal((F, T, M)) + 1j * rng.standard_normal((F, T, M))) / np.sqrt(2)
+    X *= rng.uniform(0.5, 2.0, (1, 1, M))
+    cdt = torch.complex64 if precision == "complex64" else torch.complex128
+    Xd = torch.from_numpy(X).to("cuda", cdt).contiguous()
+    Xh = Xd.cpu().numpy().astype(np.complex128)
+    Q = torch.empty((F, M, M), device="cuda", dtype=cdt)
+    w = torch.empty((F, M), device="cuda", dtype=torch.float64)
+    dims = _lib.FmDims(1, F, T, M, 1, 1, 0, _lib.FM_F32 if precision == "complex64" else _lib.FM_F64,
+                       1, 1, 0)
+    _lib.check(_lib.load().fm_spatial_init(ctypes.byref(dims), _lib.ptr(Xd), _lib.ptr(Q), _lib.ptr(w),
+                                           _lib.stream_ptr()), "fm_spatial_init")
+    torch.cuda.synchronize()
+    Qg, wg = Q.cpu().numpy().astype(np.complex128), w.cpu().numpy()
+    G1 = np.einsum("fti,ftj->fij", Xh, Xh.conj()) / T
+    ww, U = np.linalg.eigh(G1)
+    ww = np.maximum(ww, 1e-12 * np.maximum(ww.max(axis=-1, keepdims=True), 0.0))[..., ::-1]
+    U = U[..., ::-1]
+    scale = np.abs(ww).max()
+    assert np.abs(wg - ww).max() <= 1e-12 * scale
+    tol = 1e-10 if precision == "complex128" else 1e-5
+    eye = np.eye(M)
+    assert np.abs(Qg @ np.conj(Qg.swapaxes(-1, -2)) - eye).max() <= tol
+    D = Qg @ G1 @ np.conj(Qg.swapaxes(-1, -2))
+    off = D - np.einsum("fii->fi", D)[..., None] * eye
+    assert np.abs(off).max() <= tol * 10 * scale
+    if T >= M:  # distinct eigenvalues: eigenvectors unique up to phase
+        assert np.abs(np.abs(Qg) - np.abs(np.conj(U.swapaxes(-1, -2)))).max() <= tol * 100
