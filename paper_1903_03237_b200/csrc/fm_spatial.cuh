@@ -163,6 +163,9 @@ template <typename R, int M> struct VaCfg {
   static constexpr int ROWB = M * 3 * (int)sizeof(R);
   static constexpr int TB = (256 * ROWB <= 36864) ? 256 : (128 * ROWB <= 36864) ? 128 : 64;
   static constexpr int STAGEB = TB * M * (int)(sizeof(R) + 2 * sizeof(R));
+  // fp32, M = 6..8: cap registers for 3 CTAs (24 warps) per SM -- the pair loop is
+  // shared-load latency bound, not issue bound
+  static constexpr int MINB = (sizeof(R) == 4 && M >= 6 && M <= 8) ? 3 : 1;
   static constexpr bool ONEPASS = S2 * M * P * (int)(2 * sizeof(R)) <= STAGEB;
 };
 
@@ -181,7 +184,7 @@ template <typename R> struct VaccArgs {
 // g MU (separate.py:218-220) + V_fm = (1/T) sum_t x x^H / y_ftm with y from
 // the updated gains (separate.py:221-222; spatial.py:182; _kernels.py:276-293)
 template <typename R, int M>
-__global__ void __launch_bounds__(VaCfg<R, M>::BS) k_vacc(VaccArgs<R> a) {
+__global__ void __launch_bounds__(VaCfg<R, M>::BS, VaCfg<R, M>::MINB) k_vacc(VaccArgs<R> a) {
   pdl_entry();
   using C = cplx<R>;
   using Cf = VaCfg<R, M>;
