@@ -357,7 +357,11 @@ def main():
     e2e = None
     if not args.no_e2e and not sharded_f and args.config in ("c1", "c0"):
         Xh = X[0].cpu().pin_memory()
-        run(scfg, Xh, init=tuple(a[0].numpy() for a in init))  # warm
+        # warm: two results alive at once, as in the timed loop below (the pinned
+        # image blocks come from torch's caching host allocator)
+        w1 = run(scfg, Xh, init=tuple(a[0].numpy() for a in init))
+        w2 = run(scfg, Xh, init=tuple(a[0].numpy() for a in init))
+        del w1, w2
         torch.cuda.synchronize()
         reps = 3
         prof = None

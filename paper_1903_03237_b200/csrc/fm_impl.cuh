@@ -17,6 +17,7 @@
 #include "fm_ops.cuh"
 #include "fm_dp_latent.cuh"
 #include "fm_vacc_tc.cuh"
+#include "fm_vacc_blk.cuh"
 #include "fm_init.cuh"
 
 namespace fm {
@@ -97,10 +98,23 @@ inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
 struct Plan {
   int FT, TT;    // k_wstats bins per CTA, k_hstats frames per CTA
   int HS, HFR;   // k_hstats bin splits and bins per split
-  int TR, nseg;  // k_gain / k_vacc frames per CTA segment and segments per bin
+  int TR, nseg;  // k_gain (and k_vacc/k_vacc_tc) frames per CTA segment, segments per bin
+  int VTR, vnseg;  // V accumulation segments (k_ip reduces vnseg partials per bin)
   size_t off_lam, off_phi, off_gpart, off_vpart, off_gnew, off_llp, off_ldp, off_cs, off_hpart;
   size_t off_cnt, off_hcnt, total;
 };
+
+// complex64 V accumulation: 0 register-blocked SIMT (k_vacc_blk, M >= 8),
+// 1 pair-per-thread SIMT (k_vacc), 2 tensor cores (k_vacc_tc, M >= 12).
+// FM_VACC=blk|simt|tc forces one for A/B runs; read at every launch (or graph
+// capture) so tests can switch it within one process.
+inline int vacc_mode(const fm_dims* d) {
+  const char* e = getenv("FM_VACC");
+  if (e && strcmp(e, "simt") == 0) return 1;
+  if (e && strcmp(e, "tc") == 0) return d->M >= 12 ? 2 : 1;
+  if (e && strcmp(e, "blk") == 0) return 0;
+  return d->M >= 8 ? 0 : 1;  // measured: M = 4 (c2) is faster pair-per-thread
+}
 
 inline Plan make_plan(const fm_dims* d) {
   Plan p;
@@ -128,7 +142,20 @@ inline Plan make_plan(const fm_dims* d) {
   if (p.TR < 256) p.TR = 256;
   p.nseg = (int)((T + p.TR - 1) / p.TR);
   const size_t gpart = (size_t)B * F * p.nseg * N * 2 * M;
-  const size_t vpart = (size_t)B * F * p.nseg * M * (M * (M + 1) / 2) * 2;
+  p.VTR = p.TR;
+  p.vnseg = p.nseg;
+  if (d->dtype == FM_F32 && vacc_mode(d) == 0) {
+    // k_vacc_blk: long frame runs per thread amortise the slice tree; enough
+    // (bin, segment) CTAs for ~3/4 of the resident slots (VbCfg: 128-thread
+    // CTAs, 4 per SM, for M <= 8; one 512-thread CTA per SM above)
+    const long long tbv = M > 8 ? 256 : 128, slots = (M > 8 ? 1 : 4) * 148 * 3 / 4;
+    const long long vs = std::max<long long>(1, (slots + F * B - 1) / (F * B));
+    long long vtr = (T + vs - 1) / vs;
+    vtr = std::max<long long>(tbv, (vtr + tbv - 1) / tbv * tbv);
+    p.VTR = (int)vtr;
+    p.vnseg = (int)((T + vtr - 1) / vtr);
+  }
+  const size_t vpart = (size_t)B * F * p.vnseg * M * (M * (M + 1) / 2) * 2;
   size_t o = 0;
   p.off_lam = o; o = align256(o + (size_t)B * N * F * T * rs);
   p.off_phi = o; o = align256(o + (size_t)B * 2 * N * F * T * rs);
@@ -197,7 +224,7 @@ template <typename R> struct Impl {
 
 template <typename Kern>
 inline int ensure_smem(Kern k, size_t bytes) {
-  if (bytes > 48 * 1024) {
+  if (bytes + 4096 > 48 * 1024) {  // dynamic + static smem above the default 48 KB
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
     if (e != cudaSuccess) {
       set_error("cudaFuncSetAttribute(%zu B smem): %s", bytes, cudaGetErrorString(e));
@@ -249,24 +276,30 @@ int Impl<R>::vacc(const fm_dims* d, const fm_state* s, cudaStream_t st) {
   a.floorp = reinterpret_cast<const R*>(s->floor);
   a.gnew = reinterpret_cast<R*>(w + p.off_gnew);
   a.part = reinterpret_cast<R*>(w + p.off_vpart);
-  a.F = (int)d->F; a.T = (int)d->T; a.N = (int)d->N; a.TR = p.TR;
+  a.F = (int)d->F; a.T = (int)d->T; a.N = (int)d->N; a.TR = p.TR; a.gseg = p.nseg;
   static const int dbg = [] { const char* e = getenv("FM_VTC_DBG"); return e ? atoi(e) : 0; }();
   a.dbg = dbg;
   dim3 grid((unsigned)p.nseg, (unsigned)d->F, (unsigned)d->B);
-  static const bool simt = [] {  // FM_VACC=simt: the SIMT accumulation (A/B comparisons)
-    const char* e = getenv("FM_VACC");
-    return e && strcmp(e, "simt") == 0;
-  }();
+  const int mode = vacc_mode(d);
   FM_DISPATCH_M(d->M, {
-    if constexpr (sizeof(R) == 4 && MM >= 12) {
-      // complex64, M >= 12: tensor-core accumulation (fm_vacc_tc.cuh). Measured
-      // on B200: M = 16 (c3) 2.58 ms vs 4.68 ms SIMT; M = 8 (c1) 82 us vs 41 us
-      // SIMT (N = M = 8 MMAs are dominated by per-instruction cost)
-      if (!simt) {
-        const size_t smv = VtcCfg<MM>::SMEM;
-        if (int rc = ensure_smem(k_vacc_tc<MM>, smv)) return rc;
-        launch_pdl(k_vacc_tc<MM>, grid, dim3(VtcCfg<MM>::BS), smv, st, a);
-        FM_CHECK_LAUNCH("k_vacc_tc");
+    if constexpr (sizeof(R) == 4) {
+      if constexpr (MM >= 12) {
+        if (mode == 2) {
+          const size_t smv = VtcCfg<MM>::SMEM;
+          if (int rc = ensure_smem(k_vacc_tc<MM>, smv)) return rc;
+          launch_pdl(k_vacc_tc<MM>, grid, dim3(VtcCfg<MM>::BS), smv, st, a);
+          FM_CHECK_LAUNCH("k_vacc_tc");
+          return FM_OK;
+        }
+      }
+      if (mode == 0) {
+        const size_t smb = VbCfg<MM>::SMEM;
+        if (int rc = ensure_smem(k_vacc_blk<MM>, smb)) return rc;
+        VaccArgs<float> ab = *reinterpret_cast<VaccArgs<float>*>(&a);
+        ab.TR = p.VTR;
+        launch_pdl(k_vacc_blk<MM>, dim3((unsigned)p.vnseg, (unsigned)d->F, (unsigned)d->B),
+                   dim3(VbCfg<MM>::BS), smb, st, ab);
+        FM_CHECK_LAUNCH("k_vacc_blk");
         return FM_OK;
       }
     }
@@ -282,7 +315,7 @@ int Impl<R>::ip(const fm_dims* d, const fm_state* s, cudaStream_t st, R* u) {
   unsigned char* w = reinterpret_cast<unsigned char*>(s->work);
   IpArgs<R> a;
   a.Vpart = reinterpret_cast<const C*>(w + p.off_vpart);
-  a.nseg = p.nseg;
+  a.nseg = p.vnseg;
   a.T = (int)d->T;
   a.gnew = reinterpret_cast<const R*>(w + p.off_gnew);
   a.Q = reinterpret_cast<C*>(s->Q);

@@ -178,6 +178,7 @@ template <typename R> struct VaccArgs {
   R* gnew;         // (B, N, F, M) gains after the MU (written by segment 0)
   R* part;         // (B, F, nseg, M, P) complex partial V sums
   int F, T, N, TR;
+  int gseg;        // k_gain segments per bin (k_vacc_blk's own segmentation may differ)
   int dbg;         // timing experiments only (k_vacc_tc): 1 skip MMAs, 2 skip operand builds
 };
 

@@ -353,24 +353,17 @@ def _prepare_observation(X, cfg, torch):
     return Xd, scale, floor.to(cfg.device)
 
 
-_STAGING = {}
-
-
 def _to_host(t):
-    """Device tensor -> fresh host tensor: async copy into a cached pinned
-    staging buffer, then a multi-threaded host copy into pageable memory
-    (a plain .cpu() of a large tensor runs at pageable-DMA speed)."""
+    """Device tensor -> host tensor in page-locked memory from torch's caching
+    host allocator: one async DMA at full PCIe/C2C speed and no host-side copy
+    (a plain .cpu() of a large tensor runs at pageable-DMA speed, and a copy
+    into fresh pageable memory pays first-touch page faults). The returned
+    tensor (and any numpy view of it) owns the pinned block; when it is freed
+    the block goes back to the allocator's cache for the next call."""
     torch = _torch()
-    n = t.numel() * t.element_size()
-    buf = _STAGING.get("buf")
-    if buf is None or buf.numel() < n:
-        buf = torch.empty((max(n, 1),), dtype=torch.uint8, pin_memory=True)
-        _STAGING["buf"] = buf
-    st = buf[:n].view(t.dtype).view(t.shape)
-    st.copy_(t.contiguous(), non_blocking=True)
+    out = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+    out.copy_(t.contiguous(), non_blocking=True)
     torch.cuda.current_stream().synchronize()
-    out = torch.empty(t.shape, dtype=t.dtype)
-    out.copy_(st)
     return out
 
 
@@ -450,7 +443,7 @@ def run(cfg: SeparatorConfig, X_FTM, on_iteration=None, init=None) -> Separation
         time_trace.append(prev.elapsed_time(e) / 1e3)
         prev = e
     ll = loop.trace[:, 0].cpu().numpy().copy() if cfg.record_likelihood else np.zeros(0)
-    # images at the run's precision (complex64 runs return complex64), through pinned staging
+    # images at the run's precision (complex64 runs return complex64), in pinned host memory
     images = _to_host(loop.images(scale)[0]).numpy()
     res = SeparationResult(images_NFTM=images, likelihood_trace=np.asarray(ll),
                            time_trace=np.asarray(time_trace), method=cfg.method,
