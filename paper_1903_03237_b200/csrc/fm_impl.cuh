@@ -113,7 +113,10 @@ inline int vacc_mode(const fm_dims* d) {
   if (e && strcmp(e, "simt") == 0) return 1;
   if (e && strcmp(e, "tc") == 0) return d->M >= 12 ? 2 : 1;
   if (e && strcmp(e, "blk") == 0) return 0;
-  return d->M >= 8 ? 0 : 1;  // measured: M = 4 (c2) is faster pair-per-thread
+  // measured on B200: pair-per-thread wins at M = 4 (c2: 1.13 vs 1.89 ms) and
+  // M = 8 (c1: 39.1 vs 40.8 us); the blocked kernel at M = 16 (c3: 2.00 ms vs
+  // 2.57 ms tensor cores, 4.67 ms pair-per-thread)
+  return d->M > 8 ? 0 : 1;
 }
 
 inline Plan make_plan(const fm_dims* d) {
@@ -148,7 +151,7 @@ inline Plan make_plan(const fm_dims* d) {
     // k_vacc_blk: long frame runs per thread amortise the slice tree; enough
     // (bin, segment) CTAs for ~3/4 of the resident slots (VbCfg: 128-thread
     // CTAs, 4 per SM, for M <= 8; one 512-thread CTA per SM above)
-    const long long tbv = M > 8 ? 256 : 128, slots = (M > 8 ? 1 : 4) * 148 * 3 / 4;
+    const long long tbv = vb_chunk((int)M), slots = (M > 8 ? 1 : 4) * 148 * 3 / 4;
     const long long vs = std::max<long long>(1, (slots + F * B - 1) / (F * B));
     long long vtr = (T + vs - 1) / vs;
     vtr = std::max<long long>(tbv, (vtr + tbv - 1) / tbv * tbv);
