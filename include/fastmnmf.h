@@ -143,7 +143,26 @@ typedef struct fm_dp {
   void* work;     /* fm_dp_workspace_bytes() */
   int32_t adam_steps;
   float lr, beta1, beta2, eps;
+  /* ---- the reference's own latent update and decoder ----
+   * decoder_kind FM_DEC_TOY: ToyDecoder (sources.py:52-80), r = max(softplus(
+   * W3 tanh(W1 z + b1) + b3), 1e-8) with hidden width Hd; W2/b2 unused.
+   * mh_steps > 0 replaces the Adam steps by the Metropolis random walk of
+   * update_latents_fast (sources.py:307-339): per step z' = z + mh_std *
+   * noise, accept per frame iff log(unif) <= log gamma_t
+   * (metropolis_log_gamma_fast, sources.py:292-304). noise (mh_steps,B,T,D)
+   * and unif (mh_steps,B,T) are caller-filled each iteration (the
+   * reference's numpy stream), or both NULL: counter-based Philox-4x32-10
+   * draws keyed by mh_seed and the device iteration counter. */
+  int32_t decoder_kind;  /* FM_DEC_EXP_MLP (0) | FM_DEC_TOY (1) */
+  int32_t mh_steps;
+  double mh_std;         /* sqrt(MetropolisConfig.proposal_var) */
+  const void* mh_noise;
+  const void* mh_unif;
+  uint64_t mh_seed;
 } fm_dp;
+
+#define FM_DEC_EXP_MLP 0
+#define FM_DEC_TOY 1
 
 size_t fm_dp_workspace_bytes(const fm_dims* d, const fm_dp* p);
 /* decoder forward r = exp(dec(z)), lambda, projection and the first

@@ -19,6 +19,10 @@ BASELINE config 4 replaces two parts of the reference's FastMNMF-DP
   y_rest, TINY) -- the objective the reference's Metropolis ratio evaluates
   (``metropolis_log_gamma_fast``, ``sources.py:292-304``).
 
+The reference's own default (ToyDecoder + Metropolis chain)
+is restated too (``ToyDecoder``, ``MetropolisLatents``) and pinned to
+``tests/golden/run_dp_mh.npz``, a run of the unmodified reference chain.
+
 Choices BASELINE.json leaves open (documented in DESIGN.md): Adam beta1=0.9,
 beta2=0.999, eps=1e-8, bias-corrected, lr=1e-2, state persisting across outer
 iterations. Everything around the hook is the reference's own loop; the
@@ -117,6 +121,62 @@ class AdamLatents:
         return 0
 
 
+class ToyDecoder:
+    """The reference's default decoder restated (sources.py:52-80): seeded
+    draws w1 ~ N(0, 1/D) (H, D), b1 ~ N(0, 0.25) (H), w2 ~ N(0, 1/H) (F, H),
+    b2 ~ N(0, 0.25) (F); r = max(softplus(tanh(z w1^T + b1) w2^T + b2), 1e-8)
+    with softplus(x) = log1p(exp(-|x|)) + max(x, 0) (sources.py:31-35)."""
+
+    def __init__(self, n_freq, latent_dim=16, hidden=64, seed=0):
+        rng = np.random.default_rng(seed)
+        self.w1 = rng.normal(0.0, 1.0 / np.sqrt(latent_dim), (hidden, latent_dim))
+        self.b1 = rng.normal(0.0, 0.5, hidden)
+        self.w2 = rng.normal(0.0, 1.0 / np.sqrt(hidden), (n_freq, hidden))
+        self.b2 = rng.normal(0.0, 0.5, n_freq)
+
+    @property
+    def latent_dim(self):
+        return self.w1.shape[1]
+
+    @property
+    def n_freq(self):
+        return self.w2.shape[0]
+
+    def __call__(self, z):
+        h = np.tanh(np.asarray(z, dtype=np.float64) @ self.w1.T + self.b1)
+        o = h @ self.w2.T + self.b2
+        return np.maximum(np.log1p(np.exp(-np.abs(o))) + np.maximum(o, 0.0), 1e-8)
+
+
+class MetropolisLatents:
+    """The reference's latent hook restated: update_latents_fast / _run_chain
+    (sources.py:307-339) with metropolis_log_gamma_fast (:292-304). Per inner
+    step: z' = z + sqrt(var) * rng.standard_normal((T, D)); r' = dec(z');
+    log gamma_t = -sum_fm x~ (1/y' - 1/y) - sum_fm log(y'/y),
+    y = max(lambda g_0 + y_rest, TINY); accept iff
+    log(rng.uniform(size=T)) <= log gamma_t."""
+
+    def __init__(self, rng, inner_steps=30, proposal_var=1e-4):
+        self.rng, self.steps, self.std = rng, inner_steps, np.sqrt(proposal_var)
+
+    def __call__(self, dp, decoder, g_FM, y_rest_FTM, xt_FTM, cfg=None, rng=None):
+        T = dp.z_TD.shape[0]
+        lam_old = dp.lam_FT()
+        for _ in range(self.steps):
+            z_new = dp.z_TD + self.std * self.rng.standard_normal(dp.z_TD.shape)
+            r_new = decoder(z_new)
+            lam_new = dp.u_F[:, None] * (dp.v_T[:, None] * r_new).T
+            y_new = np.maximum(lam_new[..., None] * g_FM[:, None, :] + y_rest_FTM, TINY)
+            y_old = np.maximum(lam_old[..., None] * g_FM[:, None, :] + y_rest_FTM, TINY)
+            lg = (-(xt_FTM * (1.0 / y_new - 1.0 / y_old)).sum(axis=(0, 2))
+                  - np.log(y_new / y_old).sum(axis=(0, 2)))
+            acc = np.log(self.rng.uniform(size=T)) <= lg
+            dp.z_TD[acc] = z_new[acc]
+            dp.r_TF[acc] = r_new[acc]
+            lam_old[:, acc] = lam_new[:, acc]
+        return 0
+
+
 class DPState:
     """u, v, z, r of the deep-prior source (sources.py:207-220)."""
 
@@ -134,8 +194,10 @@ class DPState:
 
 
 def run_fastmnmf_dp(X_FTM, Q0, g0, u0, v0, z0, W0, H0, decoder, n_iterations, adam_steps=10,
-                    lr=1e-2, normalize=True, ip_sweeps=1, want_images=True):
-    """FastMNMF-DP with the config-4 latent update; structure of separate.py:201-330."""
+                    lr=1e-2, normalize=True, ip_sweeps=1, want_images=True, hook=None):
+    """FastMNMF-DP; structure of separate.py:201-330. The latent hook is the
+    config-4 Adam update (``adam_steps`` > 0), or ``hook`` (e.g.
+    MetropolisLatents, the reference's own chain)."""
     X = np.ascontiguousarray(X_FTM, dtype=np.complex128)
     power = float(np.mean(np.abs(X) ** 2))
     scale = np.sqrt(power)
@@ -146,7 +208,8 @@ def run_fastmnmf_dp(X_FTM, Q0, g0, u0, v0, z0, W0, H0, decoder, n_iterations, ad
     W = np.array(W0, dtype=np.float64)
     H = np.array(H0, dtype=np.float64)
     dp = DPState(u0, v0, z0, decoder)
-    hook = AdamLatents(adam_steps, lr)
+    if hook is None and adam_steps > 0:
+        hook = AdamLatents(adam_steps, lr)
     xt = project_power(Q, Xs)
 
     def lam():
@@ -158,7 +221,7 @@ def run_fastmnmf_dp(X_FTM, Q0, g0, u0, v0, z0, W0, H0, decoder, n_iterations, ad
         # latent hook (separate.py:205-213): y_rest without floor, LL captured first
         y_rest = mix_power(lam_all[1:], g[1:])
         ll_before = fast_stats(xt, g, lam_all, floor)[4]
-        if adam_steps > 0:
+        if hook is not None:
             hook(dp, decoder, g[0], y_rest, xt)
         for step in ("U", "V", "W", "H"):  # sources.py:226, 251-267
             p1, p2, _, _, _ = fast_stats(xt, g, lam(), floor)

@@ -180,11 +180,51 @@ def save_dp(name, F, T, M, K, n_iter, adam_steps, seed=5):
     print(f"{name}: LL {res.likelihood_trace[0]:.6f} -> {res.likelihood_trace[-1]:.6f}", flush=True)
 
 
+def save_dp_mh(name, F, T, M, K, n_iter, seed=5):
+    """fastsep.run(method="fast-mnmf-dp") on the reference's own default
+    latent path: its ToyDecoder(F) and its Metropolis chain
+    (update_latents_fast, sources.py:307-339, NOT patched), with the init
+    injected by the SURVEY §8(c) recipe (so the chain's draws come from a
+    fresh default_rng(cfg.seed))."""
+    from oracle.fastmnmf_dp_oracle import dp_init, make_dp_mixture
+
+    dec = SRC.ToyDecoder(F)
+    X = make_dp_mixture(F, T, M, K, dec, seed=seed).astype(np.complex64).astype(np.complex128)
+    Q0, g0, u0, v0, z0, W0, H0 = dp_init(F, T, M, K, dec.latent_dim, seed)
+    orig = (S._build_spatial, S._build_source)
+    S._build_spatial = lambda cfg, Xs: SP.DiagSpatial(Q0.copy(), g0.copy())
+    S._build_source = lambda cfg, Xs, rng: SRC.DeepPriorPlusNmfSource(
+        SRC.DeepPriorFactors(u0.copy(), v0.copy(), z0.copy()), SRC.NmfSource(W0.copy(), H0.copy()),
+        dec)
+    st = {}
+
+    def snap(it, loop):
+        src = loop.source
+        st.update(u=src.dp.u_F.copy(), v=src.dp.v_T.copy(), z=src.dp.z_TD.copy(),
+                  W=src.noise.W_NFK.copy(), H=src.noise.H_NKT.copy(),
+                  g=loop.spatial.g_NFM.copy(), Q=loop.spatial.Q_FMM.copy())
+
+    try:
+        cfg = fastsep.SeparatorConfig(method="fast-mnmf-dp", n_sources=2, n_basis=K,
+                                      n_iterations=n_iter, seed=seed)
+        res = fastsep.run(cfg, X, on_iteration=snap)
+    finally:
+        S._build_spatial, S._build_source = orig
+    np.savez_compressed(os.path.join(OUT, name), shape=np.array([F, T, M, K, seed, n_iter]),
+                        X=X.astype(np.complex64), trace=res.likelihood_trace,
+                        images=res.images_NFTM, **st)
+    print(f"{name}: LL {res.likelihood_trace[0]:.6f} -> {res.likelihood_trace[-1]:.6f}", flush=True)
+
+
 def main():
     os.makedirs(OUT, exist_ok=True)
+    if "--dp-mh-only" in sys.argv:
+        save_dp_mh("run_dp_mh.npz", 33, 64, 4, 8, 6)
+        return
     if "--dp-only" in sys.argv:
         save_dp("run_dp_mu.npz", 33, 64, 4, 8, 8, 0)
         save_dp("run_dp_adam.npz", 33, 64, 4, 8, 8, 10)
+        save_dp_mh("run_dp_mh.npz", 33, 64, 4, 8, 6)
         return
     np.savez_compressed(os.path.join(OUT, "kernels.npz"), **kernel_cases())
     print("kernels.npz written", flush=True)
@@ -205,6 +245,7 @@ def main():
     # config 1 shape, complex64-rounded X, 100 iterations
     save_dp("run_dp_mu.npz", 33, 64, 4, 8, 8, 0)
     save_dp("run_dp_adam.npz", 33, 64, 4, 8, 8, 10)
+    save_dp_mh("run_dp_mh.npz", 33, 64, 4, 8, 6)
     if "--with-c1" in sys.argv:
         X1 = make_mixture(513, 1024, 8, 4, 16, seed=0)
         save_run("run_c1_c64.npz", X1, 513, 1024, 8, 4, 16, 0, 100, False, round64=True)

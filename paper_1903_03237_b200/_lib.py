@@ -45,6 +45,8 @@ class FmDp(ctypes.Structure):
         ("adam_step", _vp), ("work", _vp),
         ("adam_steps", ctypes.c_int32), ("lr", ctypes.c_float), ("beta1", ctypes.c_float),
         ("beta2", ctypes.c_float), ("eps", ctypes.c_float),
+        ("decoder_kind", ctypes.c_int32), ("mh_steps", ctypes.c_int32), ("mh_std", ctypes.c_double),
+        ("mh_noise", _vp), ("mh_unif", _vp), ("mh_seed", ctypes.c_uint64),
     ]
 
 

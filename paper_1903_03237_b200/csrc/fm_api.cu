@@ -162,7 +162,23 @@ static int validate_dp(const fm_dims* d, const fm_dp* p) {
               DEC_DMAX, DEC_HMAX);
     return FM_EINVAL;
   }
-  if (p->D % 4 || p->Hd % 4) {
+  if (p->decoder_kind != FM_DEC_EXP_MLP && p->decoder_kind != FM_DEC_TOY) {
+    set_error("unknown decoder_kind %d", (int)p->decoder_kind);
+    return FM_EINVAL;
+  }
+  if (p->decoder_kind == FM_DEC_TOY && p->adam_steps > 0 && p->mh_steps <= 0) {
+    set_error("the Adam latent update needs the exp-MLP decoder (decoder_kind 0)");
+    return FM_EINVAL;
+  }
+  if (p->mh_steps < 0 || (p->mh_steps > 0 && !(p->mh_std > 0.0))) {
+    set_error("Metropolis needs mh_steps >= 0 and a positive proposal std");
+    return FM_EINVAL;
+  }
+  if ((p->mh_noise == nullptr) != (p->mh_unif == nullptr)) {
+    set_error("mh_noise and mh_unif must both be set (caller draws) or both NULL (Philox)");
+    return FM_EINVAL;
+  }
+  if (p->decoder_kind == FM_DEC_EXP_MLP && (p->D % 4 || p->Hd % 4)) {
     set_error("decoder sizes D=%lld Hd=%lld must be multiples of 4", (long long)p->D, (long long)p->Hd);
     return FM_EINVAL;
   }

@@ -16,6 +16,7 @@
 #include "fm_kernels.cuh"
 #include "fm_ops.cuh"
 #include "fm_dp_latent.cuh"
+#include "fm_dp_mh.cuh"
 #include "fm_vacc_tc.cuh"
 #include "fm_vacc_blk.cuh"
 #include "fm_init.cuh"
@@ -199,6 +200,7 @@ template <typename R> struct Impl {
   static int lambda_nmf(const fm_dims* d, const fm_state* s, cudaStream_t st);
   static int phi_pass(const fm_dims* d, const fm_state* s, cudaStream_t st);
   static int dp_latent(const fm_dims* d, const fm_state* s, const fm_dp* p, int steps, cudaStream_t st);
+  static int dp_mh(const fm_dims* d, const fm_state* s, const fm_dp* p, int steps, cudaStream_t st);
   static int dp_lambda(const fm_dims* d, const fm_state* s, const fm_dp* p, cudaStream_t st);
   static int prologue_dp(const fm_dims* d, const fm_state* s, const fm_dp* p, cudaStream_t st);
   static int iterate_dp(const fm_dims* d, const fm_state* s, const fm_dp* p, cudaStream_t st);
@@ -536,6 +538,58 @@ int Impl<R>::dp_latent(const fm_dims* d, const fm_state* s, const fm_dp* p, int 
   return FM_OK;
 }
 
+// The reference's Metropolis latent chain (fm_dp_mh.cuh); steps = 0 is the
+// decoder refresh r = dec(z) (any decoder kind).
+template <typename R>
+int Impl<R>::dp_mh(const fm_dims* d, const fm_state* s, const fm_dp* p, int steps, cudaStream_t st) {
+  const Plan pl = make_plan(d);
+  unsigned char* w = reinterpret_cast<unsigned char*>(s->work);
+  MhArgs<R> a;
+  a.W1 = reinterpret_cast<const R*>(p->W1);
+  a.b1 = reinterpret_cast<const R*>(p->b1);
+  a.W2 = reinterpret_cast<const R*>(p->W2);
+  a.b2 = reinterpret_cast<const R*>(p->b2);
+  a.Wo = reinterpret_cast<const R*>(p->W3);
+  a.bo = reinterpret_cast<const R*>(p->b3);
+  a.u = reinterpret_cast<const R*>(p->u);
+  a.v = reinterpret_cast<const R*>(p->v);
+  a.z = reinterpret_cast<R*>(p->z);
+  a.r = reinterpret_cast<R*>(p->r);
+  a.lam = reinterpret_cast<const R*>(w + pl.off_lam);
+  a.g = reinterpret_cast<const R*>(s->g);
+  a.xt = reinterpret_cast<const R*>(s->xt);
+  a.noise = reinterpret_cast<const R*>(p->mh_noise);
+  a.unif = reinterpret_cast<const R*>(p->mh_unif);
+  a.iter = reinterpret_cast<const unsigned*>(w + pl.off_cnt) + 1;
+  a.seed = p->mh_seed;
+  a.stdv = p->mh_std;
+  a.steps = steps;
+  a.kind = p->decoder_kind;
+  a.D = (int)p->D; a.Hd = (int)p->Hd;
+  a.N = (int)d->N; a.F = (int)d->F; a.T = (int)d->T; a.M = (int)d->M; a.B = (int)d->B;
+  // frames per CTA: 4 (fp32) / 2 (fp64), fewer while the staged x~ / y_rest do
+  // not fit; without staging they are re-read from L2 every proposal
+  const size_t rs = sizeof(R), cap = 200 * 1024;
+  a.cache = 1;
+  a.fpb = sizeof(R) == 4 ? 4 : 2;
+  while (a.fpb > 1 && mh_smem_bytes(rs, a.fpb, a.D, a.Hd, a.F, a.M, true) > cap) --a.fpb;
+  if (mh_smem_bytes(rs, a.fpb, a.D, a.Hd, a.F, a.M, true) > cap) {
+    a.cache = 0;
+    a.fpb = sizeof(R) == 4 ? 4 : 2;
+  }
+  if (steps == 0) a.cache = 0;
+  const size_t sm = mh_smem_bytes(rs, a.fpb, a.D, a.Hd, a.F, a.M, a.cache != 0);
+  if (sm > LT_SMEM_MAX) {
+    set_error("Metropolis kernel needs %zu B shared memory (F=%d Hd=%d)", sm, a.F, a.Hd);
+    return FM_EINVAL;
+  }
+  if (int rc = ensure_smem(k_dp_mh<R>, sm)) return rc;
+  launch_pdl(k_dp_mh<R>, dim3((unsigned)((d->T + a.fpb - 1) / a.fpb), (unsigned)d->B), dim3(256), sm,
+             st, a);
+  FM_CHECK_LAUNCH("k_dp_mh");
+  return FM_OK;
+}
+
 template <typename R>
 int Impl<R>::dp_lambda(const fm_dims* d, const fm_state* s, const fm_dp* p, cudaStream_t st) {
   const Plan pl = make_plan(d);
@@ -575,7 +629,11 @@ int Impl<R>::prologue_dp(const fm_dims* d, const fm_state* s, const fm_dp* p, cu
   const Plan pl = make_plan(d);
   unsigned char* w = reinterpret_cast<unsigned char*>(s->work);
   FM_CUDA(cudaMemsetAsync(w + pl.off_cnt, 0, pl.total - pl.off_cnt, st));
-  if (int rc = dp_latent(d, s, p, 0, st)) return rc;
+  if (p->decoder_kind == FM_DEC_TOY) {
+    if (int rc = dp_mh(d, s, p, 0, st)) return rc;
+  } else {
+    if (int rc = dp_latent(d, s, p, 0, st)) return rc;
+  }
   if (int rc = dp_lambda(d, s, p, st)) return rc;
   if (int rc = lambda_nmf(d, s, st)) return rc;
   return back(d, s, /*tail_only=*/1, /*record=*/0, st);
@@ -598,7 +656,10 @@ int Impl<R>::iterate_dp(const fm_dims* d, const fm_state* s, const fm_dp* p, cud
   if (int rc = dp_lambda(d, s, p, st)) return rc;
   // latent hook (separate.py:205-213): Adam on z against the frozen y_rest,
   // then r = exp(dec(z)) -- one launch
-  if (p->adam_steps > 0) {
+  if (p->mh_steps > 0) {  // the reference's Metropolis chain (sources.py:307-339)
+    if (int rc = dp_mh(d, s, p, p->mh_steps, st)) return rc;
+    if (int rc = dp_lambda(d, s, p, st)) return rc;
+  } else if (p->adam_steps > 0) {  // BASELINE config 4: Adam
     if (int rc = dp_latent(d, s, p, p->adam_steps, st)) return rc;
     if (int rc = dp_lambda(d, s, p, st)) return rc;
   }

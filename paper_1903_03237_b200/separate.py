@@ -26,7 +26,8 @@ PRECISIONS = ("complex128", "complex64")
 
 @dataclass
 class MetropolisConfig:
-    """Kept for config compatibility (sources.py:38-49); unused by fast-mnmf."""
+    """Random-walk proposal settings of the latent chain (sources.py:38-49),
+    used by fast-mnmf-dp's Metropolis update (k_dp_mh)."""
 
     proposal_var: float = 1e-4
     inner_steps: int = 30
@@ -63,6 +64,12 @@ class SeparatorConfig:
     # the chain, by metropolis_enabled=False
     adam_steps: int = 10
     adam_lr: float = 1e-2
+    # FastMNMF-DP latent update: "auto" = the reference's Metropolis chain
+    # (sources.py:307-339) for its ToyDecoder, Adam for an ExpMLPDecoder
+    latent_update: str = "auto"  # auto | metropolis | adam
+    # Metropolis draws: "numpy" = the run's Generator in the reference's order
+    # (bit-for-bit the reference's chain), "device" = Philox on the GPU
+    metropolis_rng: str = "numpy"
 
     def validate(self):  # separate.py:59-71
         if self.method not in METHODS:
@@ -81,6 +88,10 @@ class SeparatorConfig:
             raise InvalidInputError(f"unknown precision {self.precision!r}")
         if self.ip_sweeps < 1:
             raise InvalidInputError("ip_sweeps must be >= 1")
+        if self.latent_update not in ("auto", "metropolis", "adam"):
+            raise InvalidInputError(f"unknown latent_update {self.latent_update!r}")
+        if self.metropolis_rng not in ("numpy", "device"):
+            raise InvalidInputError(f"unknown metropolis_rng {self.metropolis_rng!r}")
 
 
 @dataclass
@@ -164,7 +175,8 @@ class DeviceLoop:
         self.X = X
         self.real = torch.float32 if X.dtype == torch.complex64 else torch.float64
         self.B, self.F, self.T, self.M = X.shape
-        self.dp_args = dp  # (decoder, u, v, z, adam_steps, lr) for FastMNMF-DP
+        # FastMNMF-DP: (decoder, u, v, z, adam_steps, lr[, mh_steps, mh_var, mh_rng, mh_seed])
+        self.dp_args = dp
         self.N, self.K = W.shape[1] + (1 if dp is not None else 0), W.shape[3]
         dev = X.device
         self.Q = Q.to(dev, X.dtype).resolve_conj().contiguous()
@@ -195,8 +207,10 @@ class DeviceLoop:
         if dp is not None:
             from .dp import DeviceDP
 
-            decoder, u, v, z, steps, lr = dp
-            self.dp = DeviceDP(decoder, u, v, z, self.dims, self.real, dev, adam_steps=steps, lr=lr)
+            decoder, u, v, z, steps, lr, *mh = dp
+            mh_steps, mh_var, mh_rng, mh_seed = (list(mh) + [0, 1e-4, None, 0][len(mh):])[:4]
+            self.dp = DeviceDP(decoder, u, v, z, self.dims, self.real, dev, adam_steps=steps, lr=lr,
+                               mh_steps=mh_steps, mh_var=mh_var, mh_rng=mh_rng, mh_seed=mh_seed)
         self.spatial = _SpatialView(self, 0)
         self.source = _SourceView(self, 0)
 
@@ -230,7 +244,13 @@ class DeviceLoop:
         lib = _lib.load()
         if self.iterations_done + n > self.n_trace:
             raise InvalidInputError("trace buffer too small for the requested iterations")
-        if self.dp is not None:
+        if self.dp is not None and self.dp.noise is not None:
+            for _ in range(n):  # the reference's numpy draws, one iteration at a time
+                self.dp.fill_draws()
+                _lib.check(lib.fm_run_dp(ctypes.byref(self.dims), ctypes.byref(self.state),
+                                         ctypes.byref(self.dp.struct), 1, int(bool(use_graph)),
+                                         _lib.stream_ptr()), "fm_run_dp")
+        elif self.dp is not None:
             _lib.check(lib.fm_run_dp(ctypes.byref(self.dims), ctypes.byref(self.state),
                                      ctypes.byref(self.dp.struct), int(n), int(bool(use_graph)),
                                      _lib.stream_ptr()), "fm_run_dp")
@@ -394,23 +414,34 @@ def run(cfg: SeparatorConfig, X_FTM, on_iteration=None, init=None) -> Separation
     rng = np.random.default_rng(cfg.seed)  # separate.py:295
     dp = None
     if cfg.method == "fast-mnmf-dp":
-        from .dp import ExpMLPDecoder
+        from .dp import ToyDecoder, decoder_kind
 
         F, T = Xs.shape[1], Xs.shape[2]
-        decoder = cfg.decoder if cfg.decoder is not None else ExpMLPDecoder(F, seed=cfg.seed)
+        # the reference's default decoder (separate.py:265)
+        decoder = cfg.decoder if cfg.decoder is not None else ToyDecoder(F)
         if getattr(decoder, "n_freq", F) != F:  # separate.py:266-270
             raise InvalidInputError(f"decoder output length {decoder.n_freq} does not match F={F}")
-        if not all(hasattr(decoder, a) for a in ("W1", "W2", "W3", "b1", "b2", "b3")):
-            raise InvalidInputError("the B200 deep prior needs an ExpMLPDecoder-style decoder "
-                                    "(weights W1, b1, W2, b2, W3, b3)")
+        kind = decoder_kind(decoder)
+        if kind is None:
+            raise InvalidInputError("the B200 deep prior needs a ToyDecoder (w1, b1, w2, b2) or an "
+                                    "ExpMLPDecoder (W1, b1, W2, b2, W3, b3)")
+        update = cfg.latent_update
+        if update == "auto":  # the reference's chain for its decoder, Adam for config 4's
+            update = "metropolis" if kind == 1 else "adam"
+        if update == "adam" and kind != 0:
+            raise InvalidInputError("latent_update='adam' needs an ExpMLPDecoder")
         if init is None:
             Q0, g0, W0, H0 = default_init(cfg, Xs[0], rng, n_nmf=cfg.n_sources - 1)
             u0, v0 = np.ones(F), np.ones(T)  # DeepPriorPlusNmfSource.init (sources.py:240-244)
             z0 = np.zeros((T, decoder.latent_dim))
         else:
             Q0, g0, u0, v0, z0, W0, H0 = init
-        steps = cfg.adam_steps if cfg.metropolis_enabled else 0
-        dp = (decoder, u0, v0, z0, steps, cfg.adam_lr)
+        on = cfg.metropolis_enabled  # separate.py:205
+        adam = cfg.adam_steps if (on and update == "adam") else 0
+        mh = cfg.metropolis.inner_steps if (on and update == "metropolis") else 0
+        mh_rng = rng if cfg.metropolis_rng == "numpy" else None
+        dp = (decoder, u0, v0, z0, adam, cfg.adam_lr, mh, cfg.metropolis.proposal_var, mh_rng,
+              cfg.seed)
     elif init is None:
         Q0, g0, W0, H0 = default_init(cfg, Xs[0], rng)
     else:

@@ -4,6 +4,10 @@ declares (CPU only: no compute calls)."""
 import ctypes
 import os
 import re
+import shutil
+import subprocess
+
+import pytest
 
 from conftest import REPO
 from paper_1903_03237_b200 import _lib
@@ -28,7 +32,34 @@ def test_library_exports_header():
 def test_structs_match_header_layout():
     assert ctypes.sizeof(_lib.FmDims) == 7 * 8 + 4 * 4
     assert ctypes.sizeof(_lib.FmState) == 10 * 8
-    assert ctypes.sizeof(_lib.FmDp) == 2 * 8 + 14 * 8 + 5 * 4 + 4  # padded to 8
+    # 2 int64, 14 pointers, adam_steps + 4 floats, decoder_kind, mh_steps,
+    # mh_std (8-aligned), 2 pointers, mh_seed
+    assert ctypes.sizeof(_lib.FmDp) == 2 * 8 + 14 * 8 + 5 * 4 + 2 * 4 + 4 + 8 + 2 * 8 + 8
+
+
+@pytest.mark.skipif(shutil.which("gcc") is None, reason="needs gcc")
+def test_struct_offsets_match_c_compiler(tmp_path):
+    """Every ctypes field offset equals the C compiler's offsetof for the header."""
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "fastmnmf.h"',
+             "int main(void) {"]
+    structs = (("fm_dims", _lib.FmDims), ("fm_state", _lib.FmState), ("fm_dp", _lib.FmDp))
+    for cname, cls in structs:
+        lines.append(f'  printf("%zu\\n", sizeof({cname}));')
+        for fname, _ in cls._fields_:
+            lines.append(f'  printf("%zu\\n", offsetof({cname}, {fname}));')
+    lines.append("  return 0; }")
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines) + "\n")
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-I", os.path.join(REPO, "include"), str(src), "-o", str(exe)],
+                   check=True)
+    got = [int(x) for x in subprocess.run([str(exe)], capture_output=True, text=True,
+                                          check=True).stdout.split()]
+    want = []
+    for _, cls in structs:
+        want.append(ctypes.sizeof(cls))
+        want += [getattr(cls, f).offset for f, _ in cls._fields_]
+    assert got == want
 
 
 def test_version_and_validation_without_gpu():

@@ -42,3 +42,27 @@ def test_dp_oracle_pinned_to_reference(name, steps):
     if steps:
         assert rel(out["z"], G["z"]) < 1e-12
     assert rel(out["images"], G["images"]) < 1e-12
+
+
+def test_toy_decoder_matches_oracle_restatement():
+    from paper_1903_03237_b200 import ToyDecoder
+    a, b = ToyDecoder(29), DO.ToyDecoder(29)
+    z = np.random.default_rng(4).standard_normal((7, 16))
+    np.testing.assert_array_equal(a(z), b(z))
+
+
+def test_metropolis_oracle_pinned_to_reference():
+    """The restated Metropolis chain (MetropolisLatents, sources.py:307-339)
+    reproduces the unmodified reference's default FastMNMF-DP run (ToyDecoder,
+    30 proposals per iteration, the run's numpy stream)."""
+    G = golden("run_dp_mh.npz")
+    F, T, M, K, seed, it = (int(v) for v in G["shape"])
+    dec = DO.ToyDecoder(F)
+    X = G["X"].astype(np.complex128)
+    hook = DO.MetropolisLatents(np.random.default_rng(seed))
+    out = DO.run_fastmnmf_dp(X, *DO.dp_init(F, T, M, K, dec.latent_dim, seed), dec, it,
+                             adam_steps=0, hook=hook)
+    np.testing.assert_allclose(out["likelihood_trace"], G["trace"], rtol=1e-12)
+    for k in ("u", "v", "z", "W", "H", "g", "Q"):
+        assert rel(out[k], G[k]) < 1e-12, k
+    assert rel(out["images"], G["images"]) < 1e-12
