@@ -38,6 +38,10 @@ CONFIGS = {
     "c3": dict(F=1025, T=8192, M=16, N=6, K=32, B=1, iters=100, precision="complex64"),
     "c0": dict(F=257, T=128, M=4, N=2, K=8, B=1, iters=50, precision="complex128"),
     "c4": dict(F=513, T=512, M=8, N=2, K=32, B=1, iters=100, precision="complex64", dp=True),
+    # config-4 shape on the reference's own default latent path: ToyDecoder +
+    # Metropolis (30 proposals/iteration, device Philox draws)
+    "c4mh": dict(F=513, T=512, M=8, N=2, K=32, B=1, iters=100, precision="complex64", dp=True,
+                 mh=True),
 }
 METRIC = "FastMNMF TF-bin*ch updates/s (F*T*M*mixtures*iterations/s)"
 UNIT = "TF-bin*ch/s"
@@ -130,15 +134,30 @@ def run_reference(args, cfg, world, rank):
     from paper_1903_03237_b200.synth import baseline_init, make_mixture
 
     F, T, M, N, K = cfg["F"], cfg["T"], cfg["M"], cfg["N"], cfg["K"]
-    X = make_mixture(F, T, M, N, K, 0)
-    if cfg["precision"] == "complex64":
-        X = X.astype(np.complex64).astype(np.complex128)
-    init = baseline_init(F, T, M, N, K, 0)
+    if cfg.get("dp"):  # FastMNMF-DP: Adam (c4) or the reference's Metropolis chain (c4mh)
+        from oracle import fastmnmf_dp_oracle as DO
+
+        dec = DO.ToyDecoder(F) if cfg.get("mh") else DO.ExpMLPDecoder(F, seed=0)
+        X = DO.make_dp_mixture(F, T, M, K, dec, 0).astype(np.complex64).astype(np.complex128)
+        init = DO.dp_init(F, T, M, K, dec.latent_dim, 0)
+
+        def one():
+            hook = DO.MetropolisLatents(np.random.default_rng(0)) if cfg.get("mh") else None
+            DO.run_fastmnmf_dp(X, *init, dec, 1, adam_steps=0 if hook else 10, hook=hook,
+                               want_images=False)
+    else:
+        X = make_mixture(F, T, M, N, K, 0)
+        if cfg["precision"] == "complex64":
+            X = X.astype(np.complex64).astype(np.complex128)
+        init = baseline_init(F, T, M, N, K, 0)
+
+        def one():
+            run_fastmnmf(X, *init, n_iterations=1, want_images=False)
     for _ in range(args.warmup):
-        run_fastmnmf(X, *init, n_iterations=1, want_images=False)
+        one()
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        run_fastmnmf(X, *init, n_iterations=1, want_images=False)
+        one()
     dt = (time.perf_counter() - t0) / args.steps
     value = F * T * M / dt
     cores = os.cpu_count()
@@ -238,13 +257,16 @@ def main():
         from paper_1903_03237_b200.dp import ExpMLPDecoder
         from paper_1903_03237_b200.synth import dp_init, make_dp_mixture
 
-        dec = ExpMLPDecoder(F, seed=0)
+        from paper_1903_03237_b200.dp import ToyDecoder
+
+        dec = ToyDecoder(F) if cfg.get("mh") else ExpMLPDecoder(F, seed=0)
         X = torch.from_numpy(make_dp_mixture(F, T, M, K, dec, 0)).to(dev, torch.complex64)[None]
         Q0, g0, u0, v0, z0, W0, H0 = dp_init(F, T, M, K, dec.latent_dim, 0)
         init = tuple(torch.from_numpy(a)[None] for a in (Q0, g0, W0, H0))
         Xs, scale, floor = _prepare_observation(X, scfg, torch)
+        latent = (0, 1e-2, 30, 1e-4, None, 0) if cfg.get("mh") else (10, 1e-2)
         loop = DeviceLoop(Xs, init[0], init[1], init[2], init[3], floor, True, 1, n_trace=iters,
-                          dp=(dec, u0, v0, z0, 10, 1e-2))
+                          dp=(dec, u0, v0, z0) + latent)
         dp_init_dev = [t.clone() for t in (loop.dp.u, loop.dp.v, loop.dp.z)]
     else:
         Xs, scale, floor = _prepare_observation(X, scfg, torch)
@@ -392,8 +414,8 @@ def main():
         cpu = cpu_baseline_sample(cfg)
 
     launches = args.steps * (2 + (10 if cfg['B'] == 1 else 11) * iters)
-    if cfg.get("dp"):  # 8 launches per Adam step x 10 + 2 + 17 per iteration, 4 in the prologue
-        launches = args.steps * (4 + (10 * 8 + 2 + 17) * iters)
+    if cfg.get("dp"):  # 21 per iteration (one latent-hook launch: Adam or Metropolis), 4 in the prologue
+        launches = args.steps * (4 + 21 * iters)
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,

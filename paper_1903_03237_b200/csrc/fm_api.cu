@@ -193,7 +193,11 @@ static int validate_dp(const fm_dims* d, const fm_dp* p) {
 
 size_t fm_dp_workspace_bytes(const fm_dims* d, const fm_dp* p) {
   if (validate_dims(d) || !p) return 0;
-  return 256;  // scratch reserved for the deep-prior state (the latent kernel keeps its state on chip)
+  // the output-layer weights transposed (Hd, F) for coalesced streaming in the
+  // Metropolis kernel (written by fm_prologue_dp); the Adam kernel keeps its
+  // state on chip
+  const size_t rs = d->dtype == FM_F64 ? 8 : 4;
+  return 256 + (((size_t)p->Hd * (size_t)d->F * rs + 255) & ~(size_t)255);
 }
 
 int fm_prologue_dp(const fm_dims* d, const fm_state* s, const fm_dp* p, void* stream) {

@@ -20,13 +20,14 @@
 // steps = 0 is the decoder refresh r = dec(z) alone (prologue).
 #pragma once
 #include "fm_common.cuh"
+#include "fm_nmf.cuh"
 
 namespace fm {
 
 template <typename R> struct MhArgs {
   const R *W1, *b1;  // (Hd, D), (Hd)
   const R *W2, *b2;  // (Hd, Hd), (Hd): exp-MLP second hidden layer
-  const R *Wo, *bo;  // (F, Hd), (F): output layer (W3, b3)
+  const R *WoT, *bo; // (Hd, F) transposed output layer (W3^T, written by the prologue), (F)
   const R *u, *v;    // (B, F), (B, T)
   R *z, *r;          // (B, T, D), (B, T, F)
   const R* lam;      // (B, N, F, T)
@@ -129,9 +130,8 @@ __global__ void __launch_bounds__(256) k_dp_mh(MhArgs<R> a) {
       R acc[4];
 #pragma unroll
       for (int q = 0; q < 4; ++q) acc[q] = a.bo[f];
-      const R* wr = a.Wo + (size_t)f * Hd;
       for (int j = 0; j < Hd; ++j) {
-        const R w = wr[j];
+        const R w = a.WoT[(size_t)j * F + f];  // coalesced across the f threads
 #pragma unroll
         for (int q = 0; q < 4; ++q)
           if (q < nfr) acc[q] += w * hl[q * Hd + j];
@@ -193,8 +193,14 @@ __global__ void __launch_bounds__(256) k_dp_mh(MhArgs<R> a) {
           R yn = ln * gm + yr, yo = lo * gm + yr;
           yn = yn > tiny ? yn : tiny;
           yo = yo > tiny ? yo : tiny;
-          s1[q] += x * (R(1) / yn - R(1) / yo);
-          s2[q] += log(yn / yo);
+          if constexpr (sizeof(R) == 8) {  // the reference's expression order
+            s1[q] += x * (R(1) / yn - R(1) / yo);
+            s2[q] += log(yn / yo);
+          } else {  // complex64 mode: MUFU reciprocals / log (<= 2 ulp)
+            const R iyn = rcp_r(yn), iyo = rcp_r(yo);
+            s1[q] += x * (iyn - iyo);
+            s2[q] += log_fast(yn * iyo);
+          }
         }
       }
     }
@@ -235,6 +241,22 @@ __global__ void __launch_bounds__(256) k_dp_mh(MhArgs<R> a) {
   }
   for (int e = tid; e < nfr * D; e += 256) a.z[((size_t)b * T + t0) * D + e] = zc[e];
   for (int e = tid; e < nfr * F; e += 256) a.r[((size_t)b * T + t0) * F + e] = rc[e];
+}
+
+// W3 (F, Hd) -> W3^T (Hd, F); grid (ceil(F/32), ceil(Hd/32)), block (32, 8)
+template <typename R>
+__global__ void k_transpose_fh(const R* __restrict__ W, R* __restrict__ Wt, int F, int Hd) {
+  __shared__ R tile[32][33];
+  const int f0 = blockIdx.x * 32, j0 = blockIdx.y * 32;
+  for (int i = threadIdx.y; i < 32; i += 8) {
+    const int f = f0 + i, j = j0 + threadIdx.x;
+    tile[i][threadIdx.x] = (f < F && j < Hd) ? W[(size_t)f * Hd + j] : R(0);
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += 8) {
+    const int j = j0 + i, f = f0 + threadIdx.x;
+    if (f < F && j < Hd) Wt[(size_t)j * F + f] = tile[threadIdx.x][i];
+  }
 }
 
 // shared-memory bytes of k_dp_mh for FPB frames (cache: x~ and y_rest staged)

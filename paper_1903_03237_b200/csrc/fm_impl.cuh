@@ -549,7 +549,7 @@ int Impl<R>::dp_mh(const fm_dims* d, const fm_state* s, const fm_dp* p, int step
   a.b1 = reinterpret_cast<const R*>(p->b1);
   a.W2 = reinterpret_cast<const R*>(p->W2);
   a.b2 = reinterpret_cast<const R*>(p->b2);
-  a.Wo = reinterpret_cast<const R*>(p->W3);
+  a.WoT = reinterpret_cast<const R*>(reinterpret_cast<unsigned char*>(p->work) + 256);
   a.bo = reinterpret_cast<const R*>(p->b3);
   a.u = reinterpret_cast<const R*>(p->u);
   a.v = reinterpret_cast<const R*>(p->v);
@@ -567,15 +567,15 @@ int Impl<R>::dp_mh(const fm_dims* d, const fm_state* s, const fm_dp* p, int step
   a.kind = p->decoder_kind;
   a.D = (int)p->D; a.Hd = (int)p->Hd;
   a.N = (int)d->N; a.F = (int)d->F; a.T = (int)d->T; a.M = (int)d->M; a.B = (int)d->B;
-  // frames per CTA: 4 (fp32) / 2 (fp64), fewer while the staged x~ / y_rest do
+  // frames per CTA: 2, fewer while the staged x~ / y_rest do
   // not fit; without staging they are re-read from L2 every proposal
   const size_t rs = sizeof(R), cap = 200 * 1024;
   a.cache = 1;
-  a.fpb = sizeof(R) == 4 ? 4 : 2;
+  a.fpb = 2;  // 2 frames per 256-thread CTA: ~2 CTAs (16 warps) per SM at config 4
   while (a.fpb > 1 && mh_smem_bytes(rs, a.fpb, a.D, a.Hd, a.F, a.M, true) > cap) --a.fpb;
   if (mh_smem_bytes(rs, a.fpb, a.D, a.Hd, a.F, a.M, true) > cap) {
     a.cache = 0;
-    a.fpb = sizeof(R) == 4 ? 4 : 2;
+    a.fpb = 2;
   }
   if (steps == 0) a.cache = 0;
   const size_t sm = mh_smem_bytes(rs, a.fpb, a.D, a.Hd, a.F, a.M, a.cache != 0);
@@ -629,6 +629,11 @@ int Impl<R>::prologue_dp(const fm_dims* d, const fm_state* s, const fm_dp* p, cu
   const Plan pl = make_plan(d);
   unsigned char* w = reinterpret_cast<unsigned char*>(s->work);
   FM_CUDA(cudaMemsetAsync(w + pl.off_cnt, 0, pl.total - pl.off_cnt, st));
+  k_transpose_fh<R><<<dim3((unsigned)((d->F + 31) / 32), (unsigned)((p->Hd + 31) / 32)), dim3(32, 8), 0,
+                      st>>>(reinterpret_cast<const R*>(p->W3),
+                            reinterpret_cast<R*>(reinterpret_cast<unsigned char*>(p->work) + 256),
+                            (int)d->F, (int)p->Hd);
+  FM_CHECK_LAUNCH("k_transpose_fh");
   if (p->decoder_kind == FM_DEC_TOY) {
     if (int rc = dp_mh(d, s, p, 0, st)) return rc;
   } else {
