@@ -226,6 +226,23 @@ int fm_scale_observation(const fm_dims* d, void* X, const double* scale_host, vo
  * throughout; eigenvector phases are arbitrary (as in LAPACK). */
 int fm_spatial_init(const fm_dims* d, const void* X, void* Q, double* w, void* stream);
 
+/* ---- STFT front / back end (stft.py:27-91) ---------------
+ * Periodic Hann window of length L (power of two), reflect padding by L/2,
+ * frames every hop samples (0 < hop <= L), zero tail to a whole frame.
+ * fm_stft_frames: the frame count T = 1 + ceil((n + 2 (L/2) - L) / hop).
+ * fm_stft: wave (n, M) real of dtype -> spec (L/2+1, T, M) complex, device.
+ * fm_istft: spec (L/2+1, T, M) -> out (length, M), length <= (T-1) hop
+ * (the de-padded signal, trimmed); windowed overlap-add divided by the
+ * summed squared window (max with TINY); work: fm_istft_workspace_bytes.
+ * Validation (power of two, hop range, n >= L) is the caller's, as in the
+ * reference's Python; invalid sizes return FM_EINVAL. */
+int64_t fm_stft_frames(int64_t n_samples, int64_t window_length, int64_t hop);
+int fm_stft(int dtype, int64_t n_samples, int64_t M, int64_t window_length, int64_t hop,
+            const void* wave, void* spec, void* stream);
+size_t fm_istft_workspace_bytes(int dtype, int64_t n_frames, int64_t M, int64_t window_length);
+int fm_istft(int dtype, int64_t n_frames, int64_t M, int64_t window_length, int64_t hop,
+             int64_t length, const void* spec, void* work, void* out, void* stream);
+
 const char* fm_last_error(void);
 int fm_version(void);
 

@@ -216,8 +216,38 @@ def save_dp_mh(name, F, T, M, K, n_iter, seed=5):
     print(f"{name}: LL {res.likelihood_trace[0]:.6f} -> {res.likelihood_trace[-1]:.6f}", flush=True)
 
 
+def save_stft(name="stft.npz"):
+    """The reference's stft / istft (stft.py:27-91) on seeded multichannel
+    signals: several window / hop / channel / length combinations, a 1-D
+    input, and the round trip with and without ``length``."""
+    import importlib
+
+    ST = importlib.import_module("fastsep.stft")
+
+    rng = np.random.default_rng(77)
+    out = {}
+    cases = {"a": (4096, 2, 1024, 256), "b": (3001, 3, 512, 128), "c": (2048, 1, 256, 256),
+             "d": (1500, 4, 64, 48), "e": (1024, 2, 1024, 512)}
+    for tag, (n, M, L, hop) in cases.items():
+        x = rng.standard_normal((n, M))
+        spec = ST.stft(x, L, hop)
+        out[f"{tag}_x"], out[f"{tag}_spec"] = x, spec
+        out[f"{tag}_y"] = ST.istft(spec, L, hop, length=n)
+        out[f"{tag}_yfull"] = ST.istft(spec, L, hop)
+        noisy = spec + 0.1 * (rng.standard_normal(spec.shape) + 1j * rng.standard_normal(spec.shape))
+        out[f"{tag}_noisy"], out[f"{tag}_ynoisy"] = noisy, ST.istft(noisy, L, hop)
+        out[f"{tag}_shape"] = np.array([n, M, L, hop])
+    x1 = rng.standard_normal(2000)
+    out["mono_x"], out["mono_spec"] = x1, ST.stft(x1, 512, 128)
+    np.savez_compressed(os.path.join(OUT, name), **out)
+    print(f"{name} written", flush=True)
+
+
 def main():
     os.makedirs(OUT, exist_ok=True)
+    if "--stft-only" in sys.argv:
+        save_stft()
+        return
     if "--dp-mh-only" in sys.argv:
         save_dp_mh("run_dp_mh.npz", 33, 64, 4, 8, 6)
         return
@@ -246,6 +276,7 @@ def main():
     save_dp("run_dp_mu.npz", 33, 64, 4, 8, 8, 0)
     save_dp("run_dp_adam.npz", 33, 64, 4, 8, 8, 10)
     save_dp_mh("run_dp_mh.npz", 33, 64, 4, 8, 6)
+    save_stft()
     if "--with-c1" in sys.argv:
         X1 = make_mixture(513, 1024, 8, 4, 16, seed=0)
         save_run("run_c1_c64.npz", X1, 513, 1024, 8, 4, 16, 0, 100, False, round64=True)

@@ -58,6 +58,28 @@ using namespace fm;
 
 extern "C" {
 
+int64_t fm_stft_frames(int64_t n_samples, int64_t window_length, int64_t hop) {
+  if (window_length < 2 || hop < 1 || n_samples < window_length) return 0;
+  return stft_frames(n_samples, window_length, hop);
+}
+
+int fm_stft(int dtype, int64_t n_samples, int64_t M, int64_t window_length, int64_t hop,
+            const void* wave, void* spec, void* stream) {
+  return FM_BY_DTYPE(dtype, stft(n_samples, M, window_length, hop, wave, spec, (cudaStream_t)stream));
+}
+
+size_t fm_istft_workspace_bytes(int dtype, int64_t n_frames, int64_t M, int64_t window_length) {
+  const size_t rs = dtype == FM_F64 ? 8 : 4;
+  return (size_t)std::max<int64_t>(n_frames, 1) * (size_t)std::max<int64_t>(M, 1) *
+         (size_t)std::max<int64_t>(window_length, 1) * rs;
+}
+
+int fm_istft(int dtype, int64_t n_frames, int64_t M, int64_t window_length, int64_t hop,
+             int64_t length, const void* spec, void* work, void* out, void* stream) {
+  return FM_BY_DTYPE(dtype, istft(n_frames, M, window_length, hop, length, spec, work, out,
+                                  (cudaStream_t)stream));
+}
+
 const char* fm_last_error(void) { return g_err; }
 int fm_version(void) { return 1; }
 

@@ -20,6 +20,7 @@
 #include "fm_vacc_tc.cuh"
 #include "fm_vacc_blk.cuh"
 #include "fm_init.cuh"
+#include "fm_stft.cuh"
 
 namespace fm {
 
@@ -225,6 +226,10 @@ template <typename R> struct Impl {
                        cudaStream_t st);
   static int scale(const fm_dims* d, void* X, const double* scale_host, cudaStream_t st);
   static int spatial_init(const fm_dims* d, const void* X, void* Q, double* w, cudaStream_t st);
+  static int stft(int64_t n, int64_t M, int64_t L, int64_t hop, const void* wave, void* spec,
+                  cudaStream_t st);
+  static int istft(int64_t T, int64_t M, int64_t L, int64_t hop, int64_t length, const void* spec,
+                   void* work, void* out, cudaStream_t st);
 };
 
 template <typename Kern>
@@ -930,6 +935,72 @@ int Impl<R>::spatial_init(const fm_dims* d, const void* X, void* Q, double* w, c
     k_spatial_init<R, MM><<<dim3((unsigned)d->F, (unsigned)d->B), 256, 0, st>>>(a);
     FM_CHECK_LAUNCH("k_spatial_init");
   });
+  return FM_OK;
+}
+
+// ---- STFT / iSTFT (fm_stft.cuh) ----------------------------------------------
+inline int stft_group(int64_t M, int64_t L, size_t csize) {
+  // channels per CTA: their rows + twiddles within ~96 KB (2 CTAs per SM)
+  const long long per = (long long)L * (long long)csize;
+  long long g = std::max<long long>(1, (96 * 1024 - (long long)(L / 2) * (long long)csize) / per);
+  return (int)std::min<long long>(g, M);
+}
+
+inline int stft_check(int64_t M, int64_t L, int64_t hop) {
+  if (L < 2 || (L & (L - 1)) || L > (1 << 16) || hop < 1 || hop > L || M < 1) {
+    set_error("stft sizes: window_length %lld (power of two, 2..65536), hop %lld, M %lld",
+              (long long)L, (long long)hop, (long long)M);
+    return FM_EINVAL;
+  }
+  return FM_OK;
+}
+
+template <typename R>
+int Impl<R>::stft(int64_t n, int64_t M, int64_t L, int64_t hop, const void* wave, void* spec,
+                  cudaStream_t st) {
+  if (int rc = stft_check(M, L, hop)) return rc;
+  if (n < L) {
+    set_error("signal length %lld is shorter than one window (%lld)", (long long)n, (long long)L);
+    return FM_EINVAL;
+  }
+  const long long T = stft_frames(n, L, hop);
+  const int G = stft_group(M, L, sizeof(C));
+  const size_t sm = ((size_t)G * L + L / 2) * sizeof(C);
+  if (sm > LT_SMEM_MAX) { set_error("window_length %lld too large", (long long)L); return FM_EINVAL; }
+  if (int rc = ensure_smem(k_stft<R>, sm)) return rc;
+  int logL = 0;
+  while ((1LL << logL) < L) ++logL;
+  k_stft<R><<<dim3((unsigned)T, (unsigned)((M + G - 1) / G)), STFT_THREADS, sm, st>>>(
+      reinterpret_cast<const R*>(wave), reinterpret_cast<C*>(spec), (long long)n, (int)M, (int)L, logL,
+      (int)hop, (int)T, G);
+  FM_CHECK_LAUNCH("k_stft");
+  return FM_OK;
+}
+
+template <typename R>
+int Impl<R>::istft(int64_t T, int64_t M, int64_t L, int64_t hop, int64_t length, const void* spec,
+                   void* work, void* out, cudaStream_t st) {
+  if (int rc = stft_check(M, L, hop)) return rc;
+  if (T < 1 || length < 0 || length > (T - 1) * hop) {
+    set_error("istft: length %lld outside 0..%lld", (long long)length, (long long)((T - 1) * hop));
+    return FM_EINVAL;
+  }
+  const int G = stft_group(M, L, sizeof(C));
+  const size_t sm = ((size_t)G * L + L / 2) * sizeof(C);
+  if (sm > LT_SMEM_MAX) { set_error("window_length %lld too large", (long long)L); return FM_EINVAL; }
+  if (int rc = ensure_smem(k_istft_frames<R>, sm)) return rc;
+  int logL = 0;
+  while ((1LL << logL) < L) ++logL;
+  k_istft_frames<R><<<dim3((unsigned)T, (unsigned)((M + G - 1) / G)), STFT_THREADS, sm, st>>>(
+      reinterpret_cast<const C*>(spec), reinterpret_cast<R*>(work), (int)M, (int)L, logL, (int)T, G);
+  FM_CHECK_LAUNCH("k_istft_frames");
+  if (length > 0) {
+    const long long tot = length * M;
+    const unsigned blocks = (unsigned)std::min<long long>((tot + 255) / 256, 148 * 16);
+    k_ola<R><<<blocks, 256, 0, st>>>(reinterpret_cast<const R*>(work), reinterpret_cast<R*>(out),
+                                     (long long)length, (int)M, (int)L, (int)hop, (int)T);
+    FM_CHECK_LAUNCH("k_ola");
+  }
   return FM_OK;
 }
 
