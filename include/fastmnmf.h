@@ -243,6 +243,37 @@ size_t fm_istft_workspace_bytes(int dtype, int64_t n_frames, int64_t M, int64_t 
 int fm_istft(int dtype, int64_t n_frames, int64_t M, int64_t window_length, int64_t hop,
              int64_t length, const void* spec, void* work, void* out, void* stream);
 
+/* ---- full-rank MNMF comparator (method "mnmf") ------------
+ * X (F,T,M) complex, G (N,F,M,M) complex Hermitian SCMs, lam (N,F,T) real,
+ * M <= 8; fp64 per-bin linear algebra, storage in the dtype.
+ * fm_fullrank_stats: _kernels.fullrank_stats (_kernels.py:62-180): phi
+ *   (2,N,F,T) = [phi1 | phi2] when want_phi, A/B (N,F,M,M) when want_ab,
+ *   *loglik (device fp64, may be NULL) = sum_ft (-x^H Y^-1 x - log|Y|);
+ *   work: fm_fullrank_workspace_bytes.
+ * fm_update_scm: spatial.update_scm (spatial.py:145-169) on G in place, then
+ *   normalize_trace (spatial.py:252-257) when normalize (c (N,F) = tr/M);
+ *   status code 1 at (n, f) = negative spectrum (NumericalBreakdownError).
+ * fm_wiener_fullrank: separate.wiener_fullrank (separate.py:83-107) ->
+ *   images (N,F,T,M); status code 2 at (f, t) = singular mixture covariance.
+ * fm_nmf_mu: NmfSource.apply_mu (sources.py:191-198) from phi, step 0 = W,
+ *   1 = H; fm_nmf_absorb: W (N,F,K) *= c (N,F) (sources.py:202-204).
+ * fm_reconstruct_scm: spatial.reconstruct_scm (spatial.py:211-223), status
+ *   code 3 at f = singular Q. */
+size_t fm_fullrank_workspace_bytes(int dtype, int64_t F, int64_t T, int64_t M);
+int fm_fullrank_stats(int dtype, int64_t F, int64_t T, int64_t M, int64_t N, const void* X,
+                      const void* G, const void* lam, double ridge, int want_ab, int want_phi,
+                      void* phi, void* A, void* B, void* work, double* loglik, void* stream);
+int fm_update_scm(int dtype, int64_t N, int64_t F, int64_t M, void* G, const void* A, const void* B,
+                  int normalize, void* c, uint64_t* status, void* stream);
+int fm_wiener_fullrank(int dtype, int64_t N, int64_t F, int64_t T, int64_t M, const void* lam,
+                       const void* G, const void* X, double ridge, void* images, uint64_t* status,
+                       void* stream);
+int fm_nmf_mu(int dtype, int64_t N, int64_t F, int64_t T, int64_t K, const void* phi, void* W, void* H,
+              int step, void* stream);
+int fm_nmf_absorb(int dtype, int64_t N, int64_t F, int64_t K, void* W, const void* c, void* stream);
+int fm_reconstruct_scm(int dtype, int64_t N, int64_t F, int64_t M, const void* Q, const void* g,
+                       void* G, uint64_t* status, void* stream);
+
 const char* fm_last_error(void);
 int fm_version(void);
 

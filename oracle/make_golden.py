@@ -243,8 +243,59 @@ def save_stft(name="stft.npz"):
     print(f"{name} written", flush=True)
 
 
+def save_fullrank(name="fullrank.npz"):
+    """The reference's full-rank kernels and a run(method="mnmf") with the
+    init injected (monkeypatched _build_spatial / _build_source)."""
+    rng = np.random.default_rng(31)
+    out = {}
+    F, T, M, N = 5, 24, 3, 2
+    X = rng.standard_normal((F, T, M)) + 1j * rng.standard_normal((F, T, M))
+    Aq = rng.standard_normal((N, F, M, M)) + 1j * rng.standard_normal((N, F, M, M))
+    G = Aq @ np.conj(Aq.swapaxes(-1, -2)) + 0.1 * np.eye(M)
+    lam = rng.uniform(0.2, 2.0, (N, F, T))
+    out.update(k_X=X, k_G=G, k_lam=lam)
+    p1, p2, _, _, ll = K.fullrank_stats(X, G, lam, 1e-3, want_ab=False, want_phi=True)
+    _, _, A, B, _ = K.fullrank_stats(X, G, lam, 1e-3, want_ab=True, want_phi=False)
+    out.update(k_phi1=p1, k_phi2=p2, k_ll=np.array(ll), k_A=A, k_B=B)
+    out["k_Gnew"] = SP.update_scm(G, A, B)
+    out["k_Gnorm"], out["k_c"] = SP.normalize_trace(out["k_Gnew"])
+    out["k_wiener"] = S.wiener_fullrank(lam, G, X, 1e-3)
+    Q = np.eye(M) + 0.2 * (rng.standard_normal((F, M, M)) + 1j * rng.standard_normal((F, M, M)))
+    g = rng.uniform(0.1, 1.0, (N, F, M))
+    out.update(k_Q=Q, k_g=g, k_recon=SP.reconstruct_scm(Q, g))
+    # run(method="mnmf") with an injected init (config-0 style mixture)
+    Fr, Tr, Mr, Nr, Kr, it = 12, 48, 3, 2, 4, 6
+    Xr = make_mixture(Fr, Tr, Mr, Nr, Kr, seed=8)
+    Q0, g0, W0, H0 = baseline_init(Fr, Tr, Mr, Nr, Kr, 8)
+    G0 = SP.reconstruct_scm(Q0, g0)
+    orig = (S._build_spatial, S._build_source)
+    S._build_spatial = lambda cfg, Xs: SP.FullRankSpatial(G0.copy())
+    S._build_source = lambda cfg, Xs, rng: SRC.NmfSource(W0.copy(), H0.copy())
+    st = {}
+
+    def snap(i, loop):
+        st.update(G=loop.spatial.G_NFMM.copy(), W=loop.source.W_NFK.copy(),
+                  H=loop.source.H_NKT.copy())
+
+    try:
+        cfg = fastsep.SeparatorConfig(method="mnmf", n_sources=Nr, n_basis=Kr, n_iterations=it,
+                                      seed=8)
+        res = fastsep.run(cfg, Xr, on_iteration=snap)
+    finally:
+        S._build_spatial, S._build_source = orig
+    out.update(r_X=Xr, r_G0=G0, r_W0=W0, r_H0=H0, r_trace=res.likelihood_trace,
+               r_images=res.images_NFTM, r_G=st["G"], r_W=st["W"], r_H=st["H"],
+               r_shape=np.array([Fr, Tr, Mr, Nr, Kr, it]))
+    np.savez_compressed(os.path.join(OUT, name), **out)
+    print(f"{name} written: LL {res.likelihood_trace[0]:.6f} -> {res.likelihood_trace[-1]:.6f}",
+          flush=True)
+
+
 def main():
     os.makedirs(OUT, exist_ok=True)
+    if "--fullrank-only" in sys.argv:
+        save_fullrank()
+        return
     if "--stft-only" in sys.argv:
         save_stft()
         return
@@ -277,6 +328,7 @@ def main():
     save_dp("run_dp_adam.npz", 33, 64, 4, 8, 8, 10)
     save_dp_mh("run_dp_mh.npz", 33, 64, 4, 8, 6)
     save_stft()
+    save_fullrank()
     if "--with-c1" in sys.argv:
         X1 = make_mixture(513, 1024, 8, 4, 16, seed=0)
         save_run("run_c1_c64.npz", X1, 513, 1024, 8, 4, 16, 0, 100, False, round64=True)

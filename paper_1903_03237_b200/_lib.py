@@ -52,6 +52,19 @@ class FmDp(ctypes.Structure):
 
 # (name, restype, argtypes) -- the exported surface of fastmnmf.h
 SIGNATURES = [
+    ("fm_fullrank_workspace_bytes", ctypes.c_size_t, [ctypes.c_int, _c_i64, _c_i64, _c_i64]),
+    ("fm_fullrank_stats", ctypes.c_int,
+     [ctypes.c_int, _c_i64, _c_i64, _c_i64, _c_i64, _vp, _vp, _vp, ctypes.c_double, ctypes.c_int,
+      ctypes.c_int, _vp, _vp, _vp, _vp, _vp, _vp]),
+    ("fm_update_scm", ctypes.c_int,
+     [ctypes.c_int, _c_i64, _c_i64, _c_i64, _vp, _vp, _vp, ctypes.c_int, _vp, _vp, _vp]),
+    ("fm_wiener_fullrank", ctypes.c_int,
+     [ctypes.c_int, _c_i64, _c_i64, _c_i64, _c_i64, _vp, _vp, _vp, ctypes.c_double, _vp, _vp, _vp]),
+    ("fm_nmf_mu", ctypes.c_int,
+     [ctypes.c_int, _c_i64, _c_i64, _c_i64, _c_i64, _vp, _vp, _vp, ctypes.c_int, _vp]),
+    ("fm_nmf_absorb", ctypes.c_int, [ctypes.c_int, _c_i64, _c_i64, _c_i64, _vp, _vp, _vp]),
+    ("fm_reconstruct_scm", ctypes.c_int,
+     [ctypes.c_int, _c_i64, _c_i64, _c_i64, _vp, _vp, _vp, _vp, _vp]),
     ("fm_stft_frames", _c_i64, [_c_i64, _c_i64, _c_i64]),
     ("fm_stft", ctypes.c_int, [ctypes.c_int, _c_i64, _c_i64, _c_i64, _c_i64, _vp, _vp, _vp]),
     ("fm_istft_workspace_bytes", ctypes.c_size_t, [ctypes.c_int, _c_i64, _c_i64, _c_i64]),

@@ -80,6 +80,43 @@ int fm_istft(int dtype, int64_t n_frames, int64_t M, int64_t window_length, int6
                                   (cudaStream_t)stream));
 }
 
+size_t fm_fullrank_workspace_bytes(int dtype, int64_t F, int64_t T, int64_t M) {
+  return fr_workspace(dtype == FM_F64 ? 8 : 4, F, T, M);
+}
+
+int fm_fullrank_stats(int dtype, int64_t F, int64_t T, int64_t M, int64_t N, const void* X,
+                      const void* G, const void* lam, double ridge, int want_ab, int want_phi,
+                      void* phi, void* A, void* B, void* work, double* loglik, void* stream) {
+  return FM_BY_DTYPE(dtype, fr_stats(F, T, M, N, X, G, lam, ridge, want_ab, want_phi, phi, A, B, work,
+                                     loglik, (cudaStream_t)stream));
+}
+
+int fm_update_scm(int dtype, int64_t N, int64_t F, int64_t M, void* G, const void* A, const void* B,
+                  int normalize, void* c, uint64_t* status, void* stream) {
+  return FM_BY_DTYPE(dtype, fr_scm(N, F, M, G, A, B, normalize, c, status, (cudaStream_t)stream));
+}
+
+int fm_wiener_fullrank(int dtype, int64_t N, int64_t F, int64_t T, int64_t M, const void* lam,
+                       const void* G, const void* X, double ridge, void* images, uint64_t* status,
+                       void* stream) {
+  return FM_BY_DTYPE(dtype, fr_wiener(N, F, T, M, lam, G, X, ridge, images, status,
+                                      (cudaStream_t)stream));
+}
+
+int fm_nmf_mu(int dtype, int64_t N, int64_t F, int64_t T, int64_t K, const void* phi, void* W, void* H,
+              int step, void* stream) {
+  return FM_BY_DTYPE(dtype, fr_nmf_mu(N, F, T, K, phi, W, H, step, (cudaStream_t)stream));
+}
+
+int fm_nmf_absorb(int dtype, int64_t N, int64_t F, int64_t K, void* W, const void* c, void* stream) {
+  return FM_BY_DTYPE(dtype, fr_absorb(N, F, K, W, c, (cudaStream_t)stream));
+}
+
+int fm_reconstruct_scm(int dtype, int64_t N, int64_t F, int64_t M, const void* Q, const void* g,
+                       void* G, uint64_t* status, void* stream) {
+  return FM_BY_DTYPE(dtype, fr_reconstruct(N, F, M, Q, g, G, status, (cudaStream_t)stream));
+}
+
 const char* fm_last_error(void) { return g_err; }
 int fm_version(void) { return 1; }
 

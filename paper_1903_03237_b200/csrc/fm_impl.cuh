@@ -21,6 +21,7 @@
 #include "fm_vacc_blk.cuh"
 #include "fm_init.cuh"
 #include "fm_stft.cuh"
+#include "fm_fullrank.cuh"
 
 namespace fm {
 
@@ -228,6 +229,18 @@ template <typename R> struct Impl {
   static int spatial_init(const fm_dims* d, const void* X, void* Q, double* w, cudaStream_t st);
   static int stft(int64_t n, int64_t M, int64_t L, int64_t hop, const void* wave, void* spec,
                   cudaStream_t st);
+  static int fr_stats(int64_t F, int64_t T, int64_t M, int64_t N, const void* X, const void* G,
+                      const void* lam, double ridge, int want_ab, int want_phi, void* phi, void* A,
+                      void* B, void* work, double* ll, cudaStream_t st);
+  static int fr_scm(int64_t N, int64_t F, int64_t M, void* G, const void* A, const void* B,
+                    int normalize, void* c, uint64_t* status, cudaStream_t st);
+  static int fr_wiener(int64_t N, int64_t F, int64_t T, int64_t M, const void* lam, const void* G,
+                       const void* X, double ridge, void* out, uint64_t* status, cudaStream_t st);
+  static int fr_nmf_mu(int64_t N, int64_t F, int64_t T, int64_t K, const void* phi, void* W, void* H,
+                       int step, cudaStream_t st);
+  static int fr_absorb(int64_t N, int64_t F, int64_t K, void* W, const void* c, cudaStream_t st);
+  static int fr_reconstruct(int64_t N, int64_t F, int64_t M, const void* Q, const void* g, void* G,
+                            uint64_t* status, cudaStream_t st);
   static int istft(int64_t T, int64_t M, int64_t L, int64_t hop, int64_t length, const void* spec,
                    void* work, void* out, cudaStream_t st);
 };
@@ -1001,6 +1014,114 @@ int Impl<R>::istft(int64_t T, int64_t M, int64_t L, int64_t hop, int64_t length,
                                      (long long)length, (int)M, (int)L, (int)hop, (int)T);
     FM_CHECK_LAUNCH("k_ola");
   }
+  return FM_OK;
+}
+
+// ---- full-rank MNMF comparator (fm_fullrank.cuh) ----------------------------
+#define FM_DISPATCH_M8(Mrt, ...)                                                       \
+  switch (Mrt) {                                                                       \
+    case 1: { constexpr int MM = 1; __VA_ARGS__; } break;                              \
+    case 2: { constexpr int MM = 2; __VA_ARGS__; } break;                              \
+    case 3: { constexpr int MM = 3; __VA_ARGS__; } break;                              \
+    case 4: { constexpr int MM = 4; __VA_ARGS__; } break;                              \
+    case 5: { constexpr int MM = 5; __VA_ARGS__; } break;                              \
+    case 6: { constexpr int MM = 6; __VA_ARGS__; } break;                              \
+    case 7: { constexpr int MM = 7; __VA_ARGS__; } break;                              \
+    case 8: { constexpr int MM = 8; __VA_ARGS__; } break;                              \
+    default: set_error("full-rank model: M=%d outside 1..8", (int)(Mrt)); return FM_EINVAL; \
+  }
+
+inline size_t fr_workspace(size_t rs, int64_t F, int64_t T, int64_t M) {
+  const size_t ft = (size_t)F * T;
+  return align256(ft * M * 2 * rs) + align256(ft * M * M * 2 * rs) + align256(ft * 8) + 256;
+}
+
+template <typename R>
+int Impl<R>::fr_stats(int64_t F, int64_t T, int64_t M, int64_t N, const void* X, const void* G,
+                      const void* lam, double ridge, int want_ab, int want_phi, void* phi, void* A,
+                      void* B, void* work, double* ll, cudaStream_t st) {
+  unsigned char* w = reinterpret_cast<unsigned char*>(work);
+  const size_t ft = (size_t)F * T;
+  C* Zs = reinterpret_cast<C*>(w);
+  C* Yis = reinterpret_cast<C*>(w + align256(ft * M * sizeof(C)));
+  double* llp = reinterpret_cast<double*>(w + align256(ft * M * sizeof(C)) + align256(ft * M * M * sizeof(C)));
+  const unsigned nb = (unsigned)((ft + 127) / 128);
+  FM_DISPATCH_M8(M, {
+    k_fr_bin<R, MM><<<nb, 128, 0, st>>>(reinterpret_cast<const C*>(X), reinterpret_cast<const C*>(G),
+                                        reinterpret_cast<const R*>(lam), ridge, (int)N, (int)F, (int)T,
+                                        want_phi, reinterpret_cast<R*>(phi), want_ab ? Zs : nullptr,
+                                        Yis, llp);
+    FM_CHECK_LAUNCH("k_fr_bin");
+    if (want_ab) {
+      const long long nt = N * F * (MM * (MM + 1) / 2);
+      k_fr_ab<R, MM><<<(unsigned)((nt + 127) / 128), 128, 0, st>>>(
+          reinterpret_cast<const R*>(lam), Zs, Yis, (int)N, (int)F, (int)T, reinterpret_cast<C*>(A),
+          reinterpret_cast<C*>(B));
+      FM_CHECK_LAUNCH("k_fr_ab");
+    }
+  });
+  if (ll) {
+    k_sum_fixed<<<1, 256, 0, st>>>(llp, (long long)ft, ll);
+    FM_CHECK_LAUNCH("k_sum_fixed");
+  }
+  return FM_OK;
+}
+
+template <typename R>
+int Impl<R>::fr_scm(int64_t N, int64_t F, int64_t M, void* G, const void* A, const void* B,
+                    int normalize, void* c, uint64_t* status, cudaStream_t st) {
+  FM_DISPATCH_M8(M, {
+    k_fr_scm<R, MM><<<dim3((unsigned)F, (unsigned)N), 32, 0, st>>>(
+        reinterpret_cast<C*>(G), reinterpret_cast<const C*>(A), reinterpret_cast<const C*>(B), (int)F,
+        normalize, reinterpret_cast<R*>(c), reinterpret_cast<unsigned long long*>(status));
+    FM_CHECK_LAUNCH("k_fr_scm");
+  });
+  return FM_OK;
+}
+
+template <typename R>
+int Impl<R>::fr_wiener(int64_t N, int64_t F, int64_t T, int64_t M, const void* lam, const void* G,
+                       const void* X, double ridge, void* out, uint64_t* status, cudaStream_t st) {
+  const size_t ft = (size_t)F * T;
+  FM_DISPATCH_M8(M, {
+    k_fr_wiener<R, MM><<<(unsigned)((ft + 127) / 128), 128, 0, st>>>(
+        reinterpret_cast<const R*>(lam), reinterpret_cast<const C*>(G), reinterpret_cast<const C*>(X),
+        ridge, (int)N, (int)F, (int)T, reinterpret_cast<C*>(out),
+        reinterpret_cast<unsigned long long*>(status));
+    FM_CHECK_LAUNCH("k_fr_wiener");
+  });
+  return FM_OK;
+}
+
+template <typename R>
+int Impl<R>::fr_nmf_mu(int64_t N, int64_t F, int64_t T, int64_t K, const void* phi, void* W, void* H,
+                       int step, cudaStream_t st) {
+  const long long nt = step == 0 ? N * F * K : N * K * T;
+  k_fr_nmf_mu<R><<<(unsigned)((nt + 255) / 256), 256, 0, st>>>(
+      reinterpret_cast<const R*>(phi), reinterpret_cast<R*>(W), reinterpret_cast<R*>(H), (int)N, (int)F,
+      (int)T, (int)K, step);
+  FM_CHECK_LAUNCH("k_fr_nmf_mu");
+  return FM_OK;
+}
+
+template <typename R>
+int Impl<R>::fr_absorb(int64_t N, int64_t F, int64_t K, void* W, const void* c, cudaStream_t st) {
+  const long long nt = N * F * K;
+  k_fr_absorb<R><<<(unsigned)((nt + 255) / 256), 256, 0, st>>>(reinterpret_cast<R*>(W),
+                                                               reinterpret_cast<const R*>(c), N * F, (int)K);
+  FM_CHECK_LAUNCH("k_fr_absorb");
+  return FM_OK;
+}
+
+template <typename R>
+int Impl<R>::fr_reconstruct(int64_t N, int64_t F, int64_t M, const void* Q, const void* g, void* G,
+                            uint64_t* status, cudaStream_t st) {
+  FM_DISPATCH_M8(M, {
+    k_fr_reconstruct<R, MM><<<(unsigned)((F + 63) / 64), 64, 0, st>>>(
+        reinterpret_cast<const C*>(Q), reinterpret_cast<const R*>(g), (int)N, (int)F,
+        reinterpret_cast<C*>(G), reinterpret_cast<unsigned long long*>(status));
+    FM_CHECK_LAUNCH("k_fr_reconstruct");
+  });
   return FM_OK;
 }
 

@@ -76,60 +76,7 @@ __global__ void __launch_bounds__(256) k_spatial_init(InitArgs<R> a) {
   }
   if (tid >= 32) return;
   // ---- cyclic complex Jacobi (warp 0)
-  for (int e = lane; e < M * M; e += 32) V[e] = make_double2(e / M == e % M ? 1.0 : 0.0, 0.0);
-  __syncwarp();
-  for (int sweep = 0; sweep < 40; ++sweep) {
-    double off = 0.0, dia = 0.0;
-    for (int e = lane; e < M * M; e += 32) {
-      const double2 v = G[e];
-      if (e / M == e % M) dia += v.x * v.x;
-      else off += v.x * v.x + v.y * v.y;
-    }
-    off = warp_sum(off);
-    dia = warp_sum(dia);
-    if (!(off > 1e-30 * dia) || off == 0.0) break;
-    for (int p = 0; p < M - 1; ++p) {
-      for (int q = p + 1; q < M; ++q) {
-        const double2 apq = G[p * M + q];
-        const double mag = sqrt(apq.x * apq.x + apq.y * apq.y);
-        if (!(mag > 1e-300)) continue;
-        const double app = G[p * M + p].x, aqq = G[q * M + q].x;
-        // D = diag(1, e^{-i phi}) makes the pair real; then the real rotation
-        // P = [[c, s], [-s, c]] with t = tan(theta) zeroes it (J = D P)
-        const double ep_r = apq.x / mag, ep_i = apq.y / mag;  // e^{i phi}
-        const double tau = (aqq - app) / (2.0 * mag);
-        const double t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
-        const double c = 1.0 / sqrt(1.0 + t * t), sn = t * c;
-        // columns: A J  (col_p' = c col_p - s e^{-i phi} col_q, col_q' = s col_p + c e^{-i phi} col_q)
-        if (lane < M) {
-          const double2 gp = G[lane * M + p], gq = G[lane * M + q];
-          const double2 gqe = make_double2(gq.x * ep_r + gq.y * ep_i, gq.y * ep_r - gq.x * ep_i);
-          G[lane * M + p] = make_double2(c * gp.x - sn * gqe.x, c * gp.y - sn * gqe.y);
-          G[lane * M + q] = make_double2(sn * gp.x + c * gqe.x, sn * gp.y + c * gqe.y);
-          const double2 vp = V[lane * M + p], vq = V[lane * M + q];
-          const double2 vqe = make_double2(vq.x * ep_r + vq.y * ep_i, vq.y * ep_r - vq.x * ep_i);
-          V[lane * M + p] = make_double2(c * vp.x - sn * vqe.x, c * vp.y - sn * vqe.y);
-          V[lane * M + q] = make_double2(sn * vp.x + c * vqe.x, sn * vp.y + c * vqe.y);
-        }
-        __syncwarp();
-        // rows: J^H (A J)  (row_p' = c row_p - s e^{i phi} row_q, row_q' = s row_p + c e^{i phi} row_q)
-        if (lane < M) {
-          const double2 gp = G[p * M + lane], gq = G[q * M + lane];
-          const double2 gqe = make_double2(gq.x * ep_r - gq.y * ep_i, gq.y * ep_r + gq.x * ep_i);
-          G[p * M + lane] = make_double2(c * gp.x - sn * gqe.x, c * gp.y - sn * gqe.y);
-          G[q * M + lane] = make_double2(sn * gp.x + c * gqe.x, sn * gp.y + c * gqe.y);
-        }
-        __syncwarp();
-        if (lane == 0) {
-          G[p * M + q] = make_double2(0.0, 0.0);
-          G[q * M + p] = make_double2(0.0, 0.0);
-          G[p * M + p].y = 0.0;
-          G[q * M + q].y = 0.0;
-        }
-        __syncwarp();
-      }
-    }
-  }
+  warp_jacobi_eigh<M>(G, V, lane);
   // ---- clamp (linalg.py:92: w >= 1e-12 * max(max w, 0)), descending order
   double wmax = -INFINITY;
   for (int m = 0; m < M; ++m) wmax = fmax(wmax, G[m * M + m].x);

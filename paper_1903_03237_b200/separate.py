@@ -20,7 +20,8 @@ from .errors import InvalidInputError, NumericalBreakdownError, SingularMatrixEr
 METHODS = ("fca", "mnmf", "mnmf-dp", "fast-fca", "fast-mnmf", "fast-mnmf-dp")  # separate.py:39
 FAST_METHODS = ("fast-fca", "fast-mnmf", "fast-mnmf-dp")
 DP_METHODS = ("mnmf-dp", "fast-mnmf-dp")
-SUPPORTED_METHODS = ("fast-mnmf", "fast-mnmf-dp")  # the hot path this backend provides
+# the hot path this backend provides, plus the full-rank MNMF comparator (§8(f) 4)
+SUPPORTED_METHODS = ("fast-mnmf", "fast-mnmf-dp", "mnmf")
 PRECISIONS = ("complex128", "complex64")
 
 
@@ -412,6 +413,8 @@ def run(cfg: SeparatorConfig, X_FTM, on_iteration=None, init=None) -> Separation
         raise InvalidInputError(f"observation must have shape (F, T, M), got {tuple(X_FTM.shape)}")
     Xs, scale, floor = _prepare_observation(X_FTM, cfg, torch)
     rng = np.random.default_rng(cfg.seed)  # separate.py:295
+    if cfg.method == "mnmf":
+        return _run_mnmf(cfg, Xs, scale, rng, on_iteration, init)
     dp = None
     if cfg.method == "fast-mnmf-dp":
         from .dp import ToyDecoder, decoder_kind
@@ -476,6 +479,59 @@ def run(cfg: SeparatorConfig, X_FTM, on_iteration=None, init=None) -> Separation
     ll = loop.trace[:, 0].cpu().numpy().copy() if cfg.record_likelihood else np.zeros(0)
     # images at the run's precision (complex64 runs return complex64), in pinned host memory
     images = _to_host(loop.images(scale)[0]).numpy()
+    res = SeparationResult(images_NFTM=images, likelihood_trace=np.asarray(ll),
+                           time_trace=np.asarray(time_trace), method=cfg.method,
+                           config=replace(cfg))
+    res.loop = loop
+    return res
+
+
+def _run_mnmf(cfg, Xs, scale, rng, on_iteration, init):
+    """run() (separate.py:276-330) for method="mnmf": the _FullRankLoop
+    (separate.py:128-172) on the device (fullrank.FullRankDeviceLoop).
+    ``init`` optionally injects (G_NFMM, W_NFK, H_NKT) in the scaled domain;
+    by default the reference's init: circular_init -> reconstruct_scm
+    (separate.py:246-256) and NmfSource.random from the run's rng."""
+    from . import fullrank as FR
+
+    torch = _torch()
+    X1 = Xs[0]
+    F, T, M = X1.shape
+    if M > 8:
+        raise InvalidInputError(f"the full-rank model supports M <= 8, got M={M}")
+    if init is None:
+        Q0, g0, W0, H0 = default_init(cfg, X1, rng)  # device Q (F,M,M), g (N,F,M)
+        G0 = FR.reconstruct_scm(Q0.to("cuda", X1.dtype),
+                                torch.as_tensor(g0).to("cuda", torch.float64 if X1.dtype ==
+                                                       torch.complex128 else torch.float32))
+    else:
+        G0, W0, H0 = init
+    G0 = G0 if isinstance(G0, torch.Tensor) else torch.from_numpy(np.asarray(G0))
+    W0 = W0 if isinstance(W0, torch.Tensor) else torch.from_numpy(np.asarray(W0))
+    H0 = H0 if isinstance(H0, torch.Tensor) else torch.from_numpy(np.asarray(H0))
+    # mixture_ridge (spatial.py:59-61) of the scaled observation
+    dims = _lib.FmDims(1, F, T, M, 1, 1, 0,
+                       _lib.FM_F32 if X1.dtype == torch.complex64 else _lib.FM_F64, 1, 1, 0)
+    sumsq, maxsq = (ctypes.c_double * 1)(), (ctypes.c_double * 1)()
+    _lib.check(_lib.load().fm_observation_stats(ctypes.byref(dims), _lib.ptr(X1), sumsq, maxsq,
+                                                _lib.stream_ptr()), "fm_observation_stats")
+    ridge = 1e-12 * sumsq[0] / float(F * T * M)
+    loop = FR.FullRankDeviceLoop(X1, G0, W0, H0, ridge, cfg.normalize, n_trace=cfg.n_iterations)
+    time_trace = []
+    for it in range(cfg.n_iterations):
+        start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        start.record()
+        loop.iterate()
+        end.record()
+        err = loop.status_error()  # synchronises
+        if err is not None:
+            raise type(err)(f"iteration {it}: {err}")
+        time_trace.append(start.elapsed_time(end) / 1e3)
+        if on_iteration is not None:
+            on_iteration(it, loop)
+    loop.final_loglik()
+    ll = loop.ll[1:cfg.n_iterations + 1].cpu().numpy().copy() if cfg.record_likelihood else np.zeros(0)
+    images = _to_host(loop.images(scale[0])).numpy()
     res = SeparationResult(images_NFTM=images, likelihood_trace=np.asarray(ll),
                            time_trace=np.asarray(time_trace), method=cfg.method,
                            config=replace(cfg))
