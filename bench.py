@@ -374,6 +374,21 @@ def main():
                 "kernel_ms": {n: float(v) for n, v in zip(names, acc)},
                 "step_share": float(acc[dom] * iters / ms_per_step) if ms_per_step else None,
                 "alg_bytes_per_launch": alg}
+    if names[dom] == "k_vacc" and acc[dom] > 0:
+        # the V accumulation is FP32-pipe bound, not HBM bound: its
+        # compute roofline beside the contract's HBM one. Algorithmic flops per
+        # (f, t): P = M(M+1)/2 Hermitian pairs x M weights x 4 (real x complex
+        # FMA) + 6 per pair product + the model power (2NM) and M reciprocals
+        P = M * (M + 1) // 2
+        flops = (4 * P * M + 6 * P + 2 * N * M + M) * (ftm // M)
+        peak_sm = float(json.load(open(os.path.join(REPO, "MEASURED_PEAKS.json")))["sm_max_mhz"]) \
+            if os.path.exists(os.path.join(REPO, "MEASURED_PEAKS.json")) else 1965.0
+        fp32_peak = 148 * 128 * 2 * peak_sm * 1e6 / 1e12  # TFLOP/s (FFMA, all SMs, max clock)
+        ach = flops / (acc[dom] / 1e3) / 1e12
+        roofline["compute"] = {"bound": "fp32-fma", "achieved": ach, "peak": fp32_peak,
+                               "unit": "TFLOP/s", "frac": ach / fp32_peak,
+                               "alg_flops_per_launch": flops,
+                               "peak_kind": "nominal 148 SM x 128 FP32 lanes x 2 x max SM clock"}
 
     # ---- e2e: the public API call with host buffers (pinned), copies inside the timed region
     e2e = None

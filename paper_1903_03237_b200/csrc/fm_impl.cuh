@@ -142,6 +142,11 @@ inline Plan make_plan(const fm_dims* d) {
   // k_gain / k_vacc: segments per bin so that bins x segments >= ~4 CTAs per SM,
   // each segment a multiple of 256 frames (the fp32 chunk; 64/128 divide it)
   long long segs = std::max<long long>(1, (4 * 148 + F * B - 1) / (F * B));
+  static const int seg_override = [] {  // FM_GSEG: segment-count tuning knob (A/B runs)
+    const char* e = getenv("FM_GSEG");
+    return e ? atoi(e) : 0;
+  }();
+  if (seg_override > 0) segs = seg_override;
   long long tr = (T + segs - 1) / segs;
   tr = ((tr + 255) / 256) * 256;
   p.TR = (int)std::min<long long>(tr, std::max<long long>(T, 1));
