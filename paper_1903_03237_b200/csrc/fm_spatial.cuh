@@ -647,8 +647,10 @@ template <typename R> struct BackArgs {
 // One t per thread; grid (ceil(T/256), F, B): the (f, t) plane is tiled
 // flat so every SM streams many small tiles (no per-bin serial loop).
 // ll_part is (B, F, tiles) and reduced in fixed order by the last tile.
+// 3 CTAs per SM (<= 85 registers) up to M = 8; 2 above, where the 16-channel
+// rows would otherwise spill
 template <typename R, int M>
-__global__ void __launch_bounds__(256, 3) k_back(BackArgs<R> a) {
+__global__ void __launch_bounds__(256, (M > 8 ? 2 : 3)) k_back(BackArgs<R> a) {
   pdl_entry();
   using C = cplx<R>;
   __shared__ __align__(16) C Qr[M * M];
