@@ -186,3 +186,27 @@ def test_batch_equals_single_runs():
         assert rel(br.images_BNFTM[b].cpu().numpy(), single.images_NFTM) < 1e-5
         ref = O.run_fastmnmf(Xs[b].astype(np.complex64).astype(np.complex128), *inits[b], it)
         assert rel(single.images_NFTM, ref["images"]) < 1e-3
+
+
+def test_results_own_their_pinned_images():
+    """run() returns images in page-locked blocks of torch's caching host
+    allocator: a live result keeps its block (no aliasing by later runs), and
+    a freed result's block is recycled without touching live ones."""
+    import gc
+    from paper_1903_03237_b200 import SeparatorConfig, run
+    from paper_1903_03237_b200.synth import baseline_init, make_mixture
+    F, T, M, N, K = 9, 40, 3, 2, 3
+    cfg = SeparatorConfig(method="fast-mnmf", n_sources=N, n_basis=K, n_iterations=3,
+                          precision="complex64")
+    Xa = make_mixture(F, T, M, N, K, seed=1).astype(np.complex64)
+    Xb = make_mixture(F, T, M, N, K, seed=2).astype(np.complex64)
+    ra = run(cfg, Xa, init=baseline_init(F, T, M, N, K, 1))
+    keep = ra.images_NFTM.copy()
+    for s in range(3):  # later runs, some results dropped immediately
+        rb = run(cfg, Xb, init=baseline_init(F, T, M, N, K, 2))
+        del rb
+        gc.collect()
+    rc = run(cfg, Xb, init=baseline_init(F, T, M, N, K, 2))
+    np.testing.assert_array_equal(ra.images_NFTM, keep)
+    assert not np.shares_memory(ra.images_NFTM, rc.images_NFTM)
+    assert rel(rc.images_NFTM.sum(axis=0), Xb) < 1e-5
