@@ -423,8 +423,9 @@ def main():
             prof.disable()
             pstats.Stats(prof, stream=sys.stderr).sort_stats("cumulative").print_stats(20)
         cb = 8 if cfg["precision"] == "complex64" else 16
-        h2d = F * T * M * cb + F * M * M * 16 + N * F * M * 8 + N * F * K * 8 + N * K * T * 8
-        d2h = N * F * T * M * cb + iters * 8
+        # bytes per step of the whole job (every replica copies its own)
+        h2d = (F * T * M * cb + F * M * M * 16 + N * F * M * 8 + N * F * K * 8 + N * K * T * 8) * world
+        d2h = (N * F * T * M * cb + iters * 8) * world
         e2e = {"value": F * T * M * iters * world / dt, "unit": UNIT, "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "seconds_per_step": dt,
                "api": "paper_1903_03237_b200.run(SeparatorConfig, X_host_pinned, init=...)"}
