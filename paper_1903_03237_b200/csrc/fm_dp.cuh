@@ -71,20 +71,28 @@ __global__ void __launch_bounds__(256) k_dp_umu(R* __restrict__ u, const R* __re
   }
 }
 
-// V step (sources.py:262-265): v_t *= sqrt(sum_f u_f r_tf phi1_0 / max(..., TINY))
-// grid (ceil(T/32), B), block (32, 8): lanes over t, warps stride f
+// V step (sources.py:262-265): v_t *= sqrt(sum_f u_f r_tf phi1_0 / max(..., TINY)).
+// grid (ceil(T/32), VMU_FS, B), block (32, 8): lanes over t, warps stride the
+// bins of this CTA's split (f = fs*FR + w, w + 8, ...); each split publishes
+// its (num, den) per frame and the CTA completing a 32-frame tile adds the
+// splits in order and applies the update (deterministic).
+constexpr int VMU_FS = 8;
+
 template <typename R>
 __global__ void k_dp_vmu(const R* __restrict__ u, R* __restrict__ v, const R* __restrict__ r,
-                         const R* __restrict__ phi, int N, int F, int T) {
+                         const R* __restrict__ phi, int N, int F, int T, R* __restrict__ part,
+                         unsigned* __restrict__ cnt) {
   pdl_entry();
   __shared__ R red[2][8][33];
-  const int b = blockIdx.y, t = blockIdx.x * 32 + threadIdx.x, w = threadIdx.y;
+  __shared__ int last;
+  const int b = blockIdx.z, fs = blockIdx.y, t = blockIdx.x * 32 + threadIdx.x, w = threadIdx.y;
+  const int FR = (F + VMU_FS - 1) / VMU_FS, fa = fs * FR, fb = min(F, fa + FR);
   const size_t FT = (size_t)F * T;
   const R* p1 = phi + (size_t)b * 2 * N * FT;
   const R* p2 = p1 + (size_t)N * FT;
   R sn = 0, sd = 0;
   if (t < T) {
-    for (int f = w; f < F; f += 8) {
+    for (int f = fa + w; f < fb; f += 8) {
       const R q = u[(size_t)b * F + f] * r[((size_t)b * T + t) * F + f];
       sn += q * p1[(size_t)f * T + t];
       sd += q * p2[(size_t)f * T + t];
@@ -98,6 +106,25 @@ __global__ void k_dp_vmu(const R* __restrict__ u, R* __restrict__ v, const R* __
     for (int k = 0; k < 8; ++k) {
       a += red[0][k][threadIdx.x];
       c += red[1][k][threadIdx.x];
+    }
+    part[(((size_t)b * VMU_FS + fs) * 2) * T + t] = a;
+    part[(((size_t)b * VMU_FS + fs) * 2 + 1) * T + t] = c;
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0 && w == 0) {
+    unsigned* c = cnt + (size_t)b * gridDim.x + blockIdx.x;
+    last = atomicAdd(c, 1u) == (unsigned)(VMU_FS - 1);
+    if (last) *c = 0u;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  if (w == 0 && t < T) {
+    R a = 0, c = 0;
+    for (int q = 0; q < VMU_FS; ++q) {
+      a += __ldcg(part + (((size_t)b * VMU_FS + q) * 2) * T + t);
+      c += __ldcg(part + (((size_t)b * VMU_FS + q) * 2 + 1) * T + t);
     }
     v[(size_t)b * T + t] *= mu_factor(a, c);
   }

@@ -104,7 +104,8 @@ struct Plan {
   int TR, nseg;  // k_gain (and k_vacc/k_vacc_tc) frames per CTA segment, segments per bin
   int VTR, vnseg;  // V accumulation segments (k_ip reduces vnseg partials per bin)
   size_t off_lam, off_phi, off_gpart, off_vpart, off_gnew, off_llp, off_ldp, off_cs, off_hpart;
-  size_t off_cnt, off_hcnt, total;
+  size_t off_vmu;  // FastMNMF-DP V-step split partials (B, VMU_FS, 2, T)
+  size_t off_cnt, off_hcnt, off_vcnt, total;
 };
 
 // complex64 V accumulation: 0 register-blocked SIMT (k_vacc_blk, M >= 8),
@@ -177,8 +178,10 @@ inline Plan make_plan(const fm_dims* d) {
   p.off_ldp = o; o = align256(o + (size_t)B * F * 8);
   p.off_cs = o; o = align256(o + (size_t)B * F * NMAX * rs);
   p.off_hpart = o; o = align256(o + (size_t)htiles * p.HS * 2 * 64 * 64 * rs);
+  p.off_vmu = o; o = align256(o + (size_t)B * VMU_FS * 2 * T * rs);
   p.off_cnt = o; o = align256(o + 64);
   p.off_hcnt = o; o = align256(o + (size_t)htiles * 4);
+  p.off_vcnt = o; o = align256(o + (size_t)B * ((T + 31) / 32) * 4);  // k_dp_vmu tile counters
   p.total = o;
   return p;
 }
@@ -699,8 +702,9 @@ int Impl<R>::iterate_dp(const fm_dims* d, const fm_state* s, const fm_dp* p, cud
   if (int rc = dp_lambda(d, s, p, st)) return rc;
   // V step (sources.py:262-265)
   if (int rc = phi_pass(d, s, st)) return rc;
-  launch_pdl(k_dp_vmu<R>, dim3((unsigned)((T + 31) / 32), (unsigned)B), dim3(32, 8), 0, st,
-             (const R*)u, v, r, (const R*)phi, N, F, T);
+  launch_pdl(k_dp_vmu<R>, dim3((unsigned)((T + 31) / 32), (unsigned)VMU_FS, (unsigned)B), dim3(32, 8), 0,
+             st, (const R*)u, v, r, (const R*)phi, N, F, T, reinterpret_cast<R*>(w + pl.off_vmu),
+             reinterpret_cast<unsigned*>(w + pl.off_vcnt));
   FM_CHECK_LAUNCH("k_dp_vmu");
   if (int rc = dp_lambda(d, s, p, st)) return rc;
   // W step (noise NMF, sources.py:253 -> 191-194)
