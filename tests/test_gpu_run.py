@@ -210,3 +210,22 @@ def test_results_own_their_pinned_images():
     np.testing.assert_array_equal(ra.images_NFTM, keep)
     assert not np.shares_memory(ra.images_NFTM, rc.images_NFTM)
     assert rel(rc.images_NFTM.sum(axis=0), Xb) < 1e-5
+
+
+@pytest.mark.parametrize("precision", ["complex128", "complex64"])
+def test_observation_validation(precision):
+    """separate.py:285-291: shape, non-finite and all-zero observations raise
+    InvalidInputError with the reference's messages (checked on the device
+    statistics, before any iteration)."""
+    from paper_1903_03237_b200 import InvalidInputError, SeparatorConfig, run
+    cfg = SeparatorConfig(method="fast-mnmf", n_sources=2, n_basis=2, n_iterations=2,
+                          precision=precision)
+    X = np.ones((4, 16, 2), complex)
+    with pytest.raises(InvalidInputError, match="shape"):
+        run(cfg, X[0])
+    bad = X.copy()
+    bad[1, 3, 0] = np.nan
+    with pytest.raises(InvalidInputError, match="non-finite"):
+        run(cfg, bad)
+    with pytest.raises(InvalidInputError, match="identically zero"):
+        run(cfg, np.zeros_like(X))
