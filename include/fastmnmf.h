@@ -182,7 +182,8 @@ int fm_nmf_lambda(const fm_dims* d, const void* W, const void* H, void* lam, voi
  * the first statistics pass of iteration 0 (separate.py:183, :186-193). */
 int fm_prologue(const fm_dims* d, const fm_state* s, void* stream);
 
-/* One full iteration (separate.py:201-234) on one process: nine launches. Appends
+/* One full iteration (separate.py:201-234) on one process: ten launches (nine
+ * compute kernels and the trace entry; B > 1 adds the counter advance). Appends
  * trace[i] (i = number of previous fm_iterate calls since fm_prologue) =
  * data term + 2T sum_f log|det Q_f| of the state after this iteration. */
 int fm_iterate(const fm_dims* d, const fm_state* s, void* stream);
