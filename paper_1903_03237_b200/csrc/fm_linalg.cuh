@@ -191,6 +191,46 @@ __device__ bool warp_inv_hpd(double2* A, int lane) {
   return true;
 }
 
+// warp_inv_hpd in fp32 (complex64 mode, M <= 8): the V_fm it inverts were
+// accumulated in fp32, and the fp32 pipe (2x the fp64 rate, 4-cycle FMA
+// latency) keeps the parallel inversion phase of k_ip off the fp64 pipe that
+// all resident CTAs enter together. Same algorithm and selects as above.
+template <int M>
+__device__ bool warp_inv_hpd_f32(float2* A, int lane) {
+  constexpr int NE = (M * M + 31) / 32;
+  for (int k = 0; k < M; ++k) {
+    const float2 p = A[k * M + k];
+    if (!(p.x > 0.0f) || !isfinite(p.x)) return false;
+    const float inv = 1.0f / (p.x * p.x + p.y * p.y);
+    const float2 rp = make_float2(p.x * inv, -p.y * inv);
+    float2 nv[NE];
+#pragma unroll
+    for (int r = 0; r < NE; ++r) {
+      const int e = lane + 32 * r;
+      if (e < M * M) {
+        const int i = e / M, j = e % M;
+        const float2 aik = A[i * M + k], akj = A[k * M + j], aij = A[e];
+        const float2 akjr = make_float2(akj.x * rp.x - akj.y * rp.y, akj.x * rp.y + akj.y * rp.x);
+        const float2 aikr = make_float2(aik.x * rp.x - aik.y * rp.y, aik.x * rp.y + aik.y * rp.x);
+        const float2 other = make_float2(aij.x - (aik.x * akjr.x - aik.y * akjr.y),
+                                         aij.y - (aik.x * akjr.y + aik.y * akjr.x));
+        const bool rk = i == k, ck = j == k;
+        float2 v = rk ? akjr : other;
+        v = ck ? (rk ? rp : make_float2(-aikr.x, -aikr.y)) : v;
+        nv[r] = v;
+      }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int r = 0; r < NE; ++r) {
+      const int e = lane + 32 * r;
+      if (e < M * M) A[e] = nv[r];
+    }
+    __syncwarp();
+  }
+  return true;
+}
+
 // Gauss-Jordan with partial pivoting (izamax-style first max |re|+|im|) on
 // the augmented [Q | I] (M x 2M, row-major) by one warp; on success the
 // right half holds Q^-1 and *logabs = sum_k log|pivot_k| = log|det Q|

@@ -483,7 +483,40 @@ __global__ void __launch_bounds__(IpCfg<M>::BS) k_ip(IpArgs<R> a) {
       }
     }
     for (int m = warp - 1; warp > 0 && m < M; m += NW - 1) {
-      const bool ok = warp_inv_hpd<M>(Vd + (size_t)m * M * M, lane);
+      double2* Vm = Vd + (size_t)m * M * M;
+      bool ok;
+      if constexpr (sizeof(R) == 4 && M <= 8) {  // complex64: invert in fp32 in place
+        constexpr int NE = (M * M + 31) / 32;
+        float2 tv[NE];
+#pragma unroll
+        for (int r = 0; r < NE; ++r) {
+          const int e = lane + 32 * r;
+          if (e < M * M) tv[r] = make_float2((float)Vm[e].x, (float)Vm[e].y);
+        }
+        __syncwarp();
+        float2* Vf = reinterpret_cast<float2*>(Vm);
+#pragma unroll
+        for (int r = 0; r < NE; ++r) {
+          const int e = lane + 32 * r;
+          if (e < M * M) Vf[e] = tv[r];
+        }
+        __syncwarp();
+        ok = warp_inv_hpd_f32<M>(Vf, lane);
+#pragma unroll
+        for (int r = 0; r < NE; ++r) {
+          const int e = lane + 32 * r;
+          if (e < M * M) tv[r] = Vf[e];
+        }
+        __syncwarp();
+#pragma unroll
+        for (int r = 0; r < NE; ++r) {
+          const int e = lane + 32 * r;
+          if (e < M * M) Vm[e] = make_double2((double)tv[r].x, (double)tv[r].y);
+        }
+        __syncwarp();
+      } else {
+        ok = warp_inv_hpd<M>(Vm, lane);
+      }
       if (lane == 0) vfail[m] = ok ? 0 : 1;
     }
     __syncthreads();
