@@ -178,6 +178,12 @@ int fm_run_dp(const fm_dims* d, const fm_state* s, const fm_dp* p, int n_iterati
 /* NmfSource.lam (sources.py:184-187): lam (B,N,F,T) = W (B,N,F,K) H (B,N,K,T). */
 int fm_nmf_lambda(const fm_dims* d, const void* W, const void* H, void* lam, void* stream);
 
+/* Data term sum(-x~/y - log y) of the current state per mixture (B values,
+ * host), i.e. what the first statistics pass of the next iteration returns
+ * (_DiagLoop._refresh, separate.py:186-193; _kernels.py:233). Valid after
+ * fm_prologue / any full iteration. Synchronises `stream`. */
+int fm_data_term(const fm_dims* d, const fm_state* s, double* out_host, void* stream);
+
 /* Zero counters; compute lambda = W H and the projected power xt = |Q X|^2 and
  * the first statistics pass of iteration 0 (separate.py:183, :186-193). */
 int fm_prologue(const fm_dims* d, const fm_state* s, void* stream);

@@ -291,8 +291,109 @@ def save_fullrank(name="fullrank.npz"):
           flush=True)
 
 
+def _compact(res, st, N, step_f, step_t):
+    """Golden record of a full-shape run: state, trace, a strided image
+    sample, per-source image norms and per-(n, m) image energies."""
+    img = res.images_NFTM
+    return dict(
+        trace=res.likelihood_trace, W=st["W"].astype(np.float32), H=st["H"].astype(np.float32),
+        g=st["g"].astype(np.float32), Q=st["Q"].astype(np.complex64),
+        floor=np.float64(st["floor"]),
+        img_norm=np.linalg.norm(img.reshape(N, -1), axis=1),
+        img_energy=np.einsum("nftm,nftm->nm", img, np.conj(img)).real,
+        img_sample=img[:, ::step_f, ::step_t, :].astype(np.complex64))
+
+
+def save_full_c2(n_mix=8):
+    """BASELINE config 2 at full shape: mixtures b = 0..n_mix-1 of the batch,
+    each (513, 512, 4, 3, 8) with seed base + b (base 0), complex64-rounded,
+    100 iterations, each through an unmodified reference run()."""
+    from paper_1903_03237_b200.synth import make_mixture_fast
+    F, T, M, N, K_, it = 513, 512, 4, 3, 8, 100
+    out = dict(shape=np.array([F, T, M, N, K_, 0, it, n_mix]))
+    for b in range(n_mix):
+        X = make_mixture_fast(F, T, M, N, K_, seed=b).astype(np.complex128)
+        res, st, dt = run_injected(X, *baseline_init(F, T, M, N, K_, b), it)
+        for k, v in _compact(res, st, N, 17, 19).items():
+            out[f"b{b}_{k}"] = v
+        out[f"b{b}_X_abs_sum"] = np.float64(np.abs(X).sum())
+        print(f"c2 mixture {b}: {dt:.1f}s LL {res.likelihood_trace[-1]:.6f}", flush=True)
+    np.savez_compressed(os.path.join(OUT, "run_c2_full.npz"), **out)
+
+
+def save_full_c3(n_iter=4):
+    """BASELINE config 3 at full shape (F=1025, T=8192, M=16, N=6, K=32),
+    complex64-rounded mixture, seed 0, n_iter iterations of an unmodified
+    reference run() (~70 s per iteration on the build host)."""
+    from paper_1903_03237_b200.synth import make_mixture_fast
+    F, T, M, N, K_ = 1025, 8192, 16, 6, 32
+    t0 = time.perf_counter()
+    X = make_mixture_fast(F, T, M, N, K_, seed=0).astype(np.complex128)
+    print(f"c3 mixture generated in {time.perf_counter() - t0:.1f}s", flush=True)
+    res, st, dt = run_injected(X, *baseline_init(F, T, M, N, K_, 0), n_iter)
+    d = _compact(res, st, N, 64, 97)
+    d.update(shape=np.array([F, T, M, N, K_, 0, n_iter]), X_abs_sum=np.float64(np.abs(X).sum()),
+             X_sample=X[::64, ::97, :].astype(np.complex64))
+    np.savez_compressed(os.path.join(OUT, "run_c3_full.npz"), **d)
+    print(f"c3: {n_iter} it in {dt:.1f}s LL {res.likelihood_trace[0]:.6f} -> "
+          f"{res.likelihood_trace[-1]:.6f}", flush=True)
+
+
+def save_full_c4(n_iter=100, adam_steps=10, seed=0):
+    """BASELINE config 4 at full shape (F=513, T=512, M=8, N=2, noise K=32,
+    exp-MLP decoder D=16 -> 128 -> 128 -> F, 10 Adam steps per iteration,
+    100 iterations): the unmodified reference loop with the Adam hook at
+    update_latents_fast (as save_dp), images as a sample plus norms."""
+    from oracle.fastmnmf_dp_oracle import AdamLatents, ExpMLPDecoder, dp_init, make_dp_mixture
+    F, T, M, K_ = 513, 512, 8, 32
+    dec = ExpMLPDecoder(F, seed=seed)
+    X = make_dp_mixture(F, T, M, K_, dec, seed=seed).astype(np.complex64).astype(np.complex128)
+    Q0, g0, u0, v0, z0, W0, H0 = dp_init(F, T, M, K_, dec.latent_dim, seed)
+    hook = AdamLatents(adam_steps)
+    orig = (S._build_spatial, S._build_source, SRC.update_latents_fast)
+    S._build_spatial = lambda cfg, Xs: SP.DiagSpatial(Q0.copy(), g0.copy())
+    S._build_source = lambda cfg, Xs, rng: SRC.DeepPriorPlusNmfSource(
+        SRC.DeepPriorFactors(u0.copy(), v0.copy(), z0.copy()), SRC.NmfSource(W0.copy(), H0.copy()),
+        dec)
+    SRC.update_latents_fast = hook
+    st = {}
+
+    def snap(it, loop):
+        src = loop.source
+        st.update(u=src.dp.u_F.copy(), v=src.dp.v_T.copy(), z=src.dp.z_TD.copy(),
+                  W=src.noise.W_NFK.copy(), H=src.noise.H_NKT.copy(),
+                  g=loop.spatial.g_NFM.copy(), Q=loop.spatial.Q_FMM.copy())
+
+    t0 = time.perf_counter()
+    try:
+        cfg = fastsep.SeparatorConfig(method="fast-mnmf-dp", n_sources=2, n_basis=K_,
+                                      n_iterations=n_iter, seed=0, decoder=dec,
+                                      metropolis_enabled=True)
+        res = fastsep.run(cfg, X, on_iteration=snap)
+    finally:
+        S._build_spatial, S._build_source, SRC.update_latents_fast = orig
+    img = res.images_NFTM
+    np.savez_compressed(
+        os.path.join(OUT, "run_c4_full.npz"), shape=np.array([F, T, M, K_, seed, n_iter, adam_steps]),
+        trace=res.likelihood_trace, img_norm=np.linalg.norm(img.reshape(2, -1), axis=1),
+        img_sample=img[:, ::17, ::19, :].astype(np.complex64), X_abs_sum=np.float64(np.abs(X).sum()),
+        **{k: (v.astype(np.complex64) if np.iscomplexobj(v) else v.astype(np.float32))
+           for k, v in st.items()})
+    print(f"c4: {n_iter} it in {time.perf_counter() - t0:.1f}s LL {res.likelihood_trace[0]:.6f} -> "
+          f"{res.likelihood_trace[-1]:.6f}", flush=True)
+
+
 def main():
     os.makedirs(OUT, exist_ok=True)
+    if "--full-c2" in sys.argv:
+        save_full_c2()
+        return
+    if "--full-c3" in sys.argv:
+        save_full_c3()
+        return
+    if "--full-c4" in sys.argv:
+        save_full_c4()
+        return
     if "--fullrank-only" in sys.argv:
         save_fullrank()
         return

@@ -84,6 +84,7 @@ SIGNATURES = [
     ("fm_wiener_fast", ctypes.c_int,
      [ctypes.c_int, _c_i64, _c_i64, _c_i64, _c_i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     ("fm_nmf_lambda", ctypes.c_int, [ctypes.POINTER(FmDims), _vp, _vp, _vp, _vp]),
+    ("fm_data_term", ctypes.c_int, [ctypes.POINTER(FmDims), ctypes.POINTER(FmState), _dp, _vp]),
     ("fm_dp_workspace_bytes", ctypes.c_size_t, [ctypes.POINTER(FmDims), ctypes.POINTER(FmDp)]),
     ("fm_prologue_dp", ctypes.c_int,
      [ctypes.POINTER(FmDims), ctypes.POINTER(FmState), ctypes.POINTER(FmDp), _vp]),

@@ -36,16 +36,24 @@ static int check_m(int64_t M) {
   return FM_OK;
 }
 
-// One cached CUDA graph of a full iteration (launch-bound configs).
-struct GraphCache {
+// Cached CUDA graphs of one full iteration (launch-bound configs), keyed by
+// the device, the kernel selection (variant_key: V kernel, segment knob) and
+// the exact (dims, state[, dp]) they were captured for. One capture stream
+// per device. A small LRU keeps a few problems alive at once.
+struct GraphEntry {
+  int dev = -1;
+  unsigned variant = 0;
+  bool dp = false;
   fm_dims d;
   fm_state s;
   fm_dp p;
   cudaGraphExec_t exec = nullptr;
-  cudaStream_t cap = nullptr;
-  bool valid = false;
+  unsigned long long used = 0;
 };
-static GraphCache g_graph, g_graph_dp;
+constexpr int GRAPH_SLOTS = 8, MAX_DEV = 64;
+static GraphEntry g_graphs[GRAPH_SLOTS];
+static cudaStream_t g_cap[MAX_DEV];
+static unsigned long long g_tick = 0;
 static std::mutex g_graph_mu;
 
 }  // namespace fm
@@ -166,6 +174,24 @@ int fm_wiener_fast(int dtype, int64_t N, int64_t F, int64_t T, int64_t M, const 
   return FM_BY_DTYPE(dtype, wiener(N, F, T, M, lam, Q, g, X, images, status, (cudaStream_t)stream));
 }
 
+int fm_data_term(const fm_dims* d, const fm_state* s, double* out_host, void* stream) {
+  if (int rc = validate_dims(d)) return rc;
+  if (!s || !out_host) { set_error("null state or output"); return FM_EINVAL; }
+  const Plan p = make_plan(d);
+  const size_t n = (size_t)d->B * d->F * p.ntile;
+  std::vector<double> h(n);
+  FM_CUDA(cudaMemcpyAsync(h.data(), reinterpret_cast<unsigned char*>(s->work) + p.off_llp,
+                          n * sizeof(double), cudaMemcpyDeviceToHost, (cudaStream_t)stream));
+  FM_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+  const size_t per = (size_t)d->F * p.ntile;
+  for (int64_t b = 0; b < d->B; ++b) {  // fixed order: bins, then tiles
+    double acc = 0.0;
+    for (size_t e = 0; e < per; ++e) acc += h[(size_t)b * per + e];
+    out_host[b] = acc;
+  }
+  return FM_OK;
+}
+
 size_t fm_workspace_bytes(const fm_dims* d) {
   if (validate_dims(d)) return 0;
   return make_plan(d).total;
@@ -271,10 +297,9 @@ int fm_iterate_dp(const fm_dims* d, const fm_state* s, const fm_dp* p, void* str
   return FM_BY_DTYPE(d->dtype, iterate_dp(d, s, p, (cudaStream_t)stream));
 }
 
-// n iterations, optionally from one captured CUDA graph of a single iteration
-// (cached on the exact (dims, state[, dp]) it was captured for).
-static int run_common(GraphCache& c, const fm_dims* d, const fm_state* s, const fm_dp* p,
-                      int n_iterations, int use_graph, void* stream) {
+// n iterations, optionally from one captured CUDA graph of a single iteration.
+static int run_common(const fm_dims* d, const fm_state* s, const fm_dp* p, int n_iterations,
+                      int use_graph, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   auto one = [&](void* strm) { return p ? fm_iterate_dp(d, s, p, strm) : fm_iterate(d, s, strm); };
   if (!use_graph) {
@@ -282,42 +307,63 @@ static int run_common(GraphCache& c, const fm_dims* d, const fm_state* s, const 
       if (int rc = one(stream)) return rc;
     return FM_OK;
   }
+  int dev = 0;
+  FM_CUDA(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= MAX_DEV) { set_error("device %d", dev); return FM_EINVAL; }
+  const unsigned variant = variant_key(d);
   std::lock_guard<std::mutex> lk(g_graph_mu);
-  const bool same = c.valid && std::memcmp(&c.d, d, sizeof(fm_dims)) == 0 &&
-                    std::memcmp(&c.s, s, sizeof(fm_state)) == 0 &&
-                    (!p || std::memcmp(&c.p, p, sizeof(fm_dp)) == 0);
-  if (!same) {
-    if (c.exec) { cudaGraphExecDestroy(c.exec); c.exec = nullptr; }
-    c.valid = false;
-    if (!c.cap) FM_CUDA(cudaStreamCreateWithFlags(&c.cap, cudaStreamNonBlocking));
+  GraphEntry* hit = nullptr;
+  for (auto& e : g_graphs) {
+    if (e.exec && e.dev == dev && e.variant == variant && e.dp == (p != nullptr) &&
+        std::memcmp(&e.d, d, sizeof(fm_dims)) == 0 && std::memcmp(&e.s, s, sizeof(fm_state)) == 0 &&
+        (!p || std::memcmp(&e.p, p, sizeof(fm_dp)) == 0)) {
+      hit = &e;
+      break;
+    }
+  }
+  if (!hit) {
+    hit = &g_graphs[0];  // empty slot, else the least recently used
+    for (auto& e : g_graphs) {
+      if (!e.exec) { hit = &e; break; }
+      if (e.used < hit->used) hit = &e;
+    }
+    if (hit->exec) { cudaGraphExecDestroy(hit->exec); hit->exec = nullptr; }
+    if (!g_cap[dev]) FM_CUDA(cudaStreamCreateWithFlags(&g_cap[dev], cudaStreamNonBlocking));
     cudaGraph_t graph = nullptr;
-    FM_CUDA(cudaStreamBeginCapture(c.cap, cudaStreamCaptureModeThreadLocal));
-    int rc = one((void*)c.cap);
-    cudaError_t ce = cudaStreamEndCapture(c.cap, &graph);
+    FM_CUDA(cudaStreamBeginCapture(g_cap[dev], cudaStreamCaptureModeThreadLocal));
+    int rc = one((void*)g_cap[dev]);
+    cudaError_t ce = cudaStreamEndCapture(g_cap[dev], &graph);
     if (rc) { if (graph) cudaGraphDestroy(graph); return rc; }
     if (ce != cudaSuccess) { set_error("graph capture: %s", cudaGetErrorString(ce)); return FM_ECUDA; }
-    ce = cudaGraphInstantiate(&c.exec, graph, 0);
+    ce = cudaGraphInstantiate(&hit->exec, graph, 0);
     cudaGraphDestroy(graph);
-    if (ce != cudaSuccess) { set_error("graph instantiate: %s", cudaGetErrorString(ce)); return FM_ECUDA; }
-    c.d = *d;
-    c.s = *s;
-    if (p) c.p = *p;
-    c.valid = true;
+    if (ce != cudaSuccess) {
+      hit->exec = nullptr;
+      set_error("graph instantiate: %s", cudaGetErrorString(ce));
+      return FM_ECUDA;
+    }
+    hit->dev = dev;
+    hit->variant = variant;
+    hit->dp = p != nullptr;
+    hit->d = *d;
+    hit->s = *s;
+    if (p) hit->p = *p;
   }
-  for (int i = 0; i < n_iterations; ++i) FM_CUDA(cudaGraphLaunch(c.exec, st));
+  hit->used = ++g_tick;
+  for (int i = 0; i < n_iterations; ++i) FM_CUDA(cudaGraphLaunch(hit->exec, st));
   return FM_OK;
 }
 
 int fm_run(const fm_dims* d, const fm_state* s, int n_iterations, int use_graph, void* stream) {
   if (int rc = validate_dims(d)) return rc;
-  return run_common(g_graph, d, s, nullptr, n_iterations, use_graph, stream);
+  return run_common(d, s, nullptr, n_iterations, use_graph, stream);
 }
 
 int fm_run_dp(const fm_dims* d, const fm_state* s, const fm_dp* p, int n_iterations, int use_graph,
               void* stream) {
   if (int rc = validate_dims(d)) return rc;
   if (int rc = validate_dp(d, p)) return rc;
-  return run_common(g_graph_dp, d, s, p, n_iterations, use_graph, stream);
+  return run_common(d, s, p, n_iterations, use_graph, stream);
 }
 
 int fm_observation_stats(const fm_dims* d, const void* X, double* sumsq_host, double* maxsq_host,

@@ -103,6 +103,7 @@ struct Plan {
   int HS, HFR;   // k_hstats bin splits and bins per split
   int TR, nseg;  // k_gain (and k_vacc/k_vacc_tc) frames per CTA segment, segments per bin
   int VTR, vnseg;  // V accumulation segments (k_ip reduces vnseg partials per bin)
+  int ntile;       // k_back frame tiles per bin (data-term partials per bin)
   size_t off_lam, off_phi, off_gpart, off_vpart, off_gnew, off_llp, off_ldp, off_cs, off_hpart;
   size_t off_vmu;  // FastMNMF-DP V-step split partials (B, VMU_FS, 2, T)
   size_t off_cnt, off_hcnt, off_vcnt, total;
@@ -123,12 +124,25 @@ inline int vacc_mode(const fm_dims* d) {
   return d->M > 8 ? 0 : 1;
 }
 
+// FM_GSEG: segment-count tuning knob (A/B runs); read at every plan
+inline int gseg_override() {
+  const char* e = getenv("FM_GSEG");
+  return e ? atoi(e) : 0;
+}
+
+// Everything outside fm_dims that changes which kernels an iteration
+// launches: part of the CUDA-graph cache key (fm_api.cu run_common).
+inline unsigned variant_key(const fm_dims* d) {
+  return (unsigned)vacc_mode(d) | ((unsigned)(gseg_override() & 0xffff) << 4);
+}
+
 inline Plan make_plan(const fm_dims* d) {
   Plan p;
   const size_t rs = d->dtype == FM_F64 ? 8 : 4;
   const long long B = d->B, F = d->F, T = d->T, N = d->N, M = d->M;
   const long long target = 2 * 148;  // >= 2 CTAs per SM
   // largest tile that still gives ~2 CTAs per SM
+  p.ntile = (int)((T + 255) / 256);
   p.FT = 32;
   while (p.FT > 8 && ((F + p.FT - 1) / p.FT) * B * N < target) p.FT /= 2;
   p.TT = 64;
@@ -143,10 +157,7 @@ inline Plan make_plan(const fm_dims* d) {
   // k_gain / k_vacc: segments per bin so that bins x segments >= ~4 CTAs per SM,
   // each segment a multiple of 256 frames (the fp32 chunk; 64/128 divide it)
   long long segs = std::max<long long>(1, (4 * 148 + F * B - 1) / (F * B));
-  static const int seg_override = [] {  // FM_GSEG: segment-count tuning knob (A/B runs)
-    const char* e = getenv("FM_GSEG");
-    return e ? atoi(e) : 0;
-  }();
+  const int seg_override = gseg_override();
   if (seg_override > 0) segs = seg_override;
   long long tr = (T + segs - 1) / segs;
   tr = ((tr + 255) / 256) * 256;
@@ -174,7 +185,7 @@ inline Plan make_plan(const fm_dims* d) {
   p.off_gpart = o; o = align256(o + gpart * rs);
   p.off_vpart = o; o = align256(o + vpart * rs);
   p.off_gnew = o; o = align256(o + (size_t)B * N * F * M * rs);
-  p.off_llp = o; o = align256(o + (size_t)B * F * ((T + 255) / 256) * 8);
+  p.off_llp = o; o = align256(o + (size_t)B * F * p.ntile * 8);
   p.off_ldp = o; o = align256(o + (size_t)B * F * 8);
   p.off_cs = o; o = align256(o + (size_t)B * F * NMAX * rs);
   p.off_hpart = o; o = align256(o + (size_t)htiles * p.HS * 2 * 64 * 64 * rs);

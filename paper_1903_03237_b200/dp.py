@@ -149,8 +149,13 @@ class DeviceDP:
         if self.mh_steps > 0 and mh_rng is not None:
             self.noise = torch.empty((self.mh_steps, B, T, D), device=device, dtype=real)
             self.unif = torch.empty((self.mh_steps, B, T), device=device, dtype=real)
-            self._stage = torch.empty((self.mh_steps * B * T * (D + 1),), dtype=real,
-                                      pin_memory=True)
+            # two pinned staging buffers, each guarded by the event of the copy
+            # that last read it (fill_draws must not overwrite a buffer whose
+            # host->device copy is still queued behind the GPU)
+            self._stage = [torch.empty((self.mh_steps * B * T * (D + 1),), dtype=real,
+                                       pin_memory=True) for _ in range(2)]
+            self._stage_ev = [None, None]
+            self._stage_i = 0
 
         def p(t):
             return None if t is None else _lib.ptr(t).value
@@ -183,8 +188,15 @@ class DeviceDP:
         for s in range(S):
             n[s] = self.mh_rng.standard_normal((T, D))
             u[s] = self.mh_rng.uniform(size=T)
-        st = self._stage
+        i = self._stage_i
+        self._stage_i ^= 1
+        if self._stage_ev[i] is not None:
+            self._stage_ev[i].synchronize()  # the copy that last read this buffer is done
+        st = self._stage[i]
         st[: S * T * D].copy_(torch.from_numpy(n.reshape(-1)))
         st[S * T * D:].copy_(torch.from_numpy(u.reshape(-1)))
         self.noise.view(-1).copy_(st[: S * T * D], non_blocking=True)
         self.unif.view(-1).copy_(st[S * T * D:], non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record()
+        self._stage_ev[i] = ev

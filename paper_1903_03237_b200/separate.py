@@ -122,7 +122,8 @@ def wiener_fast(lam_NFT, Q_FMM, g_NFM, X_FTM):
 # ---------------------------------------------------------------------------
 
 class _SpatialView:
-    """``loop.spatial`` surface (DiagSpatial, spatial.py:47-56): host copies."""
+    """``loop.spatial`` surface (DiagSpatial, spatial.py:47-56): host copies
+    on read; assignment uploads (the reference's iterate assigns them)."""
 
     def __init__(self, loop, b):
         self._loop, self._b = loop, b
@@ -131,9 +132,17 @@ class _SpatialView:
     def Q_FMM(self):
         return self._loop.Q[self._b].cpu().numpy().astype(np.complex128)
 
+    @Q_FMM.setter
+    def Q_FMM(self, v):
+        self._loop.Q[self._b].copy_(self._loop._as_dev(v, self._loop.Q.dtype))
+
     @property
     def g_NFM(self):
         return self._loop.g[self._b].cpu().numpy().astype(np.float64)
+
+    @g_NFM.setter
+    def g_NFM(self, v):
+        self._loop.g[self._b].copy_(self._loop._as_dev(v, self._loop.real))
 
     @property
     def n_sources(self):
@@ -141,7 +150,8 @@ class _SpatialView:
 
 
 class _SourceView:
-    """``loop.source`` surface (NmfSource, sources.py:167-204): host copies."""
+    """``loop.source`` surface (NmfSource, sources.py:167-204): host copies
+    on read; assignment uploads."""
 
     mu_steps = ("W", "H")
 
@@ -152,17 +162,54 @@ class _SourceView:
     def W_NFK(self):
         return self._loop.W[self._b].cpu().numpy().astype(np.float64)
 
+    @W_NFK.setter
+    def W_NFK(self, v):
+        self._loop.W[self._b].copy_(self._loop._as_dev(v, self._loop.real))
+
     @property
     def H_NKT(self):
         return self._loop.H[self._b].cpu().numpy().astype(np.float64)
+
+    @H_NKT.setter
+    def H_NKT(self, v):
+        self._loop.H[self._b].copy_(self._loop._as_dev(v, self._loop.real))
+
+    @property
+    def n_sources(self):
+        return self._loop.N
+
+    @property
+    def n_basis(self):
+        return self._loop.K
 
     def lam(self):
         return self._loop.lam_device()[self._b].cpu().numpy().astype(np.float64)
 
 
+def _on_device(fn):
+    """Run a DeviceLoop method with the loop's device current, so the kernels
+    launch on that device's current stream (SeparatorConfig.device)."""
+    import functools
+
+    @functools.wraps(fn)
+    def wrapped(self, *a, **kw):
+        with self.torch.cuda.device(self.device):
+            return fn(self, *a, **kw)
+
+    return wrapped
+
+
 class DeviceLoop:
     """The _DiagLoop (separate.py:175-243) over a batch of B mixtures held in
-    HBM. ``X`` is the SCALED observation (B,F,T,M) on the device.
+    HBM.
+
+    Device state: ``X_dev`` the SCALED observation (B,F,T,M), ``xt_dev`` the
+    projected power, ``Q``, ``g``, ``W``, ``H`` and ``floor_dev`` (B,).
+
+    The reference loop's own surface reads mixture 0 back to the host:
+    ``X`` (F,T,M) complex128, ``xt`` (F,T,M), ``floor`` (float),
+    ``spatial.Q_FMM/g_NFM``, ``source.W_NFK/H_NKT/lam()``, and
+    ``iterate(cfg, rng)``, ``loglik()``, ``logdet_term()``, ``images()``.
 
     Frequency sharding: ``f_offset`` is the global index of local bin 0 and
     ``hstat_allreduce`` (a callable on the packed (B,2,N,K,T) H statistics)
@@ -173,7 +220,15 @@ class DeviceLoop:
                  f_offset=0, hstat_allreduce=None, dp=None):
         torch = _torch()
         self.torch = torch
-        self.X = X
+        self.device = X.device
+        with torch.cuda.device(self.device):
+            self._init(X, Q, g, W, H, floor, normalize, ip_sweeps, n_trace, f_offset,
+                       hstat_allreduce, dp)
+
+    def _init(self, X, Q, g, W, H, floor, normalize, ip_sweeps, n_trace, f_offset,
+              hstat_allreduce, dp):
+        torch = self.torch
+        self.X_dev = X
         self.real = torch.float32 if X.dtype == torch.complex64 else torch.float64
         self.B, self.F, self.T, self.M = X.shape
         # FastMNMF-DP: (decoder, u, v, z, adam_steps, lr[, mh_steps, mh_var, mh_rng, mh_seed])
@@ -184,8 +239,8 @@ class DeviceLoop:
         self.g = g.to(dev, self.real).contiguous()
         self.W = W.to(dev, self.real).contiguous()
         self.H = H.to(dev, self.real).contiguous()
-        self.floor = floor.to(dev, self.real).contiguous()
-        self.xt = torch.empty((self.B, self.F, self.T, self.M), device=dev, dtype=self.real)
+        self.floor_dev = floor.to(dev, self.real).contiguous()
+        self.xt_dev = torch.empty((self.B, self.F, self.T, self.M), device=dev, dtype=self.real)
         self.n_trace = max(1, int(n_trace))
         self.trace = torch.zeros((self.n_trace, self.B), device=dev, dtype=torch.float64)
         self.status = torch.full((1,), -1, dtype=torch.int64, device=dev)
@@ -198,12 +253,13 @@ class DeviceLoop:
             raise InvalidInputError(f"unsupported problem: {lib.fm_last_error().decode()}")
         self.work = torch.empty((nbytes,), dtype=torch.uint8, device=dev)
         self.state = _lib.FmState(*[_lib.ptr(t).value for t in (
-            self.X, self.xt, self.Q, self.g, self.W, self.H, self.floor, self.trace,
+            self.X_dev, self.xt_dev, self.Q, self.g, self.W, self.H, self.floor_dev, self.trace,
             self.status, self.work)])
         self.hstat_allreduce = hstat_allreduce
         self.hstat = (torch.empty((self.B, 2, self.N, self.K, self.T), device=dev, dtype=self.real)
                       if hstat_allreduce is not None else None)
         self.iterations_done = 0
+        self._prologue_done = False
         self.dp = None
         if dp is not None:
             from .dp import DeviceDP
@@ -215,15 +271,90 @@ class DeviceLoop:
         self.spatial = _SpatialView(self, 0)
         self.source = _SourceView(self, 0)
 
-    # reference-facing attributes of _DiagLoop
+    def _as_dev(self, v, dtype):
+        t = self.torch
+        v = v if isinstance(v, t.Tensor) else t.from_numpy(np.ascontiguousarray(v))
+        return v.to(self.device, dtype)
+
+    # ---- the reference _DiagLoop surface (separate.py:175-243), mixture 0 ----
+    @property
+    def X(self):
+        """Scaled observation (F,T,M) complex128 on the host (separate.py:179)."""
+        return self.X_dev[0].cpu().numpy().astype(np.complex128)
+
+    @property
+    def xt(self):
+        """Projected power x~ (F,T,M) on the host (separate.py:183)."""
+        return self.xt_dev[0].cpu().numpy().astype(np.float64)
+
+    @property
+    def floor(self):
+        """Model-power floor (separate.py:182, spatial.py:64-66)."""
+        return float(self.floor_dev[0])
+
+    @_on_device
+    def data_term(self):
+        """sum(-x~/y - log y) of the current state, per mixture (B,): the
+        first statistics pass of the next iteration (_kernels.py:233)."""
+        out = (ctypes.c_double * self.B)()
+        _lib.check(_lib.load().fm_data_term(ctypes.byref(self.dims), ctypes.byref(self.state), out,
+                                            _lib.stream_ptr()), "fm_data_term")
+        return np.array(out[:])
+
+    @_on_device
+    def logdet_terms(self):
+        """2T sum_f log|det Q_f| per mixture (B,) (separate.py:236-238)."""
+        ld = K.logdet(self.Q.reshape(self.B * self.F, self.M, self.M))
+        return 2.0 * self.T * ld.reshape(self.B, self.F).double().sum(dim=1).cpu().numpy()
+
+    def logdet_term(self):
+        """separate.py:236-238 (mixture 0)."""
+        return float(self.logdet_terms()[0])
+
+    def loglik(self):
+        """loglik_fast of the current state (separate.py:195-199, spatial.py:233-241)."""
+        return float(self.data_term()[0]) + self.logdet_term()
+
+    def iterate(self, cfg=None, rng=None):
+        """One pass (separate.py:201-234): returns the data term of the first
+        statistics refresh, i.e. of the state before the pass. Raises the
+        reference's SingularMatrixError (without run()'s iteration prefix)."""
+        if self.iterations_done >= self.n_trace:
+            self._grow_trace(self.iterations_done + 1)
+        if not self._prologue_done:
+            self.prologue()
+        if rng is not None and self.dp is not None and self.dp.noise is not None:
+            self.dp.mh_rng = rng
+        ll = float(self.data_term()[0])
+        self.run(1, use_graph=bool(getattr(cfg, "use_graph", True)))
+        err = self.status_error(prefix=False)
+        if err is not None:
+            raise err
+        return ll
+
+    def _grow_trace(self, n):
+        torch = self.torch
+        t = torch.zeros((max(n, 2 * self.n_trace), self.B), device=self.device, dtype=torch.float64)
+        t[: self.n_trace] = self.trace
+        self.trace, self.n_trace = t, t.shape[0]
+        self.state.trace = _lib.ptr(self.trace).value
+
+    def images(self):
+        """separate.py:240-243: Wiener images (N,F,T,M) of mixture 0 in the
+        scaled domain, as numpy (run() multiplies by the scale)."""
+        img = self.images_batch([1.0] * self.B)[0]
+        return img.cpu().numpy()
+
+    # ---- batched device helpers ----
     @property
     def xt_FTM(self):
-        return self.xt[0]
+        return self.xt_dev[0]
 
+    @_on_device
     def lam_device(self):
         """lambda = W H of the current state (sources.py:184-187), (B,N,F,T)."""
         torch = self.torch
-        lam = torch.empty((self.B, self.N, self.F, self.T), device=self.X.device, dtype=self.real)
+        lam = torch.empty((self.B, self.N, self.F, self.T), device=self.device, dtype=self.real)
         lib = _lib.load()
         _lib.check(lib.fm_nmf_lambda(ctypes.byref(self.dims), _lib.ptr(self.W), _lib.ptr(self.H),
                                      _lib.ptr(lam), _lib.stream_ptr()), "fm_nmf_lambda")
@@ -231,7 +362,9 @@ class DeviceLoop:
             lam[:, 0] = self.dp.lam0()
         return lam
 
+    @_on_device
     def prologue(self):
+        self._prologue_done = True
         lib = _lib.load()
         if self.dp is not None:
             _lib.check(lib.fm_prologue_dp(ctypes.byref(self.dims), ctypes.byref(self.state),
@@ -241,6 +374,7 @@ class DeviceLoop:
         _lib.check(lib.fm_prologue(ctypes.byref(self.dims), ctypes.byref(self.state),
                                    _lib.stream_ptr()), "fm_prologue")
 
+    @_on_device
     def run(self, n, use_graph=False):
         lib = _lib.load()
         if self.iterations_done + n > self.n_trace:
@@ -269,21 +403,27 @@ class DeviceLoop:
                            "fm_iterate_phase(1)")
         self.iterations_done += n
 
-    def status_error(self):
-        """The first numerical failure as the reference's exception, or None."""
+    def status_error(self, prefix=True):
+        """The first numerical failure as the reference's exception, or None;
+        ``prefix`` adds run()'s "iteration {it}: " (separate.py:310-311)."""
         s = K.decode_status(self.status.item())
         if s is None:
             return None
         code, it, m, f = s
-        return SingularMatrixError(f"iteration {it}: {K.status_message(code, m, f)}")
+        msg = K.status_message(code, m, f)
+        return SingularMatrixError(f"iteration {it}: {msg}" if prefix else msg)
 
-    def images(self, scale):
-        """separate.py:240-243 + the scale-back of :323, per mixture."""
+    @_on_device
+    def images_batch(self, scale):
+        """separate.py:240-243 + the scale-back of :323, for every mixture:
+        one wiener_fast launch per mixture on the stream, no host sync."""
         lam = self.lam_device()
         out = []
         for b in range(self.B):
-            img = K.wiener_fast(lam[b], self.Q[b], self.g[b], self.X[b])
-            out.append(img * float(scale[b]))
+            img = K.wiener_fast(lam[b], self.Q[b], self.g[b], self.X_dev[b])
+            if float(scale[b]) != 1.0:
+                img.mul_(float(scale[b]))
+            out.append(img)
         return out
 
 
@@ -343,6 +483,8 @@ def _prepare_observation(X, cfg, torch):
     cdt = torch.complex64 if cfg.precision == "complex64" else torch.complex128
     if isinstance(X, torch.Tensor):
         Xd = X.to(device=cfg.device, dtype=cdt).contiguous()
+        if Xd.data_ptr() == X.data_ptr():  # never scale the caller's tensor in place
+            Xd = Xd.clone()
     else:  # host numpy: copy at its own width, convert on the device (non-finite values
         # surface in the device power statistics below)
         Xn = np.ascontiguousarray(np.asarray(X))
@@ -401,10 +543,16 @@ def run(cfg: SeparatorConfig, X_FTM, on_iteration=None, init=None) -> Separation
     ``init`` optionally injects the initial (Q_FMM, g_NFM, W_NFK, H_NKT) in
     the scaled domain -- where the reference's _build_spatial/_build_source
     place theirs; by default the reference's own init is used.
+    The input is never modified. Everything runs on ``cfg.device``.
     """
     cfg.validate()
     _check_method(cfg)
     torch = _torch()
+    with torch.cuda.device(torch.device(cfg.device)):
+        return _run(cfg, X_FTM, on_iteration, init, torch)
+
+
+def _run(cfg, X_FTM, on_iteration, init, torch):
     if not isinstance(X_FTM, torch.Tensor):
         Xn = np.asarray(X_FTM)
         if Xn.ndim != 3:
@@ -452,8 +600,6 @@ def run(cfg: SeparatorConfig, X_FTM, on_iteration=None, init=None) -> Separation
     loop = DeviceLoop(Xs, _as_batch(Q0, torch, 1), _as_batch(g0, torch, 1),
                       _as_batch(W0, torch, 1), _as_batch(H0, torch, 1), floor,
                       cfg.normalize, cfg.ip_sweeps, n_trace=cfg.n_iterations, dp=dp)
-    loop.X_FTM = Xs[0]
-    loop.floor_value = float(floor[0])
     loop.prologue()
     time_trace = []
     start = torch.cuda.Event(enable_timing=True)
@@ -478,7 +624,7 @@ def run(cfg: SeparatorConfig, X_FTM, on_iteration=None, init=None) -> Separation
         prev = e
     ll = loop.trace[:, 0].cpu().numpy().copy() if cfg.record_likelihood else np.zeros(0)
     # images at the run's precision (complex64 runs return complex64), in pinned host memory
-    images = _to_host(loop.images(scale)[0]).numpy()
+    images = _to_host(loop.images_batch(scale)[0]).numpy()
     res = SeparationResult(images_NFTM=images, likelihood_trace=np.asarray(ll),
                            time_trace=np.asarray(time_trace), method=cfg.method,
                            config=replace(cfg))
@@ -554,8 +700,14 @@ def run_batch(cfg: SeparatorConfig, X_BFTM, init, want_images=True) -> BatchSepa
     """B independent fast-mnmf runs in lock-step on one device (BASELINE
     config 2); equal to B separate ``run`` calls."""
     cfg.validate()
-    _check_method(cfg)
+    if cfg.method != "fast-mnmf":
+        raise InvalidInputError(f"run_batch runs method='fast-mnmf' only, got {cfg.method!r}")
     torch = _torch()
+    with torch.cuda.device(torch.device(cfg.device)):
+        return _run_batch(cfg, X_BFTM, init, want_images, torch)
+
+
+def _run_batch(cfg, X_BFTM, init, want_images, torch):
     Xs, scale, floor = _prepare_observation(X_BFTM, cfg, torch)
     Q0, g0, W0, H0 = init
     B = Xs.shape[0]
@@ -570,6 +722,7 @@ def run_batch(cfg: SeparatorConfig, X_BFTM, init, want_images=True) -> BatchSepa
     err = loop.status_error()
     if err is not None:
         raise err
-    imgs = torch.stack(loop.images(scale)) if want_images else None
-    return BatchSeparationResult(images_BNFTM=imgs, likelihood_trace=loop.trace.cpu().numpy().T,
+    imgs = torch.stack(loop.images_batch(scale)) if want_images else None
+    ll = loop.trace.cpu().numpy().T if cfg.record_likelihood else np.zeros((B, 0))
+    return BatchSeparationResult(images_BNFTM=imgs, likelihood_trace=ll,
                                  seconds=dt, config=replace(cfg), loop=loop)

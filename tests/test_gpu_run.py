@@ -116,8 +116,8 @@ def test_ip_invariant_along_run():
 
     def check(it, loop):
         lam = loop.source.lam()
-        y = np.maximum(np.einsum("nft,nfm->ftm", lam, loop.spatial.g_NFM), loop.floor_value)
-        Xs = loop.X_FTM.cpu().numpy()
+        y = np.maximum(np.einsum("nft,nfm->ftm", lam, loop.spatial.g_NFM), loop.floor)
+        Xs = loop.X
         V = O.ip_weights(Xs, y)
         Q = loop.spatial.Q_FMM
         for m in range(M):

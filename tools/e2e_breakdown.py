@@ -50,7 +50,7 @@ for rep in range(2):
     for _ in range(99):
         loop.run(1, use_graph=True)
     t = tick("iterations 2..100", t)
-    img = loop.images(scale)[0]
+    img = loop.images_batch(scale)[0]
     t = tick("images (device)", t)
     out = torch.empty(img.shape, dtype=img.dtype, pin_memory=True)
     t = tick("pinned alloc (host cache)", t)
