@@ -5,7 +5,7 @@ TF-bin*channel updates/s; roofline fraction; CPU baseline).
 Default workload (N=1): BASELINE config 1 -- one mixture, F=513, T=1024, M=8,
 N=4, K=16, complex64, 100 iterations. A *step* is one full fit: prologue +
 100 FastMNMF iterations over the device-resident mixture (CUDA-graph replays
-of the 5-kernel iteration). L2 (126 MB) is flushed between timed steps with a
+of the 6-launch iteration). L2 (126 MB) is flushed between timed steps with a
 256 MiB write; each step is bracketed by its own CUDA events.
 
 --gpus N under torchrun: config 1 is a single-mixture problem that does not
@@ -14,9 +14,10 @@ only"); ``--config c2`` shards the 256-mixture batch across ranks and
 ``--config c3`` shards the long recording by frequency with one NCCL
 all-reduce of the H statistics per iteration.
 
---impl reference: the CPU oracle (numpy restatement of the reference path,
-oracle/fastmnmf_oracle.py) on the host cores, rank 0 only, one iteration per
-step (bounded sample), same metric and units.
+--impl reference: the unmodified reference package (fastsep, pip-installed
+into baseline/_ref) on the host cores, rank 0 only, one iteration per step
+(bounded sample), same metric and units; config 4's Adam latent update has
+no reference implementation and runs the numpy restatement (oracle/).
 """
 
 import argparse
@@ -126,39 +127,106 @@ def make_problem(cfg, seed, torch, dev):
     return X, init
 
 
+REF_DIR = os.path.join(REPO, "baseline", "_ref")
+
+
+def _import_reference():
+    """The UNMODIFIED reference package (pip-installed into baseline/_ref; see
+    DESIGN.md "Reference arm"), its numba kernels cached outside the tree."""
+    if not os.path.isdir(os.path.join(REF_DIR, "fastsep")):
+        return None
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/fastsep_numba_cache")
+    sys.path.insert(0, REF_DIR)
+    import fastsep  # noqa: E402
+    from fastsep import separate as S, sources as SRC, spatial as SP  # noqa: E402
+
+    return fastsep, S, SRC, SP
+
+
 def run_reference(args, cfg, world, rank):
-    """--impl reference: the oracle on the host cores (bounded sample)."""
+    """--impl reference: the reference's own CPU implementation on the host
+    cores (rank 0 only). fastsep.run() from baseline/_ref with the BASELINE
+    init injected by the SURVEY §8(c) recipe (monkeypatched _build_spatial /
+    _build_source -- the iteration itself is the stock code path: numba
+    kernels, numpy/OpenBLAS on every host core). One step = one iteration
+    (the reference's own per-iteration time_trace); --warmup iterations
+    (numba JIT included) are discarded. Config 4 (Adam + exp-MLP decoder) has
+    no reference implementation: that arm runs the numpy restatement."""
     if rank != 0:
         return
-    from oracle.fastmnmf_oracle import run_fastmnmf
     from paper_1903_03237_b200.synth import baseline_init, make_mixture
 
     F, T, M, N, K = cfg["F"], cfg["T"], cfg["M"], cfg["N"], cfg["K"]
-    if cfg.get("dp"):  # FastMNMF-DP: Adam (c4) or the reference's Metropolis chain (c4mh)
-        from oracle import fastmnmf_dp_oracle as DO
+    ref = _import_reference()
+    n_it = args.warmup + args.steps
+    kind, dts = "reference", None
+    if cfg.get("dp") and not cfg.get("mh") or ref is None:
+        kind = "port"
+    if kind == "reference":
+        fastsep, S, SRC, SP = ref
+        orig = (S._build_spatial, S._build_source)
+        if cfg.get("dp"):  # c4mh: the reference's own ToyDecoder + Metropolis chain
+            from oracle.fastmnmf_dp_oracle import dp_init, make_dp_mixture
 
-        dec = DO.ToyDecoder(F) if cfg.get("mh") else DO.ExpMLPDecoder(F, seed=0)
-        X = DO.make_dp_mixture(F, T, M, K, dec, 0).astype(np.complex64).astype(np.complex128)
-        init = DO.dp_init(F, T, M, K, dec.latent_dim, 0)
-
-        def one():
-            hook = DO.MetropolisLatents(np.random.default_rng(0)) if cfg.get("mh") else None
-            DO.run_fastmnmf_dp(X, *init, dec, 1, adam_steps=0 if hook else 10, hook=hook,
-                               want_images=False)
+            dec = SRC.ToyDecoder(F)
+            X = make_dp_mixture(F, T, M, K, dec, 0).astype(np.complex64).astype(np.complex128)
+            Q0, g0, u0, v0, z0, W0, H0 = dp_init(F, T, M, K, dec.latent_dim, 0)
+            S._build_spatial = lambda c, Xs: SP.DiagSpatial(Q0.copy(), g0.copy())
+            S._build_source = lambda c, Xs, rng: SRC.DeepPriorPlusNmfSource(
+                SRC.DeepPriorFactors(u0.copy(), v0.copy(), z0.copy()),
+                SRC.NmfSource(W0.copy(), H0.copy()), dec)
+            rcfg = fastsep.SeparatorConfig(method="fast-mnmf-dp", n_sources=2, n_basis=K,
+                                           n_iterations=n_it, seed=0)
+        else:
+            X = make_mixture(F, T, M, N, K, 0)
+            if cfg["precision"] == "complex64":
+                X = X.astype(np.complex64).astype(np.complex128)
+            Q0, g0, W0, H0 = baseline_init(F, T, M, N, K, 0)
+            S._build_spatial = lambda c, Xs: SP.DiagSpatial(Q0.copy(), g0.copy())
+            S._build_source = lambda c, Xs, rng: SRC.NmfSource(W0.copy(), H0.copy())
+            rcfg = fastsep.SeparatorConfig(method="fast-mnmf", n_sources=N, n_basis=K,
+                                           n_iterations=n_it, seed=0)
+        try:
+            res = fastsep.run(rcfg, X)
+        finally:
+            S._build_spatial, S._build_source = orig
+        dts = np.asarray(res.time_trace, dtype=np.float64)[args.warmup:]
+        sample = (f"{args.steps} iterations of {args.config} after {args.warmup} warm-up (numba "
+                  "JIT included there), unmodified fastsep.run from baseline/_ref (numba kernels "
+                  "single-threaded, numpy/OpenBLAS on all host cores)")
     else:
-        X = make_mixture(F, T, M, N, K, 0)
-        if cfg["precision"] == "complex64":
-            X = X.astype(np.complex64).astype(np.complex128)
-        init = baseline_init(F, T, M, N, K, 0)
+        from oracle.fastmnmf_oracle import run_fastmnmf
 
-        def one():
-            run_fastmnmf(X, *init, n_iterations=1, want_images=False)
-    for _ in range(args.warmup):
-        one()
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        one()
-    dt = (time.perf_counter() - t0) / args.steps
+        if cfg.get("dp"):
+            from oracle import fastmnmf_dp_oracle as DO
+
+            dec = DO.ExpMLPDecoder(F, seed=0)
+            X = DO.make_dp_mixture(F, T, M, K, dec, 0).astype(np.complex64).astype(np.complex128)
+            init = DO.dp_init(F, T, M, K, dec.latent_dim, 0)
+
+            def one():
+                DO.run_fastmnmf_dp(X, *init, dec, 1, adam_steps=10, hook=None, want_images=False)
+        else:
+            X = make_mixture(F, T, M, N, K, 0)
+            if cfg["precision"] == "complex64":
+                X = X.astype(np.complex64).astype(np.complex128)
+            init = baseline_init(F, T, M, N, K, 0)
+
+            def one():
+                run_fastmnmf(X, *init, n_iterations=1, want_images=False)
+        for _ in range(args.warmup):
+            one()
+        dl = []
+        for _ in range(args.steps):
+            t0 = time.perf_counter()
+            one()
+            dl.append(time.perf_counter() - t0)
+        dts = np.asarray(dl)
+        sample = (f"{args.steps} single iterations of {args.config} after {args.warmup} warm-up, "
+                  "numpy restatement of the reference path (oracle/, fp64)"
+                  + ("; config 4's Adam/exp-MLP latent update has no reference implementation"
+                     if cfg.get("dp") else "; baseline/_ref missing"))
+    dt = float(np.mean(dts))
     value = F * T * M / dt
     cores = os.cpu_count()
     line = {
@@ -169,9 +237,8 @@ def run_reference(args, cfg, world, rank):
         "config": {"workload": f"{args.config}: F={F} T={T} M={M} N={N} K={K}, "
                                "one FastMNMF iteration per step (bounded CPU sample)"},
         "iters_per_s": 1.0 / dt,
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": f"{args.steps} single iterations of {args.config} after "
-                                   f"{args.warmup} warm-up, numpy oracle (fp64)"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
+                         "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -334,61 +401,97 @@ def main():
     value = units / (ms_per_step / 1e3)
     iters_per_s = iters / (ms_per_step / 1e3)
 
-    # ---- roofline of the dominant kernel: per-kernel CUDA events on the launch stream
-    names = ["k_wstats", "k_lambda(W)", "k_phi", "k_hstats", "k_lambda(H)", "k_gain", "k_vacc",
-             "k_ip", "k_back"]
-    acc = np.zeros(9)
-    nprof = 10
-    if not sharded_f and loop.dp is None:
-        ms = (ctypes.c_float * 9)()
-        for _ in range(nprof):
-            _lib.check(lib.fm_iterate_profiled(ctypes.byref(loop.dims), ctypes.byref(loop.state), ms,
-                                               _lib.stream_ptr()), "fm_iterate_profiled")
-            acc += np.array(ms[:])
-        acc /= nprof
-    dom = int(np.argmax(acc)) if acc.any() else len(names) - 1
+    # ---- roofline of the dominant kernel: per-kernel device times from CUDA
+    # event-record nodes between the launches of one graph-replayed iteration
+    # (the production path), median of nprof replays
     rs = 4 if cfg["precision"] == "complex64" else 8
     Bl = cfg["B"]
     ftm = F * T * M * Bl if not sharded_f else (loop.F * T * M)
-    # algorithmic bytes per launch
-    alg = {
-        "k_gain": ftm * rs + N * (ftm // M) * rs,          # read xt, lambda
-        "k_vacc": ftm * 2 * rs + N * (ftm // M) * rs,      # read X, lambda
-        "k_back": ftm * (2 * rs + rs) + 3 * N * (ftm // M) * rs,  # read X, lambda; write xt, phi
-        "k_hstats": 2 * N * (ftm // M) * rs,               # read phi1, phi2
-        "k_wstats": 2 * N * (ftm // M) * rs,               # read phi1, phi2
-        "k_phi": ftm * rs + 3 * N * (ftm // M) * rs,       # read xt, lambda; write phi
-        "k_lambda(W)": N * (ftm // M) * rs,                # write lambda
-        "k_lambda(H)": N * (ftm // M) * rs,
-        "k_ip": 0,
-    }[names[dom]]
+    nprof = 10
+    if loop.dp is None:
+        names = ["k_hpass", "k_gpass", "k_vacc", "k_ip", "k_bpass", "k_trace"]
+        samples = []
+        if not sharded_f:
+            ms = (ctypes.c_float * 6)()
+            for _ in range(nprof):
+                reset()
+                loop.prologue()
+                _lib.check(lib.fm_iterate_profiled(ctypes.byref(loop.dims), ctypes.byref(loop.state),
+                                                   ms, _lib.stream_ptr()), "fm_iterate_profiled")
+                samples.append(list(ms[:]))
+    else:
+        lat = "k_dp_mh" if cfg.get("mh") else "k_dp_latent"
+        names = ["k_lambda", "k_dp_lambda", lat, "k_dp_lambda", "k_phi", "k_dp_umu", "k_dp_lambda",
+                 "k_phi", "k_dp_vmu", "k_dp_lambda", "k_phi", "k_wstats", "k_lambda", "k_phi",
+                 "k_hstats", "k_lambda", "k_gain", "k_vacc", "k_ip", "k_back", "k_trace"]
+        samples = []
+        ms = (ctypes.c_float * 24)()
+        nint = ctypes.c_int(0)
+        for _ in range(nprof):
+            reset()
+            loop.prologue()
+            _lib.check(lib.fm_iterate_dp_profiled(ctypes.byref(loop.dims), ctypes.byref(loop.state),
+                                                  ctypes.byref(loop.dp.struct), ms, ctypes.byref(nint),
+                                                  _lib.stream_ptr()), "fm_iterate_dp_profiled")
+            samples.append(list(ms[:nint.value]))
+    kernel_ms = {}
+    if samples:
+        med = np.median(np.array(samples), axis=0)
+        for n_, v in zip(names, med):  # launches of the same kernel summed per iteration
+            kernel_ms[n_] = kernel_ms.get(n_, 0.0) + float(v)
+    dom = max(kernel_ms, key=kernel_ms.get) if kernel_ms else None
+    launches_of = {n_: names.count(n_) for n_ in kernel_ms}
+    # algorithmic bytes per launch: x~ reads (P1-P3), X reads
+    # (P4, P5) and the x~ write (P5); lambda / phi / y are on-chip by definition
+    FT = ftm // M
+    alg_tab = {
+        "k_hpass": ftm * rs,                  # read x~ (H step)
+        "k_gpass": ftm * rs,                  # read x~ (gain step)
+        "k_vacc": ftm * 2 * rs,               # read X (V accumulation)
+        "k_bpass": ftm * 3 * rs,              # read X, write x~ (projection + next W step)
+        "k_back": ftm * 3 * rs,               # deep prior: read X, write x~
+        "k_phi": ftm * rs, "k_gain": ftm * rs,
+        "k_dp_latent": ftm * rs + FT * rs,    # x~ and y_rest (F,T) per Adam step
+        "k_dp_mh": ftm * rs + FT * rs,
+    }
     hbm, peak_kind = peaks()
-    achieved = alg / (acc[dom] / 1e3) / 1e9 if acc[dom] > 0 else None
-    traffic = None
-    tpath = os.path.join(REPO, "profiles", "traffic.json")
-    if os.path.exists(tpath):
-        traffic = json.load(open(tpath)).get(f"{args.config}:{names[dom]}")
-    roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                "frac": (achieved / hbm) if achieved else None, "traffic": traffic,
-                "kernel": names[dom], "peak_kind": peak_kind,
-                "kernel_ms": {n: float(v) for n, v in zip(names, acc)},
-                "step_share": float(acc[dom] * iters / ms_per_step) if ms_per_step else None,
-                "alg_bytes_per_launch": alg}
-    if names[dom] == "k_vacc" and acc[dom] > 0:
-        # the V accumulation is FP32-pipe bound, not HBM bound: its
-        # compute roofline beside the contract's HBM one. Algorithmic flops per
-        # (f, t): P = M(M+1)/2 Hermitian pairs x M weights x 4 (real x complex
-        # FMA) + 6 per pair product + the model power (2NM) and M reciprocals
-        P = M * (M + 1) // 2
-        flops = (4 * P * M + 6 * P + 2 * N * M + M) * (ftm // M)
-        peak_sm = float(json.load(open(os.path.join(REPO, "MEASURED_PEAKS.json")))["sm_max_mhz"]) \
-            if os.path.exists(os.path.join(REPO, "MEASURED_PEAKS.json")) else 1965.0
-        fp32_peak = 148 * 128 * 2 * peak_sm * 1e6 / 1e12  # TFLOP/s (FFMA, all SMs, max clock)
-        ach = flops / (acc[dom] / 1e3) / 1e12
-        roofline["compute"] = {"bound": "fp32-fma", "achieved": ach, "peak": fp32_peak,
-                               "unit": "TFLOP/s", "frac": ach / fp32_peak,
-                               "alg_flops_per_launch": flops,
-                               "peak_kind": "nominal 148 SM x 128 FP32 lanes x 2 x max SM clock"}
+    roofline = {"bound": "hbm", "achieved": None, "peak": hbm, "unit": "GB/s", "frac": None,
+                "traffic": None, "kernel": dom, "peak_kind": peak_kind,
+                "kernel_ms": kernel_ms, "kernel_ms_source": "graph replay, event nodes, median of "
+                f"{nprof}" if kernel_ms else None}
+    if dom is not None:
+        per_launch_ms = kernel_ms[dom] / launches_of[dom]
+        alg = alg_tab.get(dom, 0)
+        achieved = alg / (per_launch_ms / 1e3) / 1e9 if alg and per_launch_ms > 0 else None
+        traffic = None
+        tpath = os.path.join(REPO, "profiles", "traffic.json")
+        if os.path.exists(tpath):
+            traffic = json.load(open(tpath)).get(f"{args.config}:{dom}")
+        roofline.update(achieved=achieved, frac=(achieved / hbm) if achieved else None,
+                        traffic=traffic, alg_bytes_per_launch=alg,
+                        step_share=float(kernel_ms[dom] * iters / ms_per_step))
+        if dom == "k_vacc":
+            # the V accumulation is FP32-pipe bound at M >= 8: its
+            # compute roofline beside the contract's HBM one. Algorithmic flops
+            # per (f, t): M weights x P = M(M+1)/2 Hermitian pairs x 2 FMA (real
+            # weight x complex product) + 3 FMA per pair product + the model
+            # power (N M FMA), all x 2 flop/FMA
+            P = M * (M + 1) // 2
+            flops = 2 * (2 * P * M + 3 * P + N * M) * FT
+            peak_sm = float(json.load(open(os.path.join(REPO, "MEASURED_PEAKS.json")))["sm_max_mhz"]) \
+                if os.path.exists(os.path.join(REPO, "MEASURED_PEAKS.json")) else 1965.0
+            fp32_peak = 148 * 128 * 2 * peak_sm * 1e6 / 1e12  # TFLOP/s (FFMA, all SMs, max clock)
+            ach = flops / (per_launch_ms / 1e3) / 1e12
+            roofline["compute"] = {"bound": "fp32-fma", "achieved": ach, "peak": fp32_peak,
+                                   "unit": "TFLOP/s", "frac": ach / fp32_peak,
+                                   "alg_flops_per_launch": flops,
+                                   "peak_kind": "nominal 148 SM x 128 FP32 lanes x 2 x max SM clock"}
+    # whole iteration against B_it = (4 b_r + 2 b_c) F T M per mixture
+    b_it = 8 * rs * (F * T * M * (B_total if args.config == "c2" else Bl))
+    it_s = ms_per_step / 1e3 / iters
+    roofline["iteration"] = {"B_it": b_it, "ms": it_s * 1e3, "achieved": b_it / it_s / 1e9,
+                             "frac": b_it / it_s / 1e9 / hbm,
+                             "kernel_ms_sum": float(sum(kernel_ms.values())) if kernel_ms else None}
 
     # ---- e2e: the public API call with host buffers (pinned), copies inside the timed region
     e2e = None
@@ -438,9 +541,13 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline and args.config in ("c1", "c0"):
         cpu = cpu_baseline_sample(cfg)
 
-    launches = args.steps * (2 + (10 if cfg['B'] == 1 else 11) * iters)
-    if cfg.get("dp"):  # 21 per iteration (one latent-hook launch: Adam or Metropolis), 4 in the prologue
-        launches = args.steps * (4 + 21 * iters)
+    # per iteration: k_hpass, k_gpass, k_vacc, k_ip, k_bpass, k_trace (+ the
+    # counter advance when B > 1); the prologue is k_hstore + k_bpass
+    launches = args.steps * (2 + (6 if cfg['B'] == 1 else 7) * iters)
+    if sharded_f:  # + k_hstore (H MU + Ht) after the all-reduce
+        launches = args.steps * (2 + 7 * iters)
+    if cfg.get("dp"):  # 21 per iteration (one latent-hook launch: Adam or Metropolis), 5 in the prologue
+        launches = args.steps * (5 + 21 * iters)
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,

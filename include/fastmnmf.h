@@ -117,8 +117,10 @@ typedef struct fm_state {
   void* work;     /* fm_workspace_bytes() bytes, 256-B aligned */
 } fm_state;
 
-/* Workspace: lambda (B,N,F,T), phi (B,2,N,F,T), H-statistic partials, bin
- * partials of the log-likelihood, counters. */
+/* Workspace: lambda (B,N,F,T) (written once per iteration for the V pass),
+ * the W of the coming H step (B,N,F,K), segment partials of the gain, V, W
+ * and H statistics and of the log-likelihood, counters; the deep-prior path
+ * also phi (B,2,N,F,T). */
 size_t fm_workspace_bytes(const fm_dims* d);
 
 /* ---- FastMNMF-DP (BASELINE config 4) ------------------------------------ */
@@ -184,29 +186,46 @@ int fm_nmf_lambda(const fm_dims* d, const void* W, const void* H, void* lam, voi
  * fm_prologue / any full iteration. Synchronises `stream`. */
 int fm_data_term(const fm_dims* d, const fm_state* s, double* out_host, void* stream);
 
-/* Zero counters; compute lambda = W H and the projected power xt = |Q X|^2 and
- * the first statistics pass of iteration 0 (separate.py:183, :186-193). */
+/* Zero counters; the projected power xt = |Q X|^2, the data term of the
+ * initial state and iteration 0's W step (separate.py:183, :186-193, :214-216)
+ * -- one k_bpass launch. */
 int fm_prologue(const fm_dims* d, const fm_state* s, void* stream);
 
-/* One full iteration (separate.py:201-234) on one process: ten launches (nine
- * compute kernels and the trace entry; B > 1 adds the counter advance). Appends
+/* fm_prologue without the counter reset: re-derives xt, the transposed H and
+ * the coming W step from the current state after the caller changed Q, g, W
+ * or H between iterations (the reference loop's attributes are plain
+ * assignable arrays, separate.py:178-184); the trace index continues. */
+int fm_refresh(const fm_dims* d, const fm_state* s, void* stream);
+
+/* One full iteration (separate.py:201-234) on one process: six launches
+ * (k_hpass, k_gpass, k_vacc, k_ip, k_bpass and the trace entry; B > 1 adds the
+ * counter advance); the W step of the NEXT iteration runs inside k_bpass, so
+ * the state W after a call is the reference's post-absorb W. Appends
  * trace[i] (i = number of previous fm_iterate calls since fm_prologue) =
  * data term + 2T sum_f log|det Q_f| of the state after this iteration. */
 int fm_iterate(const fm_dims* d, const fm_state* s, void* stream);
 
 /* Frequency-sharded iteration, split around the one exchange step: phase 0
- * runs the W update and the H statistics of this shard and leaves the packed
+ * runs the H statistics of this shard (its W step ran in the previous k_bpass) and leaves the packed
  * [num_H | den_H] (B,2,N,K,T) sums in *hstat (device, caller-sized); the
  * caller all-reduces it (sum) across shards; phase 1 applies the H update
  * from *hstat and runs the per-frequency rest of the iteration. */
 int fm_iterate_phase(const fm_dims* d, const fm_state* s, int phase, void* hstat,
                      void* stream);
 
-/* fm_iterate with CUDA events recorded between its nine launches on `stream`
- * (synchronises): ms_host[0..8] = device ms of k_wstats, k_lambda, k_phi,
- * k_hstats, k_lambda, k_gain, k_vacc, k_ip, k_back. Used by bench.py for the
- * per-kernel roofline. */
+/* One fm_iterate captured into a CUDA graph with event-record nodes between
+ * its launches and replayed once on `stream` (synchronises): ms_host[0..5] =
+ * device ms of k_hpass, k_gpass, k_vacc, k_ip, k_bpass, k_trace as they run
+ * inside a graph replay. Used by bench.py for the per-kernel roofline. */
 int fm_iterate_profiled(const fm_dims* d, const fm_state* s, float* ms_host, void* stream);
+
+/* The same for one fm_iterate_dp: ms_host (>= 21 floats) receives the device
+ * ms of each launch in order (k_lambda, k_dp_lambda, [latent hook, k_dp_lambda,]
+ * k_phi, k_dp_umu, k_dp_lambda, k_phi, k_dp_vmu, k_dp_lambda, k_phi, k_wstats,
+ * k_lambda, k_phi, k_hstats, k_lambda, k_gain, k_vacc, k_ip, k_back,
+ * k_trace); *n_intervals their count (21 with a latent hook, else 19). */
+int fm_iterate_dp_profiled(const fm_dims* d, const fm_state* s, const fm_dp* p, float* ms_host,
+                           int* n_intervals, void* stream);
 
 /* n fm_iterate calls, optionally captured once into a CUDA graph that is
  * replayed (launch-bound configs). */

@@ -95,6 +95,7 @@ SIGNATURES = [
       ctypes.c_int, _vp]),
     ("fm_workspace_bytes", ctypes.c_size_t, [ctypes.POINTER(FmDims)]),
     ("fm_prologue", ctypes.c_int, [ctypes.POINTER(FmDims), ctypes.POINTER(FmState), _vp]),
+    ("fm_refresh", ctypes.c_int, [ctypes.POINTER(FmDims), ctypes.POINTER(FmState), _vp]),
     ("fm_iterate", ctypes.c_int, [ctypes.POINTER(FmDims), ctypes.POINTER(FmState), _vp]),
     ("fm_iterate_phase", ctypes.c_int,
      [ctypes.POINTER(FmDims), ctypes.POINTER(FmState), ctypes.c_int, _vp, _vp]),
@@ -102,6 +103,9 @@ SIGNATURES = [
      [ctypes.POINTER(FmDims), ctypes.POINTER(FmState), ctypes.POINTER(ctypes.c_float), _vp]),
     ("fm_run", ctypes.c_int,
      [ctypes.POINTER(FmDims), ctypes.POINTER(FmState), ctypes.c_int, ctypes.c_int, _vp]),
+    ("fm_iterate_dp_profiled", ctypes.c_int,
+     [ctypes.POINTER(FmDims), ctypes.POINTER(FmState), ctypes.POINTER(FmDp),
+      ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_int), _vp]),
     ("fm_observation_stats", ctypes.c_int, [ctypes.POINTER(FmDims), _vp, _dp, _dp, _vp]),
     ("fm_scale_observation", ctypes.c_int, [ctypes.POINTER(FmDims), _vp, _dp, _vp]),
     ("fm_spatial_init", ctypes.c_int, [ctypes.POINTER(FmDims), _vp, _vp, _vp, _vp]),

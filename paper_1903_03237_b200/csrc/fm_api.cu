@@ -178,12 +178,14 @@ int fm_data_term(const fm_dims* d, const fm_state* s, double* out_host, void* st
   if (int rc = validate_dims(d)) return rc;
   if (!s || !out_host) { set_error("null state or output"); return FM_EINVAL; }
   const Plan p = make_plan(d);
-  const size_t n = (size_t)d->B * d->F * p.ntile;
+  // data-term partials per mixture: (F, ntile) from k_back (deep prior),
+  // (nfb, bseg) from k_bpass
+  const size_t per = d->dp ? (size_t)d->F * p.ntile : (size_t)p.nfb * p.bseg;
+  const size_t n = (size_t)d->B * per;
   std::vector<double> h(n);
   FM_CUDA(cudaMemcpyAsync(h.data(), reinterpret_cast<unsigned char*>(s->work) + p.off_llp,
                           n * sizeof(double), cudaMemcpyDeviceToHost, (cudaStream_t)stream));
   FM_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
-  const size_t per = (size_t)d->F * p.ntile;
   for (int64_t b = 0; b < d->B; ++b) {  // fixed order: bins, then tiles
     double acc = 0.0;
     for (size_t e = 0; e < per; ++e) acc += h[(size_t)b * per + e];
@@ -211,6 +213,12 @@ int fm_prologue(const fm_dims* d, const fm_state* s, void* stream) {
   return FM_BY_DTYPE(d->dtype, prologue(d, s, (cudaStream_t)stream));
 }
 
+int fm_refresh(const fm_dims* d, const fm_state* s, void* stream) {
+  if (int rc = validate_dims(d)) return rc;
+  if (d->dp) { set_error("dims.dp set: use fm_prologue_dp"); return FM_EINVAL; }
+  return FM_BY_DTYPE(d->dtype, prologue(d, s, (cudaStream_t)stream, false));
+}
+
 int fm_iterate(const fm_dims* d, const fm_state* s, void* stream) {
   if (int rc = validate_dims(d)) return rc;
   if (d->dp) { set_error("dims.dp set: use fm_iterate_dp"); return FM_EINVAL; }
@@ -224,17 +232,43 @@ int fm_iterate_phase(const fm_dims* d, const fm_state* s, int phase, void* hstat
 }
 
 int fm_iterate_profiled(const fm_dims* d, const fm_state* s, float* ms_host, void* stream) {
+  // One iteration captured into a CUDA graph with external event-record
+  // nodes between its launches, replayed once: ms_host[0..5] = device ms of
+  // k_hpass, k_gpass, k_vacc, k_ip, k_bpass, k_trace as they run inside a
+  // graph replay (the production path), not as separately synchronised
+  // eager launches.
   if (int rc = validate_dims(d)) return rc;
+  if (d->dp) { set_error("fm_iterate_profiled: plain FastMNMF only"); return FM_EINVAL; }
   cudaStream_t st = (cudaStream_t)stream;
-  cudaEvent_t ev[10];
-  for (int i = 0; i < 10; ++i) FM_CUDA(cudaEventCreate(&ev[i]));
-  int rc = d->dtype == FM_F64 ? Impl<double>::iterate_phase(d, s, 2, nullptr, st, ev)
-                              : Impl<float>::iterate_phase(d, s, 2, nullptr, st, ev);
-  if (rc == FM_OK) {
-    FM_CUDA(cudaEventSynchronize(ev[9]));
-    for (int i = 0; i < 9; ++i) FM_CUDA(cudaEventElapsedTime(&ms_host[i], ev[i], ev[i + 1]));
+  constexpr int NEV = 7;
+  cudaEvent_t ev[NEV];
+  for (int i = 0; i < NEV; ++i) FM_CUDA(cudaEventCreate(&ev[i]));
+  cudaStream_t cap = nullptr;
+  FM_CUDA(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  int rc = FM_OK;
+  FM_CUDA(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
+  rc = d->dtype == FM_F64 ? Impl<double>::iterate_phase(d, s, 2, nullptr, cap, ev)
+                          : Impl<float>::iterate_phase(d, s, 2, nullptr, cap, ev);
+  cudaError_t ce = cudaStreamEndCapture(cap, &graph);
+  if (rc == FM_OK && ce != cudaSuccess) {
+    set_error("profiled capture: %s", cudaGetErrorString(ce));
+    rc = FM_ECUDA;
   }
-  for (int i = 0; i < 10; ++i) cudaEventDestroy(ev[i]);
+  if (rc == FM_OK && cudaGraphInstantiate(&exec, graph, 0) != cudaSuccess) {
+    set_error("profiled instantiate failed");
+    rc = FM_ECUDA;
+  }
+  if (rc == FM_OK) {
+    FM_CUDA(cudaGraphLaunch(exec, st));
+    FM_CUDA(cudaStreamSynchronize(st));
+    for (int i = 0; i + 1 < NEV; ++i) FM_CUDA(cudaEventElapsedTime(&ms_host[i], ev[i], ev[i + 1]));
+  }
+  if (exec) cudaGraphExecDestroy(exec);
+  if (graph) cudaGraphDestroy(graph);
+  cudaStreamDestroy(cap);
+  for (int i = 0; i < NEV; ++i) cudaEventDestroy(ev[i]);
   return rc;
 }
 
@@ -295,6 +329,51 @@ int fm_iterate_dp(const fm_dims* d, const fm_state* s, const fm_dp* p, void* str
   if (int rc = validate_dims(d)) return rc;
   if (int rc = validate_dp(d, p)) return rc;
   return FM_BY_DTYPE(d->dtype, iterate_dp(d, s, p, (cudaStream_t)stream));
+}
+
+static int dp_profiled(const fm_dims* d, const fm_state* s, const fm_dp* p, float* ms_host,
+                       int* n_out, cudaStream_t st) {
+  constexpr int NEV = 24;
+  cudaEvent_t ev[NEV];
+  for (int i = 0; i < NEV; ++i) FM_CUDA(cudaEventCreate(&ev[i]));
+  cudaStream_t cap = nullptr;
+  FM_CUDA(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  FM_CUDA(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
+  int rc = d->dtype == FM_F64 ? Impl<double>::iterate_dp(d, s, p, cap, ev)
+                              : Impl<float>::iterate_dp(d, s, p, cap, ev);
+  cudaError_t ce = cudaStreamEndCapture(cap, &graph);
+  if (rc == FM_OK && ce != cudaSuccess) {
+    set_error("profiled capture: %s", cudaGetErrorString(ce));
+    rc = FM_ECUDA;
+  }
+  if (rc == FM_OK && cudaGraphInstantiate(&exec, graph, 0) != cudaSuccess) {
+    set_error("profiled instantiate failed");
+    rc = FM_ECUDA;
+  }
+  int nint = 0;
+  if (rc == FM_OK) {
+    FM_CUDA(cudaGraphLaunch(exec, st));
+    FM_CUDA(cudaStreamSynchronize(st));
+    const int nlaunch = 19 + ((p->mh_steps > 0 || p->adam_steps > 0) ? 2 : 0);
+    for (int i = 0; i < nlaunch; ++i) FM_CUDA(cudaEventElapsedTime(&ms_host[i], ev[i], ev[i + 1]));
+    nint = nlaunch;
+  }
+  if (exec) cudaGraphExecDestroy(exec);
+  if (graph) cudaGraphDestroy(graph);
+  cudaStreamDestroy(cap);
+  for (int i = 0; i < NEV; ++i) cudaEventDestroy(ev[i]);
+  *n_out = nint;
+  return rc;
+}
+
+int fm_iterate_dp_profiled(const fm_dims* d, const fm_state* s, const fm_dp* p, float* ms_host,
+                           int* n_intervals, void* stream) {
+  if (int rc = validate_dims(d)) return rc;
+  if (int rc = validate_dp(d, p)) return rc;
+  if (!ms_host || !n_intervals) { set_error("null output"); return FM_EINVAL; }
+  return dp_profiled(d, s, p, ms_host, n_intervals, (cudaStream_t)stream);
 }
 
 // n iterations, optionally from one captured CUDA graph of a single iteration.

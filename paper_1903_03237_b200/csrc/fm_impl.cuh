@@ -22,6 +22,7 @@
 #include "fm_init.cuh"
 #include "fm_stft.cuh"
 #include "fm_fullrank.cuh"
+#include "fm_fused.cuh"
 
 namespace fm {
 
@@ -76,6 +77,18 @@ void set_error(const char* fmt, ...);
   else if ((Krt) <= 64) { constexpr int KB = 64; __VA_ARGS__; }                        \
   else { set_error("K=%d outside the supported 1..64", (int)(Krt)); return FM_EINVAL; }
 
+// padded channel count of the fused statistics passes (fm_fused.cuh)
+#define FM_DISPATCH_MP(Mrt, ...)                                               \
+  if ((Mrt) <= 4) { constexpr int MP = 4; __VA_ARGS__; }                               \
+  else if ((Mrt) <= 8) { constexpr int MP = 8; __VA_ARGS__; }                          \
+  else { constexpr int MP = 16; __VA_ARGS__; }
+
+#define FM_DISPATCH_IT(ITrt, ...)                                              \
+  if ((ITrt) <= 1) { constexpr int IT = 1; __VA_ARGS__; }                              \
+  else if ((ITrt) <= 2) { constexpr int IT = 2; __VA_ARGS__; }                         \
+  else if ((ITrt) <= 4) { constexpr int IT = 4; __VA_ARGS__; }                         \
+  else { constexpr int IT = 8; __VA_ARGS__; }
+
 inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 // Launch with programmatic stream serialisation (PDL): the kernel may begin
@@ -106,7 +119,16 @@ struct Plan {
   int ntile;       // k_back frame tiles per bin (data-term partials per bin)
   size_t off_lam, off_phi, off_gpart, off_vpart, off_gnew, off_llp, off_ldp, off_cs, off_hpart;
   size_t off_vmu;  // FastMNMF-DP V-step split partials (B, VMU_FS, 2, T)
-  size_t off_cnt, off_hcnt, off_vcnt, total;
+  // fused statistics passes (plain FastMNMF; fm_fused.cuh)
+  int FB, nfb;            // bins per CTA, bin blocks
+  int gTR, gseg;          // k_gpass frames per segment, segments
+  int bTR, bseg, bIT;     // k_bpass frames per segment, segments, items per lane
+  int hHS, hHFR, hNS, hNG, hIT, htl;  // k_hpass bin splits, bins per split, sources per
+                                      // CTA, source groups, items per thread, T tiles
+  size_t smem_g, smem_b, smem_h;
+  int gS, bS, hS;  // cp.async pipeline stages of k_gpass, k_bpass, k_hpass
+  size_t off_wn, off_wpart, off_hpart2, off_ht;
+  size_t off_cnt, off_hcnt, off_vcnt, off_bcnt, off_hcnt2, total;
 };
 
 // complex64 V accumulation: 0 register-blocked SIMT (k_vacc_blk, M >= 8),
@@ -179,20 +201,92 @@ inline Plan make_plan(const fm_dims* d) {
     p.vnseg = (int)((T + vtr - 1) / vtr);
   }
   const size_t vpart = (size_t)B * F * p.vnseg * M * (M * (M + 1) / 2) * 2;
+  // ---- fused passes: bins per CTA (8 warps; fewer where fp64 rows overflow
+  // shared memory), segments for >= ~3 CTAs per SM
+  {
+    const int K = (int)d->K, K4 = k4_of(K), KQ = K4 / 4;
+    const int MPv = M <= 4 ? 4 : M <= 8 ? 8 : 16;
+    p.bIT = N * KQ <= 32 ? 1 : (int)((N * KQ + 31) / 32);
+    p.bIT = p.bIT <= 1 ? 1 : p.bIT <= 2 ? 2 : 4;
+    p.FB = 8;
+    auto fit = [&](int FB, int& NS, int& NG, int& IT) {
+      NG = 1;
+      NS = (int)N;
+      IT = (NS * KQ + FB - 1) / FB;
+      while (IT > 8) {
+        ++NG;
+        NS = (int)((N + NG - 1) / NG);
+        IT = (NS * KQ + FB - 1) / FB;
+      }
+      IT = IT <= 1 ? 1 : IT <= 2 ? 2 : IT <= 4 ? 4 : 8;
+      // cp.async stages: the deepest of 4..2 that keeps two CTAs per SM
+      // (<= 112 KB), else the deepest that fits one
+      auto pick = [&](auto total_of, int& S, size_t& bytes) {
+        for (int pass = 0; pass < 2; ++pass) {
+          const size_t cap = pass == 0 ? (size_t)112 * 1024 : (size_t)200 * 1024;
+          for (S = 4; S >= 2; --S) {
+            bytes = total_of(S);
+            if (bytes <= cap) return true;
+          }
+        }
+        S = 2;
+        bytes = total_of(2);
+        return false;
+      };
+      bool ok = pick([&](int S) { return GpLayout((int)rs, (int)N, K, (int)M, MPv, FB, S).total; },
+                     p.gS, p.smem_g);
+      ok = pick([&](int S) { return BpLayout((int)rs, (int)N, K, (int)M, MPv, FB, p.bIT, S).total; },
+                p.bS, p.smem_b) && ok;
+      ok = pick([&](int S) { return HpLayout((int)rs, (int)N, K, (int)M, MPv, FB, NS, S).total; },
+                p.hS, p.smem_h) && ok;
+      return ok;
+    };
+    while (p.FB > 1 && !fit(p.FB, p.hNS, p.hNG, p.hIT)) p.FB /= 2;
+    fit(p.FB, p.hNS, p.hNG, p.hIT);
+    p.nfb = (int)((F + p.FB - 1) / p.FB);
+    const long long want = 3 * 148, chunks = (T + FTC - 1) / FTC;
+    auto segs_for = [&](long long ctas, int& TRo, int& nsego) {
+      long long sg = std::max<long long>(1, (want + ctas - 1) / ctas);
+      sg = std::min(sg, chunks);
+      long long tr = (chunks + sg - 1) / sg * FTC;
+      TRo = (int)tr;
+      nsego = (int)((T + tr - 1) / tr);
+    };
+    segs_for((long long)p.nfb * B, p.gTR, p.gseg);
+    segs_for((long long)p.nfb * B, p.bTR, p.bseg);
+    p.htl = (int)chunks;
+    const long long hct = chunks * B * p.hNG;
+    long long hs = std::max<long long>(1, (want + hct - 1) / hct);
+    hs = std::min<long long>(hs, p.nfb);
+    p.hHFR = (int)(((F + hs - 1) / hs + p.FB - 1) / p.FB * p.FB);
+    p.hHS = (int)((F + p.hHFR - 1) / p.hHFR);
+  }
+  const size_t gpart_f = (size_t)B * F * p.gseg * N * 2 * M;
   size_t o = 0;
   p.off_lam = o; o = align256(o + (size_t)B * N * F * T * rs);
   p.off_phi = o; o = align256(o + (size_t)B * 2 * N * F * T * rs);
-  p.off_gpart = o; o = align256(o + gpart * rs);
+  p.off_gpart = o; o = align256(o + std::max<size_t>(gpart, gpart_f) * rs);
   p.off_vpart = o; o = align256(o + vpart * rs);
   p.off_gnew = o; o = align256(o + (size_t)B * N * F * M * rs);
-  p.off_llp = o; o = align256(o + (size_t)B * F * p.ntile * 8);
+  p.off_llp = o; o = align256(o + std::max<size_t>((size_t)B * F * p.ntile, (size_t)B * p.nfb * p.bseg) * 8);
   p.off_ldp = o; o = align256(o + (size_t)B * F * 8);
   p.off_cs = o; o = align256(o + (size_t)B * F * NMAX * rs);
   p.off_hpart = o; o = align256(o + (size_t)htiles * p.HS * 2 * 64 * 64 * rs);
   p.off_vmu = o; o = align256(o + (size_t)B * VMU_FS * 2 * T * rs);
+  {
+    const size_t K4 = (size_t)k4_of((int)d->K);
+    p.off_wn = o; o = align256(o + (size_t)B * N * F * d->K * rs);
+    p.off_ht = o; o = align256(o + (size_t)B * N * T * K4 * rs);
+    p.off_wpart = o; o = align256(o + (size_t)B * F * p.bseg * 2 * N * K4 * rs);
+    p.off_hpart2 = o;
+    if (p.hHS > 1)
+      o = align256(o + (size_t)p.htl * B * p.hNG * p.hHS * 2 * p.hNS * K4 * FTC * rs);
+  }
   p.off_cnt = o; o = align256(o + 64);
   p.off_hcnt = o; o = align256(o + (size_t)htiles * 4);
   p.off_vcnt = o; o = align256(o + (size_t)B * ((T + 31) / 32) * 4);  // k_dp_vmu tile counters
+  p.off_bcnt = o; o = align256(o + (size_t)B * p.nfb * 4);
+  p.off_hcnt2 = o; o = align256(o + (size_t)p.htl * B * p.hNG * 4);
   p.total = o;
   return p;
 }
@@ -211,7 +305,7 @@ int validate_dims(const fm_dims* d);
 template <typename R> struct Impl {
   using C = cplx<R>;
 
-  static int prologue(const fm_dims* d, const fm_state* s, cudaStream_t st);
+  static int prologue(const fm_dims* d, const fm_state* s, cudaStream_t st, bool reset = true);
   static int iterate_phase(const fm_dims* d, const fm_state* s, int phase, void* hstat,
                            cudaStream_t st, cudaEvent_t* ev = nullptr);  // ev: 10 events
   static int lambda(const fm_dims* d, const R* W, const R* H, R* lam, cudaStream_t st);
@@ -224,8 +318,14 @@ template <typename R> struct Impl {
   static int dp_mh(const fm_dims* d, const fm_state* s, const fm_dp* p, int steps, cudaStream_t st);
   static int dp_lambda(const fm_dims* d, const fm_state* s, const fm_dp* p, cudaStream_t st);
   static int prologue_dp(const fm_dims* d, const fm_state* s, const fm_dp* p, cudaStream_t st);
-  static int iterate_dp(const fm_dims* d, const fm_state* s, const fm_dp* p, cudaStream_t st);
+  static int iterate_dp(const fm_dims* d, const fm_state* s, const fm_dp* p, cudaStream_t st,
+                        cudaEvent_t* ev = nullptr);  // ev: DP_NEV events
   static int back(const fm_dims* d, const fm_state* s, int tail_only, int record, cudaStream_t st);
+  static int hpass(const fm_dims* d, const fm_state* s, int mode, void* hout, cudaStream_t st);
+  static int gpass(const fm_dims* d, const fm_state* s, cudaStream_t st);
+  static int bpass(const fm_dims* d, const fm_state* s, cudaStream_t st);
+  static int trace(const fm_dims* d, const fm_state* s, cudaStream_t st);
+  static int hstore(const fm_dims* d, const fm_state* s, const void* hbuf, cudaStream_t st);
 
   static int fast_stats(int64_t F, int64_t T, int64_t M, int64_t N, const void* xt,
                         const void* g, const void* lam, double floor, int want_gain,
@@ -318,7 +418,8 @@ int Impl<R>::vacc(const fm_dims* d, const fm_state* s, cudaStream_t st) {
   a.floorp = reinterpret_cast<const R*>(s->floor);
   a.gnew = reinterpret_cast<R*>(w + p.off_gnew);
   a.part = reinterpret_cast<R*>(w + p.off_vpart);
-  a.F = (int)d->F; a.T = (int)d->T; a.N = (int)d->N; a.TR = p.TR; a.gseg = p.nseg;
+  a.F = (int)d->F; a.T = (int)d->T; a.N = (int)d->N; a.TR = p.TR;
+  a.gseg = d->dp ? p.nseg : p.gseg;  // k_gain (deep prior) or k_gpass partials
   static const int dbg = [] { const char* e = getenv("FM_VTC_DBG"); return e ? atoi(e) : 0; }();
   a.dbg = dbg;
   dim3 grid((unsigned)p.nseg, (unsigned)d->F, (unsigned)d->B);
@@ -363,6 +464,8 @@ int Impl<R>::ip(const fm_dims* d, const fm_state* s, cudaStream_t st, R* u) {
   a.Q = reinterpret_cast<C*>(s->Q);
   a.g = reinterpret_cast<R*>(s->g);
   a.W = reinterpret_cast<R*>(s->W);
+  // plain FastMNMF: the W-stepped Wn (k_bpass) is absorbed into the state W
+  a.Wsrc = d->dp ? a.W : reinterpret_cast<const R*>(w + p.off_wn);
   a.cs_out = reinterpret_cast<R*>(w + p.off_cs);
   a.ld_part = reinterpret_cast<double*>(w + p.off_ldp);
   a.iter = reinterpret_cast<const unsigned*>(w + p.off_cnt) + 1;
@@ -412,103 +515,74 @@ int Impl<R>::back(const fm_dims* d, const fm_state* s, int tail_only, int record
   return FM_OK;
 }
 
+// trace entry of the state after this iteration, then the device iteration
+// counter (k_trace; a separate advance when B > 1)
 template <typename R>
-int Impl<R>::prologue(const fm_dims* d, const fm_state* s, cudaStream_t st) {
+int Impl<R>::trace(const fm_dims* d, const fm_state* s, cudaStream_t st) {
   const Plan p = make_plan(d);
   unsigned char* w = reinterpret_cast<unsigned char*>(s->work);
-  FM_CUDA(cudaMemsetAsync(w + p.off_cnt, 0, p.total - p.off_cnt, st));
-  if (int rc = lambda(d, reinterpret_cast<const R*>(s->W), reinterpret_cast<const R*>(s->H),
-                      reinterpret_cast<R*>(w + p.off_lam), st))
-    return rc;
-  return back(d, s, /*tail_only=*/1, /*record=*/0, st);
+  unsigned* itp = reinterpret_cast<unsigned*>(w + p.off_cnt) + 1;
+  // data-term partials: (B, F, ntile) from k_back (deep prior), (B, nfb, bseg)
+  // from k_bpass
+  const int np1 = d->dp ? (int)d->F : p.nfb, np2 = d->dp ? p.ntile : p.bseg;
+  launch_pdl(k_trace, dim3((unsigned)d->B), dim3(256), 0, st,
+             reinterpret_cast<const double*>(w + p.off_llp),
+             reinterpret_cast<const double*>(w + p.off_ldp), s->trace, itp, (int)d->B, np1, np2,
+             (int)d->F, (int)d->T);
+  FM_CHECK_LAUNCH("k_trace");
+  if (d->B > 1) {
+    launch_pdl(k_iter_advance, dim3(1), dim3(1), 0, st, itp);
+    FM_CHECK_LAUNCH("k_iter_advance");
+  }
+  return FM_OK;
+}
+
+
+template <typename R>
+int Impl<R>::prologue(const fm_dims* d, const fm_state* s, cudaStream_t st, bool reset) {
+  const Plan p = make_plan(d);
+  unsigned char* w = reinterpret_cast<unsigned char*>(s->work);
+  if (reset) FM_CUDA(cudaMemsetAsync(w + p.off_cnt, 0, p.total - p.off_cnt, st));
+  // Ht from H, then x~ of the initial Q, the data term of the initial state
+  // and the first iteration's W step (separate.py:183, :186-193, :214-216)
+  if (int rc = hstore(d, s, nullptr, st)) return rc;
+  return bpass(d, s, st);
 }
 
 template <typename R>
 int Impl<R>::iterate_phase(const fm_dims* d, const fm_state* s, int phase, void* hstat,
                            cudaStream_t st, cudaEvent_t* ev) {
 #define FM_EV(i) \
-  if (ev) FM_CUDA(cudaEventRecord(ev[i], st));
-  const Plan p = make_plan(d);
-  unsigned char* w = reinterpret_cast<unsigned char*>(s->work);
-  R* lam = reinterpret_cast<R*>(w + p.off_lam);
-  R* phi = reinterpret_cast<R*>(w + p.off_phi);
-  R* W = reinterpret_cast<R*>(s->W);
-  R* H = reinterpret_cast<R*>(s->H);
-  const int N = (int)d->N, F = (int)d->F, T = (int)d->T, K = (int)d->K;
-  const int n0 = d->dp ? 1 : 0;
-  const unsigned BN = (unsigned)(d->B * (d->N - n0));
+  if (ev) FM_CUDA(cudaEventRecordWithFlags(ev[i], st, cudaEventRecordExternal));
+  // The plain FastMNMF iteration (separate.py:201-234) in five compute
+  // launches; its W step already ran in the previous k_bpass (or the
+  // prologue), leaving Wn:
+  //   k_hpass   H step: phi from lambda(Wn, H), H MU        (separate.py:214-216)
+  //   k_gpass   gain statistics from lambda(Wn, H_new)     (separate.py:217)
+  //   k_vacc    g MU + V_fm                                 (separate.py:218-222)
+  //   k_ip      IP rows, row/gain normalisation, W = Wn c   (separate.py:222-233)
+  //   k_bpass   x~ = |Qx|^2, data term, next W step -> Wn   (separate.py:230; :186-193)
+  //   k_trace   trace entry
+  if (d->dp) { set_error("deep-prior dims: use fm_iterate_dp"); return FM_EINVAL; }
+  FM_EV(0);
   if (phase == 0 || phase == 2) {
-    // W step (separate.py:214-216 with step "W"): statistics from the phi of the
-    // previous pass, MU, then the refresh with the new W (lambda + phi)
-    FM_EV(0);
-    FM_DISPATCH_KB(K, {
-      FM_DISPATCH_TILE(p.FT, FTT, {
-        if constexpr (FTT <= 32) {
-          const size_t smw = WsCfg<R, KB, FTT>::bytes;
-          if (int rc = ensure_smem(k_wstats<R, KB, FTT>, smw)) return rc;
-          launch_pdl(k_wstats<R, KB, FTT>, dim3((unsigned)((F + FTT - 1) / FTT), BN), dim3(256),
-                     smw, st, phi, H, W, N, F, T, K, 0);
-          FM_CHECK_LAUNCH("k_wstats");
-        }
-      });
-    });
-    FM_EV(1);
-    if (int rc = lambda(d, W, H, lam, st)) return rc;
-    FM_EV(2);
-    FM_DISPATCH_M(d->M, {
-      launch_pdl(k_phi<R, MM>, dim3((unsigned)((T + 255) / 256), (unsigned)F, (unsigned)d->B),
-                 dim3(256), 0, st, lam, reinterpret_cast<const R*>(s->xt),
-                 reinterpret_cast<const R*>(s->g), reinterpret_cast<const R*>(s->floor), phi, N, F,
-                 T);
-      FM_CHECK_LAUNCH("k_phi");
-    });
-    // H step (separate.py:214-216 with step "H")
-    FM_EV(3);
-    FM_DISPATCH_KB(K, {
-      FM_DISPATCH_TILE(p.TT, TTT, {
-        if constexpr (TTT >= 16) {
-          const size_t smh = HsCfg<R, KB, TTT>::bytes;
-          if (int rc = ensure_smem(k_hstats<R, KB, TTT>, smh)) return rc;
-          launch_pdl(k_hstats<R, KB, TTT>, dim3((unsigned)((T + TTT - 1) / TTT), BN, (unsigned)p.HS),
-                     dim3(256), smh, st, phi, W, H, reinterpret_cast<R*>(hstat), N, F, T, K,
-                     phase == 0 ? 1 : 0, 0, p.HFR, reinterpret_cast<R*>(w + p.off_hpart),
-                     reinterpret_cast<unsigned*>(w + p.off_hcnt));
-          FM_CHECK_LAUNCH("k_hstats");
-        }
-      });
-    });
+    if (int rc = hpass(d, s, phase == 0 ? 1 : 0, hstat, st)) return rc;
   }
   if (phase == 0) return FM_OK;
-  if (phase == 1) {
-    const long long NKT = (long long)N * K * T, total = (long long)d->B * NKT;
-    k_hupdate<R><<<(unsigned)((total + 255) / 256), 256, 0, st>>>(
-        nullptr, H, reinterpret_cast<R*>(hstat), 1, NKT, total, 2);
-    FM_CHECK_LAUNCH("k_hupdate");
+  if (phase == 1) {  // H MU from the all-reduced statistics, and Ht
+    if (int rc = hstore(d, s, hstat, st)) return rc;
   }
-  FM_EV(4);
-  if (int rc = lambda(d, W, H, lam, st)) return rc;
-  FM_EV(5);
-  if (int rc = gain(d, s, st)) return rc;
-  FM_EV(6);
+  FM_EV(1);
+  if (int rc = gpass(d, s, st)) return rc;
+  FM_EV(2);
   if (int rc = vacc(d, s, st)) return rc;
-  FM_EV(7);
+  FM_EV(3);
   if (int rc = ip(d, s, st)) return rc;
-  FM_EV(8);
-  if (int rc = back(d, s, /*tail_only=*/0, /*record=*/1, st)) return rc;
-  FM_EV(9);
-  {  // trace entry of this iteration, then advance the device iteration counter
-    const unsigned* cnt = reinterpret_cast<const unsigned*>(w + p.off_cnt);
-    unsigned* itp = const_cast<unsigned*>(cnt) + 1;
-    launch_pdl(k_trace, dim3((unsigned)d->B), dim3(256), 0, st,
-               reinterpret_cast<const double*>(w + p.off_llp),
-               reinterpret_cast<const double*>(w + p.off_ldp), s->trace, itp, (int)d->B, F,
-               (T + 255) / 256, T);
-    FM_CHECK_LAUNCH("k_trace");
-    if (d->B > 1) {
-      launch_pdl(k_iter_advance, dim3(1), dim3(1), 0, st, itp);
-      FM_CHECK_LAUNCH("k_iter_advance");
-    }
-  }
+  FM_EV(4);
+  if (int rc = bpass(d, s, st)) return rc;
+  FM_EV(5);
+  if (int rc = trace(d, s, st)) return rc;
+  FM_EV(6);
   return FM_OK;
 #undef FM_EV
 }
@@ -682,7 +756,11 @@ int Impl<R>::prologue_dp(const fm_dims* d, const fm_state* s, const fm_dp* p, cu
 }
 
 template <typename R>
-int Impl<R>::iterate_dp(const fm_dims* d, const fm_state* s, const fm_dp* p, cudaStream_t st) {
+int Impl<R>::iterate_dp(const fm_dims* d, const fm_state* s, const fm_dp* p, cudaStream_t st,
+                        cudaEvent_t* ev) {
+  int nev = 0;  // external event-record nodes between launches (fm_iterate_dp_profiled)
+#define FM_EVD() \
+  if (ev) FM_CUDA(cudaEventRecordWithFlags(ev[nev++], st, cudaEventRecordExternal));
   const Plan pl = make_plan(d);
   unsigned char* w = reinterpret_cast<unsigned char*>(s->work);
   R* phi = reinterpret_cast<R*>(w + pl.off_phi);
@@ -694,32 +772,46 @@ int Impl<R>::iterate_dp(const fm_dims* d, const fm_state* s, const fm_dp* p, cud
   const int N = (int)d->N, F = (int)d->F, T = (int)d->T, K = (int)d->K, B = (int)d->B;
   const unsigned BN = (unsigned)(d->B * (d->N - 1));
   // lambda of the state after the previous iteration (u absorbed c[0], W c[1:])
+  FM_EVD();
   if (int rc = lambda_nmf(d, s, st)) return rc;
+  FM_EVD();
   if (int rc = dp_lambda(d, s, p, st)) return rc;
   // latent hook (separate.py:205-213): Adam on z against the frozen y_rest,
   // then r = exp(dec(z)) -- one launch
   if (p->mh_steps > 0) {  // the reference's Metropolis chain (sources.py:307-339)
+    FM_EVD();
     if (int rc = dp_mh(d, s, p, p->mh_steps, st)) return rc;
+    FM_EVD();
     if (int rc = dp_lambda(d, s, p, st)) return rc;
   } else if (p->adam_steps > 0) {  // BASELINE config 4: Adam
+    FM_EVD();
     if (int rc = dp_latent(d, s, p, p->adam_steps, st)) return rc;
+    FM_EVD();
     if (int rc = dp_lambda(d, s, p, st)) return rc;
   }
   // U step (sources.py:258-261)
+  FM_EVD();
   if (int rc = phi_pass(d, s, st)) return rc;
+  FM_EVD();
   launch_pdl(k_dp_umu<R>, dim3((unsigned)F, (unsigned)B), dim3(256), 0, st, u, (const R*)v, r,
              (const R*)phi, N, F, T);
   FM_CHECK_LAUNCH("k_dp_umu");
+  FM_EVD();
   if (int rc = dp_lambda(d, s, p, st)) return rc;
   // V step (sources.py:262-265)
+  FM_EVD();
   if (int rc = phi_pass(d, s, st)) return rc;
+  FM_EVD();
   launch_pdl(k_dp_vmu<R>, dim3((unsigned)((T + 31) / 32), (unsigned)VMU_FS, (unsigned)B), dim3(32, 8), 0,
              st, (const R*)u, v, r, (const R*)phi, N, F, T, reinterpret_cast<R*>(w + pl.off_vmu),
              reinterpret_cast<unsigned*>(w + pl.off_vcnt));
   FM_CHECK_LAUNCH("k_dp_vmu");
+  FM_EVD();
   if (int rc = dp_lambda(d, s, p, st)) return rc;
   // W step (noise NMF, sources.py:253 -> 191-194)
+  FM_EVD();
   if (int rc = phi_pass(d, s, st)) return rc;
+  FM_EVD();
   FM_DISPATCH_KB(K, {
     FM_DISPATCH_TILE(pl.FT, FTT, {
       if constexpr (FTT <= 32) {
@@ -732,8 +824,11 @@ int Impl<R>::iterate_dp(const fm_dims* d, const fm_state* s, const fm_dp* p, cud
     });
   });
   // H step
+  FM_EVD();
   if (int rc = lambda_nmf(d, s, st)) return rc;
+  FM_EVD();
   if (int rc = phi_pass(d, s, st)) return rc;
+  FM_EVD();
   FM_DISPATCH_KB(K, {
     FM_DISPATCH_TILE(pl.TT, TTT, {
       if constexpr (TTT >= 16) {
@@ -747,23 +842,22 @@ int Impl<R>::iterate_dp(const fm_dims* d, const fm_state* s, const fm_dp* p, cud
       }
     });
   });
+  FM_EVD();
   if (int rc = lambda_nmf(d, s, st)) return rc;
   // spatial part as in the plain iteration; k_ip folds c[0] into u
+  FM_EVD();
   if (int rc = gain(d, s, st)) return rc;
+  FM_EVD();
   if (int rc = vacc(d, s, st)) return rc;
+  FM_EVD();
   if (int rc = ip(d, s, st, u)) return rc;
+  FM_EVD();
   if (int rc = back(d, s, /*tail_only=*/0, /*record=*/1, st)) return rc;
-  unsigned* itp = reinterpret_cast<unsigned*>(w + pl.off_cnt) + 1;
-  launch_pdl(k_trace, dim3((unsigned)d->B), dim3(256), 0, st,
-             reinterpret_cast<const double*>(w + pl.off_llp),
-             reinterpret_cast<const double*>(w + pl.off_ldp), s->trace, itp, (int)d->B, F,
-             (T + 255) / 256, T);
-  FM_CHECK_LAUNCH("k_trace");
-  if (d->B > 1) {
-    launch_pdl(k_iter_advance, dim3(1), dim3(1), 0, st, itp);
-    FM_CHECK_LAUNCH("k_iter_advance");
-  }
+  FM_EVD();
+  if (int rc = trace(d, s, st)) return rc;
+  FM_EVD();
   return FM_OK;
+#undef FM_EVD
 }
 
 // ---------------------------------------------------------------------------

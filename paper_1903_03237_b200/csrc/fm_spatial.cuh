@@ -233,9 +233,9 @@ __global__ void __launch_bounds__(VaCfg<R, M>::BS, VaCfg<R, M>::MINB) k_vacc(Vac
   // finish the gain MU from the k_gain segment partials (fixed order)
   for (int e = tid; e < N * M; e += BS) {
     const int n = e / M, m = e % M;
-    const R* gp = a.gpart + ((size_t)b * F + f) * nseg * N * 2 * M + n * 2 * M;
+    const R* gp = a.gpart + ((size_t)b * F + f) * a.gseg * N * 2 * M + n * 2 * M;
     R sn = 0, sd = 0;
-    for (int q = 0; q < nseg; ++q) {
+    for (int q = 0; q < a.gseg; ++q) {
       sn += gp[(size_t)q * N * 2 * M + m];
       sd += gp[(size_t)q * N * 2 * M + M + m];
     }
@@ -381,6 +381,7 @@ template <typename R> struct IpArgs {
   cplx<R>* Q;
   R* g;
   R* W;
+  const R* Wsrc;  // W before the absorb (== W: in place; else W = Wsrc c)
   R* cs_out;
   double* ld_part;
   const unsigned* iter;
@@ -435,6 +436,7 @@ __global__ void __launch_bounds__(IpCfg<M>::BS) k_ip(IpArgs<R> a) {
   C* Qg = a.Q + ((size_t)b * F + f) * M * M;
   R* gg = a.g + (size_t)b * N * F * M + (size_t)f * M;
   R* Wg = a.W + (size_t)b * (N - a.n0) * F * K + (size_t)f * K;
+  const R* Wsg = a.Wsrc + (size_t)b * (N - a.n0) * F * K + (size_t)f * K;
   const unsigned it = *a.iter;
   const long long fglob = a.f_offset + f;
   {  // V_f = (1/T) sum over the segment partials (fixed order, fp64), mirrored
@@ -646,10 +648,15 @@ __global__ void __launch_bounds__(IpCfg<M>::BS) k_ip(IpArgs<R> a) {
     const int Nn = N - a.n0;
     for (int e = tid; e < Nn * K; e += BS) {
       const int n = e / K, k = e % K;
-      R* wp = Wg + (size_t)n * F * K + k;
-      *wp = *wp * cs[a.n0 + n];
+      const size_t wi = (size_t)n * F * K + k;
+      Wg[wi] = Wsg[wi] * cs[a.n0 + n];  // sources.py:202-204
     }
     if (a.n0 && tid == 0) a.u[(size_t)b * F + f] *= cs[0];
+  } else if (Wsg != Wg) {  // no absorb: the state W is the W-stepped one
+    for (int e = tid; e < (N - a.n0) * K; e += BS) {
+      const size_t wi = (size_t)(e / K) * F * K + e % K;
+      Wg[wi] = Wsg[wi];
+    }
   }
   for (int e = tid; e < M * M; e += BS) Qg[e] = cmake<C>(Qd[e].x, Qd[e].y);
   for (int e = tid; e < N * M; e += BS) gg[(size_t)(e / M) * F * M + (e % M)] = gs[e];
@@ -751,16 +758,16 @@ __global__ void __launch_bounds__(256, (M > 8 ? 2 : 3)) k_back(BackArgs<R> a) {
 }
 
 // trace entry of the state after this iteration (separate.py:313-318, :321):
-// sum of the data-term partials (B, F, tiles) + 2T sum_f log|det Q_f|, one CTA
+// sum of the data-term partials (B, np1, np2) + 2T sum_f log|det Q_f|, one CTA
 // per mixture, fixed-order strided + tree reduction (deterministic).
 static __global__ void __launch_bounds__(256) k_trace(const double* __restrict__ ll_part,
                                                const double* __restrict__ ld_part,
                                                double* __restrict__ trace, unsigned* iter, int B,
-                                               int F, int ntile, int T) {
+                                               int np1, int np2, int F, int T) {
   pdl_entry();
   __shared__ double r1[8], r2[8];
   const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const size_t n1 = (size_t)F * ntile;
+  const size_t n1 = (size_t)np1 * np2;  // data-term partials per mixture
   const double* p1 = ll_part + (size_t)b * n1;
   const double* p2 = ld_part + (size_t)b * F;
   double s1 = 0.0, s2 = 0.0;

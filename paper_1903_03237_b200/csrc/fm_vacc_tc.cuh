@@ -171,9 +171,9 @@ __global__ void __launch_bounds__(256) k_vacc_tc(VaccArgs<float> a) {
   // gain MU from the k_gain segment partials (fixed order; as k_vacc)
   for (int e = tid; e < N * M; e += BS) {
     const int n = e / M, m = e % M;
-    const float* gp = a.gpart + ((size_t)b * F + f) * nseg * N * 2 * M + n * 2 * M;
+    const float* gp = a.gpart + ((size_t)b * F + f) * a.gseg * N * 2 * M + n * 2 * M;
     float sn = 0, sd = 0;
-    for (int q = 0; q < nseg; ++q) {
+    for (int q = 0; q < a.gseg; ++q) {
       sn += gp[(size_t)q * N * 2 * M + m];
       sd += gp[(size_t)q * N * 2 * M + M + m];
     }

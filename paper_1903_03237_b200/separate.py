@@ -135,6 +135,7 @@ class _SpatialView:
     @Q_FMM.setter
     def Q_FMM(self, v):
         self._loop.Q[self._b].copy_(self._loop._as_dev(v, self._loop.Q.dtype))
+        self._loop._prologue_done = False  # x~, Ht and the W step derive from the state
 
     @property
     def g_NFM(self):
@@ -143,6 +144,7 @@ class _SpatialView:
     @g_NFM.setter
     def g_NFM(self, v):
         self._loop.g[self._b].copy_(self._loop._as_dev(v, self._loop.real))
+        self._loop._prologue_done = False  # x~, Ht and the W step derive from the state
 
     @property
     def n_sources(self):
@@ -165,6 +167,7 @@ class _SourceView:
     @W_NFK.setter
     def W_NFK(self, v):
         self._loop.W[self._b].copy_(self._loop._as_dev(v, self._loop.real))
+        self._loop._prologue_done = False  # x~, Ht and the W step derive from the state
 
     @property
     def H_NKT(self):
@@ -173,6 +176,7 @@ class _SourceView:
     @H_NKT.setter
     def H_NKT(self, v):
         self._loop.H[self._b].copy_(self._loop._as_dev(v, self._loop.real))
+        self._loop._prologue_done = False  # x~, Ht and the W step derive from the state
 
     @property
     def n_sources(self):
@@ -322,7 +326,7 @@ class DeviceLoop:
         if self.iterations_done >= self.n_trace:
             self._grow_trace(self.iterations_done + 1)
         if not self._prologue_done:
-            self.prologue()
+            self.prologue() if self.iterations_done == 0 else self.refresh()
         if rng is not None and self.dp is not None and self.dp.noise is not None:
             self.dp.mh_rng = rng
         ll = float(self.data_term()[0])
@@ -375,8 +379,21 @@ class DeviceLoop:
                                    _lib.stream_ptr()), "fm_prologue")
 
     @_on_device
+    def refresh(self):
+        """Re-derive x~, the transposed H and the coming W step after the
+        state was assigned between iterations (fm_refresh); the trace index
+        continues."""
+        if self.dp is not None:
+            raise InvalidInputError("state assignment between deep-prior iterations is not supported")
+        self._prologue_done = True
+        _lib.check(_lib.load().fm_refresh(ctypes.byref(self.dims), ctypes.byref(self.state),
+                                          _lib.stream_ptr()), "fm_refresh")
+
+    @_on_device
     def run(self, n, use_graph=False):
         lib = _lib.load()
+        if not self._prologue_done:
+            self.prologue() if self.iterations_done == 0 else self.refresh()
         if self.iterations_done + n > self.n_trace:
             raise InvalidInputError("trace buffer too small for the requested iterations")
         if self.dp is not None and self.dp.noise is not None:
