@@ -409,16 +409,21 @@ def main():
     ftm = F * T * M * Bl if not sharded_f else (loop.F * T * M)
     nprof = 10
     if loop.dp is None:
-        names = ["k_hpass", "k_gpass", "k_vacc", "k_ip", "k_bpass", "k_trace"]
+        fused = os.environ.get("FM_SCHEDULE") == "fused"
+        names = (["k_hpass", "k_gpass", "k_vacc", "k_ip", "k_bpass", "k_trace"] if fused else
+                 ["k_wstats", "k_lambda", "k_phi", "k_hstats", "k_lambda", "k_gain", "k_vacc",
+                  "k_ip", "k_back", "k_trace"])
         samples = []
         if not sharded_f:
-            ms = (ctypes.c_float * 6)()
+            ms = (ctypes.c_float * 16)()
+            nint = ctypes.c_int(0)
             for _ in range(nprof):
                 reset()
                 loop.prologue()
                 _lib.check(lib.fm_iterate_profiled(ctypes.byref(loop.dims), ctypes.byref(loop.state),
-                                                   ms, _lib.stream_ptr()), "fm_iterate_profiled")
-                samples.append(list(ms[:]))
+                                                   ms, ctypes.byref(nint), _lib.stream_ptr()),
+                           "fm_iterate_profiled")
+                samples.append(list(ms[:nint.value]))
     else:
         lat = "k_dp_mh" if cfg.get("mh") else "k_dp_latent"
         names = ["k_lambda", "k_dp_lambda", lat, "k_dp_lambda", "k_phi", "k_dp_umu", "k_dp_lambda",
@@ -445,6 +450,7 @@ def main():
     # (P4, P5) and the x~ write (P5); lambda / phi / y are on-chip by definition
     FT = ftm // M
     alg_tab = {
+        "k_wstats": 0, "k_hstats": 0, "k_lambda": 0,  # phi / lambda traffic: not algorithmic
         "k_hpass": ftm * rs,                  # read x~ (H step)
         "k_gpass": ftm * rs,                  # read x~ (gain step)
         "k_vacc": ftm * 2 * rs,               # read X (V accumulation)
@@ -541,11 +547,13 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline and args.config in ("c1", "c0"):
         cpu = cpu_baseline_sample(cfg)
 
-    # per iteration: k_hpass, k_gpass, k_vacc, k_ip, k_bpass, k_trace (+ the
-    # counter advance when B > 1); the prologue is k_hstore + k_bpass
-    launches = args.steps * (2 + (6 if cfg['B'] == 1 else 7) * iters)
-    if sharded_f:  # + k_hstore (H MU + Ht) after the all-reduce
-        launches = args.steps * (2 + 7 * iters)
+    # per iteration, split schedule: k_wstats, k_lambda, k_phi, k_hstats, k_lambda,
+    # k_gain, k_vacc, k_ip, k_back, k_trace; fused: k_hpass, k_gpass, k_vacc,
+    # k_ip, k_bpass, k_trace (+ the counter advance when B > 1); prologue 2
+    per_it = 6 if os.environ.get("FM_SCHEDULE") == "fused" else 10
+    launches = args.steps * (2 + (per_it if cfg['B'] == 1 else per_it + 1) * iters)
+    if sharded_f:  # + the H update after the all-reduce
+        launches = args.steps * (2 + (per_it + 1) * iters)
     if cfg.get("dp"):  # 21 per iteration (one latent-hook launch: Adam or Metropolis), 5 in the prologue
         launches = args.steps * (5 + 21 * iters)
     if rank == 0:

@@ -197,10 +197,13 @@ int fm_prologue(const fm_dims* d, const fm_state* s, void* stream);
  * assignable arrays, separate.py:178-184); the trace index continues. */
 int fm_refresh(const fm_dims* d, const fm_state* s, void* stream);
 
-/* One full iteration (separate.py:201-234) on one process: six launches
- * (k_hpass, k_gpass, k_vacc, k_ip, k_bpass and the trace entry; B > 1 adds the
- * counter advance); the W step of the NEXT iteration runs inside k_bpass, so
- * the state W after a call is the reference's post-absorb W. Appends
+/* One full iteration (separate.py:201-234) on one process. Split schedule
+ * (default): ten launches (k_wstats, k_lambda, k_phi, k_hstats, k_lambda,
+ * k_gain, k_vacc, k_ip, k_back, k_trace). Fused schedule (FM_SCHEDULE=fused):
+ * six (k_hpass, k_gpass, k_vacc, k_ip, k_bpass, k_trace), lambda formed on
+ * chip and the W step of the NEXT iteration inside k_bpass (the state W after
+ * a call is still the reference's post-absorb W). B > 1 adds the counter
+ * advance. Appends
  * trace[i] (i = number of previous fm_iterate calls since fm_prologue) =
  * data term + 2T sum_f log|det Q_f| of the state after this iteration. */
 int fm_iterate(const fm_dims* d, const fm_state* s, void* stream);
@@ -214,10 +217,14 @@ int fm_iterate_phase(const fm_dims* d, const fm_state* s, int phase, void* hstat
                      void* stream);
 
 /* One fm_iterate captured into a CUDA graph with event-record nodes between
- * its launches and replayed once on `stream` (synchronises): ms_host[0..5] =
- * device ms of k_hpass, k_gpass, k_vacc, k_ip, k_bpass, k_trace as they run
- * inside a graph replay. Used by bench.py for the per-kernel roofline. */
-int fm_iterate_profiled(const fm_dims* d, const fm_state* s, float* ms_host, void* stream);
+ * its launches and replayed once on `stream` (synchronises): ms_host (>= 10
+ * floats) receives the device ms of each launch as it runs inside a graph
+ * replay, *n_intervals their count -- split schedule (default, 10): k_wstats,
+ * k_lambda, k_phi, k_hstats, k_lambda, k_gain, k_vacc, k_ip, k_back, k_trace;
+ * fused schedule (FM_SCHEDULE=fused, 6): k_hpass, k_gpass, k_vacc, k_ip,
+ * k_bpass, k_trace. Used by bench.py for the per-kernel roofline. */
+int fm_iterate_profiled(const fm_dims* d, const fm_state* s, float* ms_host, int* n_intervals,
+                        void* stream);
 
 /* The same for one fm_iterate_dp: ms_host (>= 21 floats) receives the device
  * ms of each launch in order (k_lambda, k_dp_lambda, [latent hook, k_dp_lambda,]

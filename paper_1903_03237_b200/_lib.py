@@ -100,7 +100,8 @@ SIGNATURES = [
     ("fm_iterate_phase", ctypes.c_int,
      [ctypes.POINTER(FmDims), ctypes.POINTER(FmState), ctypes.c_int, _vp, _vp]),
     ("fm_iterate_profiled", ctypes.c_int,
-     [ctypes.POINTER(FmDims), ctypes.POINTER(FmState), ctypes.POINTER(ctypes.c_float), _vp]),
+     [ctypes.POINTER(FmDims), ctypes.POINTER(FmState), ctypes.POINTER(ctypes.c_float),
+      ctypes.POINTER(ctypes.c_int), _vp]),
     ("fm_run", ctypes.c_int,
      [ctypes.POINTER(FmDims), ctypes.POINTER(FmState), ctypes.c_int, ctypes.c_int, _vp]),
     ("fm_iterate_dp_profiled", ctypes.c_int,

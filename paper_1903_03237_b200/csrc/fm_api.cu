@@ -180,7 +180,7 @@ int fm_data_term(const fm_dims* d, const fm_state* s, double* out_host, void* st
   const Plan p = make_plan(d);
   // data-term partials per mixture: (F, ntile) from k_back (deep prior),
   // (nfb, bseg) from k_bpass
-  const size_t per = d->dp ? (size_t)d->F * p.ntile : (size_t)p.nfb * p.bseg;
+  const size_t per = (d->dp || !use_fused(d)) ? (size_t)d->F * p.ntile : (size_t)p.nfb * p.bseg;
   const size_t n = (size_t)d->B * per;
   std::vector<double> h(n);
   FM_CUDA(cudaMemcpyAsync(h.data(), reinterpret_cast<unsigned char*>(s->work) + p.off_llp,
@@ -231,16 +231,17 @@ int fm_iterate_phase(const fm_dims* d, const fm_state* s, int phase, void* hstat
   return FM_BY_DTYPE(d->dtype, iterate_phase(d, s, phase, hstat, (cudaStream_t)stream));
 }
 
-int fm_iterate_profiled(const fm_dims* d, const fm_state* s, float* ms_host, void* stream) {
+int fm_iterate_profiled(const fm_dims* d, const fm_state* s, float* ms_host, int* n_intervals,
+                        void* stream) {
   // One iteration captured into a CUDA graph with external event-record
-  // nodes between its launches, replayed once: ms_host[0..5] = device ms of
-  // k_hpass, k_gpass, k_vacc, k_ip, k_bpass, k_trace as they run inside a
-  // graph replay (the production path), not as separately synchronised
-  // eager launches.
+  // nodes between its launches, replayed once: the device ms of each launch
+  // as it runs inside a graph replay (the production path), not as
+  // separately synchronised eager launches (fastmnmf.h lists the order).
   if (int rc = validate_dims(d)) return rc;
   if (d->dp) { set_error("fm_iterate_profiled: plain FastMNMF only"); return FM_EINVAL; }
   cudaStream_t st = (cudaStream_t)stream;
-  constexpr int NEV = 7;
+  constexpr int NEV = 11;
+  const int nint = use_fused(d) ? 6 : 10;
   cudaEvent_t ev[NEV];
   for (int i = 0; i < NEV; ++i) FM_CUDA(cudaEventCreate(&ev[i]));
   cudaStream_t cap = nullptr;
@@ -263,7 +264,8 @@ int fm_iterate_profiled(const fm_dims* d, const fm_state* s, float* ms_host, voi
   if (rc == FM_OK) {
     FM_CUDA(cudaGraphLaunch(exec, st));
     FM_CUDA(cudaStreamSynchronize(st));
-    for (int i = 0; i + 1 < NEV; ++i) FM_CUDA(cudaEventElapsedTime(&ms_host[i], ev[i], ev[i + 1]));
+    for (int i = 0; i < nint; ++i) FM_CUDA(cudaEventElapsedTime(&ms_host[i], ev[i], ev[i + 1]));
+    if (n_intervals) *n_intervals = nint;
   }
   if (exec) cudaGraphExecDestroy(exec);
   if (graph) cudaGraphDestroy(graph);

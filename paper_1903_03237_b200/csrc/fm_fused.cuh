@@ -280,10 +280,57 @@ __global__ void __launch_bounds__(256) k_hstore(R* __restrict__ H, R* __restrict
 }
 
 // ---------------------------------------------------------------------------
+// lambda tile: lam_s[(n * FB + fl) * 32 + tl] = W[fl][n] . H[n][tl] for the
+// CTA's FB bins x 32 frames. Warp w takes source n = w % N and bin group
+// w / N (FB / N groups), so each H row a lane loads serves every bin of its
+// group (the W rows are warp broadcasts).
+// ---------------------------------------------------------------------------
+template <typename R, int NN, int KC>
+__device__ __forceinline__ void lam_tile(const R* __restrict__ Ws, const R* __restrict__ Hs,
+                                         R* __restrict__ lam_s, int Nrt, int K4rt, int FB, int warp,
+                                         int lane) {
+  const int N = NN ? NN : Nrt, K4 = KC ? KC : K4rt, KP = K4 + 4;
+  const int NBG = FB / N > 1 ? FB / N : 1;
+  const int BPG = (FB + NBG - 1) / NBG;
+  for (int as = warp; as < N * NBG; as += FB) {  // (source, bin group) assignments of this warp
+    const int n = as % N, fb0 = (as / N) * BPG;
+    const int nb = min(BPG, FB - fb0);
+    R acc[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[j] = R(0);
+    const R* hr = Hs + (n * FTC + lane) * KP;
+    const R* wr = Ws + (fb0 * N + n) * KP;
+    auto quad = [&](int k) {
+      R h[4];
+      lds4(hr + k, h);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        if (j < nb) {
+          R w[4];
+          lds4(wr + j * N * KP + k, w);
+#pragma unroll
+          for (int c = 0; c < 4; ++c) acc[j] += w[c] * h[c];
+        }
+      }
+    };
+    if constexpr (KC > 0) {
+#pragma unroll
+      for (int k = 0; k < KC; k += 4) quad(k);
+    } else {
+      for (int k = 0; k < K4; k += 4) quad(k);
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (j < nb) lam_s[(n * FB + fb0 + j) * FTC + lane] = acc[j];
+  }
+}
+
+// ---------------------------------------------------------------------------
 // k_hpass: H statistics + H MU. grid (ceil(T/32), B * NG, HS), block 32 * FB.
-// Each CTA accumulates sources [ng * NS, ng * NS + NS) of its tile; a thread
-// owns items j = warp + FB * i (i < IT): (source nl = j / KQ, k-quad kq = j %
-// KQ) at frame lane.
+// Each CTA accumulates sources [ng * NS, ng * NS + NS) of its 32-frame tile:
+// item j = tid + 256 i (i < IT) is (source nl, k-chunk ko of KCH = 8 or 4
+// bases) at frame lane, so a warp's 32 lanes share one (nl, ko) and the W
+// loads are broadcasts.
 // ---------------------------------------------------------------------------
 template <typename R> struct HpArgs {
   const R* xt;
@@ -302,9 +349,12 @@ template <typename R> struct HpArgs {
   int S;        // cp.async pipeline stages (2..4)
 };
 
-// shared-memory layout (bytes): Hs | S x (Ws | gs) | S x per-warp x~ rows | phi
+__host__ __device__ constexpr int hp_kch(int K4) { return K4 % 8 == 0 ? 8 : 4; }
+
+// shared-memory layout (bytes): Hs | S x (Ws | gs) | S x per-warp x~ rows |
+// lambda tile | phi
 struct HpLayout {
-  size_t o_ws0, wg_stride, gs_off, o_rows0, rows_stride, o_ph, total;
+  size_t o_ws0, wg_stride, gs_off, o_rows0, rows_stride, o_lam, o_ph, total;
   int rowp;
   __host__ __device__ HpLayout(int rs, int N, int K, int M, int MP, int FB, int NS, int S) {
     o_ws0 = al16((size_t)rs * N * FTC * kp_of(K));
@@ -313,7 +363,8 @@ struct HpLayout {
     rowp = row_pitch(rs * M);
     o_rows0 = o_ws0 + S * wg_stride;
     rows_stride = al16((size_t)FB * FTC * rowp);
-    o_ph = o_rows0 + S * rows_stride;
+    o_lam = o_rows0 + S * rows_stride;
+    o_ph = o_lam + al16((size_t)rs * N * FB * FTC);
     total = o_ph + al16((size_t)rs * FB * 2 * NS * FTC);
   }
   __host__ __device__ size_t ws(int buf) const { return o_ws0 + buf * wg_stride; }
@@ -327,11 +378,13 @@ __global__ void __launch_bounds__(256) k_hpass(HpArgs<R> a) {
   extern __shared__ __align__(16) unsigned char smraw[];
   const int FB = blockDim.x / FTC;
   const int N = NN ? NN : a.N, K = a.K, M = a.M, F = a.F, T = a.T, NS = a.NS;
-  const int K4 = KC ? KC : k4_of(K), KP = K4 + 4, KQ = K4 / 4;
+  const int K4 = KC ? KC : k4_of(K), KP = K4 + 4;
+  const int KCH = hp_kch(K4), KO = K4 / KCH;
   const int S = a.S;
   const HpLayout L((int)sizeof(R), N, K, M, MP, FB, NS, S);
   R* Hs = reinterpret_cast<R*>(smraw);
-  R* ph = reinterpret_cast<R*>(smraw + L.o_ph);  // [fl][2][NS][32]
+  R* lam_s = reinterpret_cast<R*>(smraw + L.o_lam);  // [N][FB][32]
+  R* ph = reinterpret_cast<R*>(smraw + L.o_ph);      // [fl][2][NS][32]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int t0 = blockIdx.x * FTC;
   const int b = blockIdx.y / a.NG, ng = blockIdx.y % a.NG;
@@ -357,22 +410,21 @@ __global__ void __launch_bounds__(256) k_hpass(HpArgs<R> a) {
     cp_async_commit();
   }
   const R fl = a.floorp[b];
-  R a1[IT][4], a2[IT][4];
+  R a1[IT][8], a2[IT][8];
 #pragma unroll
   for (int i = 0; i < IT; ++i)
 #pragma unroll
-    for (int c = 0; c < 4; ++c) a1[i][c] = a2[i][c] = R(0);
-  // this thread's accumulation items (hoisted: source row offset in Ws, phi
-  // offset; -1 = no item)
+    for (int c = 0; c < 8; ++c) a1[i][c] = a2[i][c] = R(0);
+  // this thread's items (hoisted): W row offset (-1: none) and phi offset
   int iw[IT], ip1[IT];
 #pragma unroll
   for (int i = 0; i < IT; ++i) {
-    const int j = warp + FB * i;
+    const int r = warp + FB * i;  // (nl, ko) index; lane = frame
     iw[i] = -1;
     ip1[i] = 0;
-    if (j < ns * KQ) {
-      const int nl = j / KQ, kq = j % KQ;
-      iw[i] = (nb + nl) * KP + kq * 4;
+    if (r < ns * KO) {
+      const int nl = r / KO, ko = r % KO;
+      iw[i] = (nb + nl) * KP + ko * KCH;
       ip1[i] = nl * FTC + lane;
     }
   }
@@ -384,11 +436,14 @@ __global__ void __launch_bounds__(256) k_hpass(HpArgs<R> a) {
     cp_async_commit();
     const R* Ws = reinterpret_cast<const R*>(smraw + L.ws(buf));
     const R* gs = reinterpret_cast<const R*>(smraw + L.gs(buf));
+    lam_tile<R, NN, KC>(Ws, Hs, lam_s, N, K4, FB, warp, lane);
+    __syncthreads();
     {  // phi at (bin f0 + warp, frame t)
       const int f = f0 + warp;
       const bool v = f < fend && t < T;
       R l[NMAX];
-      lam_point<R, NN, KC>(Ws + warp * N * KP, Hs, lane, N, K4, l);
+#pragma unroll
+      for (int n = 0; n < NMAX; ++n) l[n] = n < N ? lam_s[(n * FB + warp) * FTC + lane] : R(0);
       R xv[MP];
       read_row<R, MP>(reinterpret_cast<const R*>(smraw + L.rows(buf) + (size_t)(warp * FTC + lane) * L.rowp),
                       M, xv);
@@ -414,13 +469,18 @@ __global__ void __launch_bounds__(256) k_hpass(HpArgs<R> a) {
 #pragma unroll
       for (int i = 0; i < IT; ++i) {
         if (iw[i] >= 0) {
-          R w4[4];
-          lds4(wr + iw[i], w4);
           const R p1 = pw[ip1[i]], p2 = pw[NS * FTC + ip1[i]];
 #pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            a1[i][c] += w4[c] * p1;
-            a2[i][c] += w4[c] * p2;
+          for (int q = 0; q < 2; ++q) {
+            if (q * 4 < KCH) {
+              R w4[4];
+              lds4(wr + iw[i] + q * 4, w4);
+#pragma unroll
+              for (int c = 0; c < 4; ++c) {
+                a1[i][q * 4 + c] += w4[c] * p1;
+                a2[i][q * 4 + c] += w4[c] * p2;
+              }
+            }
           }
         }
       }
@@ -431,15 +491,17 @@ __global__ void __launch_bounds__(256) k_hpass(HpArgs<R> a) {
   const size_t tileid = ((size_t)blockIdx.x * gridDim.y + blockIdx.y);
   const size_t PSZ = (size_t)2 * NS * K4 * FTC;  // one split's partial
   R* pt = a.part + tileid * HS * PSZ;
+  auto pidx = [&](int i, int c) {  // partial index of (item i, basis c of its chunk)
+    const int r = warp + FB * i, nl = r / KO, ko = r % KO;
+    return (size_t)(nl * K4 + ko * KCH + c) * FTC + lane;
+  };
   if (HS > 1) {
 #pragma unroll
     for (int i = 0; i < IT; ++i) {
-      const int j = warp + FB * i;
-      if (j < ns * KQ) {
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          pt[(size_t)blockIdx.z * PSZ + ((size_t)(j * 4 + c)) * FTC + lane] = a1[i][c];
-          pt[(size_t)blockIdx.z * PSZ + ((size_t)NS * K4 + j * 4 + c) * FTC + lane] = a2[i][c];
+      if (iw[i] >= 0) {
+        for (int c = 0; c < KCH; ++c) {
+          pt[(size_t)blockIdx.z * PSZ + pidx(i, c)] = a1[i][c];
+          pt[(size_t)blockIdx.z * PSZ + (size_t)NS * K4 * FTC + pidx(i, c)] = a2[i][c];
         }
       }
     }
@@ -453,17 +515,18 @@ __global__ void __launch_bounds__(256) k_hpass(HpArgs<R> a) {
     if (tid == 0) a.cnt[tileid] = 0;  // re-armed for the next launch
 #pragma unroll
     for (int i = 0; i < IT; ++i) {
-      const int j = warp + FB * i;
-      if (j < ns * KQ) {
+      if (iw[i] >= 0) {
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          R sn = 0, sd = 0;
-          for (int z = 0; z < HS; ++z) {  // split order
-            sn += __ldcg(pt + (size_t)z * PSZ + ((size_t)(j * 4 + c)) * FTC + lane);
-            sd += __ldcg(pt + (size_t)z * PSZ + ((size_t)NS * K4 + j * 4 + c) * FTC + lane);
+        for (int c = 0; c < 8; ++c) {
+          if (c < KCH) {
+            R sn = 0, sd = 0;
+            for (int z = 0; z < HS; ++z) {  // split order
+              sn += __ldcg(pt + (size_t)z * PSZ + pidx(i, c));
+              sd += __ldcg(pt + (size_t)z * PSZ + (size_t)NS * K4 * FTC + pidx(i, c));
+            }
+            a1[i][c] = sn;
+            a2[i][c] = sd;
           }
-          a1[i][c] = sn;
-          a2[i][c] = sd;
         }
       }
     }
@@ -471,34 +534,33 @@ __global__ void __launch_bounds__(256) k_hpass(HpArgs<R> a) {
   if (t >= T) return;
 #pragma unroll
   for (int i = 0; i < IT; ++i) {
-    const int j = warp + FB * i;
-    if (j < ns * KQ) {
-      const int n = nb + j / KQ, kq = j % KQ;
-      if (a.mode == 0) {
-        R hv[4];
+    if (iw[i] < 0) continue;
+    const int r = warp + FB * i, n = nb + r / KO, k0 = (r % KO) * KCH;
+    if (a.mode == 0) {
+      R hv[8];
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          const int k = kq * 4 + c;
-          hv[c] = R(0);
-          if (k < K) {
-            const size_t hi = (((size_t)b * N + n) * K + k) * T + t;
-            hv[c] = a.H[hi] * mu_factor(a1[i][c], a2[i][c]);  // sources.py:198
-            a.H[hi] = hv[c];
-          }
+      for (int c = 0; c < 8; ++c) {
+        hv[c] = R(0);
+        const int k = k0 + c;
+        if (c < KCH && k < K) {
+          const size_t hi = (((size_t)b * N + n) * K + k) * T + t;
+          hv[c] = a.H[hi] * mu_factor(a1[i][c], a2[i][c]);  // sources.py:198
+          a.H[hi] = hv[c];
         }
-        R* ht = a.Ht + (((size_t)b * N + n) * T + t) * K4 + kq * 4;
+      }
+      R* ht = a.Ht + (((size_t)b * N + n) * T + t) * K4 + k0;
 #pragma unroll
-        for (int c = 0; c < 4; ++c) ht[c] = hv[c];
-      } else {
-        const size_t NKT = (size_t)N * K * T;
+      for (int c = 0; c < 8; ++c)
+        if (c < KCH) ht[c] = hv[c];
+    } else {
+      const size_t NKT = (size_t)N * K * T;
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          const int k = kq * 4 + c;
-          if (k < K) {
-            const size_t hi = ((size_t)n * K + k) * T + t;
-            a.hout[(size_t)b * 2 * NKT + hi] = a1[i][c];
-            a.hout[(size_t)b * 2 * NKT + NKT + hi] = a2[i][c];
-          }
+      for (int c = 0; c < 8; ++c) {
+        const int k = k0 + c;
+        if (c < KCH && k < K) {
+          const size_t hi = ((size_t)n * K + k) * T + t;
+          a.hout[(size_t)b * 2 * NKT + hi] = a1[i][c];
+          a.hout[(size_t)b * 2 * NKT + NKT + hi] = a2[i][c];
         }
       }
     }
@@ -506,8 +568,8 @@ __global__ void __launch_bounds__(256) k_hpass(HpArgs<R> a) {
 }
 
 // ---------------------------------------------------------------------------
-// Per-warp reduction layout shared by k_gpass and k_bpass: NI items (one per
-// lane when NI <= 32, S = 32 / NI frame slices; else IT items per lane, S = 1).
+// Per-warp reduction layout of k_gpass: NI items (one per lane when NI <= 32,
+// S = 32 / NI frame slices; else IT items per lane, S = 1).
 // ---------------------------------------------------------------------------
 struct WarpItems {
   int NI, S, item, slice;
@@ -542,10 +604,10 @@ template <typename R> struct GpArgs {
 };
 
 // shared-memory layout (bytes): S x Hs | Ws | gs | S x per-warp x~ rows |
-// per warp: lam [N][33], iy [32][MP + 4], xr [32][MP + 4], red [32][8]
+// lambda tile | per warp: iy [32][MP + 4], xr [32][MP + 4], red [32][8]
 struct GpLayout {
-  size_t hs_stride, o_ws, o_gs, o_rows0, rows_stride, o_warp, warp_bytes, total;
-  int rowp, lamw;
+  size_t hs_stride, o_ws, o_gs, o_rows0, rows_stride, o_lam, o_warp, warp_bytes, total;
+  int rowp;
   __host__ __device__ GpLayout(int rs, int N, int K, int M, int MP, int FB, int S) {
     hs_stride = al16((size_t)rs * N * FTC * kp_of(K));
     o_ws = S * hs_stride;
@@ -553,9 +615,9 @@ struct GpLayout {
     o_rows0 = o_gs + al16((size_t)rs * FB * N * MP);
     rowp = row_pitch(rs * M);
     rows_stride = al16((size_t)FB * FTC * rowp);
-    lamw = (N * 33 + 3) & ~3;
-    warp_bytes = al16((size_t)rs * (lamw + 2 * FTC * (MP + 4) + 32 * 8));
-    o_warp = o_rows0 + S * rows_stride;
+    o_lam = o_rows0 + S * rows_stride;
+    warp_bytes = al16((size_t)rs * (2 * FTC * (MP + 4) + 32 * 8));
+    o_warp = o_lam + al16((size_t)rs * N * FB * FTC);
     total = o_warp + (size_t)FB * warp_bytes;
   }
   __host__ __device__ size_t hs(int buf) const { return buf * hs_stride; }
@@ -568,15 +630,15 @@ __global__ void __launch_bounds__(256) k_gpass(GpArgs<R> a) {
   extern __shared__ __align__(16) unsigned char smraw[];
   const int FB = blockDim.x / FTC;
   const int N = NN ? NN : a.N, K = a.K, M = a.M, F = a.F, T = a.T;
-  const int K4 = KC ? KC : k4_of(K), KP = K4 + 4;
+  const int K4 = KC ? KC : k4_of(K);
   constexpr int MQ = MP / 4, LDR = MP + 4;
   const int S = a.S;
   const GpLayout L((int)sizeof(R), N, K, M, MP, FB, S);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   R* Ws = reinterpret_cast<R*>(smraw + L.o_ws);
   R* gs = reinterpret_cast<R*>(smraw + L.o_gs);
-  R* lw = reinterpret_cast<R*>(smraw + L.o_warp + (size_t)warp * L.warp_bytes);  // [N][33]
-  R* iyw = lw + L.lamw;          // [32][LDR]
+  R* lam_s = reinterpret_cast<R*>(smraw + L.o_lam);  // [N][FB][32]
+  R* iyw = reinterpret_cast<R*>(smraw + L.o_warp + (size_t)warp * L.warp_bytes);  // [32][LDR]
   R* xrw = iyw + FTC * LDR;      // [32][LDR]
   R* red = xrw + FTC * LDR;      // [32][8]
   const int seg = blockIdx.x, nseg = gridDim.x, b = blockIdx.z;
@@ -605,6 +667,7 @@ __global__ void __launch_bounds__(256) k_gpass(GpArgs<R> a) {
   const int n1 = wi.item / MQ, mq = wi.item % MQ;
   R num[4] = {0, 0, 0, 0}, den[4] = {0, 0, 0, 0};
   const R* gw = gs + warp * N * MP;
+  const R* lw = lam_s + warp * FTC;  // + n FB 32 + t
   const size_t FTs = (size_t)F * T;
   R* lamp = a.lam + (size_t)b * N * FTs + (size_t)(fv ? f : 0) * T + lane;  // + n FT + t0
   int buf = 0;
@@ -614,29 +677,31 @@ __global__ void __launch_bounds__(256) k_gpass(GpArgs<R> a) {
     if (t0 + (S - 1) * FTC < tb) issue(t0 + (S - 1) * FTC, buf == 0 ? S - 1 : buf - 1);
     cp_async_commit();
     const R* Hs = reinterpret_cast<const R*>(smraw + L.hs(buf));
+    lam_tile<R, NN, KC>(Ws, Hs, lam_s, N, K4, FB, warp, lane);
+    __syncthreads();
     const bool v = fv && t0 + lane < tb;
     R l[NMAX];
-    lam_point<R, NN, KC>(Ws + warp * N * KP, Hs, lane, N, K4, l);
+#pragma unroll
+    for (int n = 0; n < NMAX; ++n) l[n] = n < N ? lw[n * FB * FTC + lane] : R(0);
     R xv[MP];
     read_row<R, MP>(reinterpret_cast<const R*>(smraw + L.rows(buf) + (size_t)(warp * FTC + lane) * L.rowp),
                     M, xv);
     R y[MP], iy[MP];
     power_point<R, MP, NN>(l, gw, N, M, fl, v, y, iy);
+    if (v) {
 #pragma unroll
-    for (int n = 0; n < NMAX; ++n) {
-      if (n >= N) break;
-      if (v) lamp[(size_t)n * FTs + t0] = l[n];
-      lw[n * 33 + lane] = v ? l[n] : R(0);
+      for (int n = 0; n < NMAX; ++n)
+        if (n < N) lamp[(size_t)n * FTs + t0] = l[n];
     }
     R xr[MP];
 #pragma unroll
     for (int m = 0; m < MP; ++m) xr[m] = xv[m] * iy[m] * iy[m];
-    RowIO<R, MP>::store(iyw + lane * LDR, iy);
+    RowIO<R, MP>::store(iyw + lane * LDR, iy);  // iy = 0 on invalid frames
     RowIO<R, MP>::store(xrw + lane * LDR, xr);
     __syncwarp();
     if (wi.slice >= 0) {
       for (int tl = wi.slice; tl < FTC; tl += wi.S) {
-        const R lv = lw[n1 * 33 + tl];
+        const R lv = lw[n1 * FB * FTC + tl];
         R xq[4], iq[4];
         lds4(xrw + tl * LDR + mq * 4, xq);
         lds4(iyw + tl * LDR + mq * 4, iq);
@@ -647,7 +712,6 @@ __global__ void __launch_bounds__(256) k_gpass(GpArgs<R> a) {
         }
       }
     }
-    __syncwarp();
   }
   cp_async_wait<0>();
   // slice sums in fixed order, then the segment partial of (n, f, m)
@@ -684,6 +748,10 @@ __global__ void __launch_bounds__(256) k_gpass(GpArgs<R> a) {
 // ---------------------------------------------------------------------------
 // k_bpass: projection + data term + W statistics -> Wn.
 // grid (nseg, ceil(F/FB), B), block 32 * FB.
+// W statistics: CTA item j = (source n, bin pair fp, k-quad kq), NI =
+// N (FB/2) KQ; threads tid = s NI + j take frames t = s, s + BS, ... of every
+// chunk (BS = 256 / NI frame slices, or IT items per thread when NI > 256);
+// one 16-B H load feeds two bins' numerators and denominators.
 // ---------------------------------------------------------------------------
 template <typename R> struct BpArgs {
   const cplx<R>* X;
@@ -699,24 +767,28 @@ template <typename R> struct BpArgs {
   double* llp;    // (B, nfb, nseg) data-term partials
   int F, T, N, K, M, TR;
   int S;          // cp.async pipeline stages (2..4)
+  int dbg;        // timing experiments only: bit 0 skip W statistics, 1 lambda, 2 projection, 3 phi
 };
 
 // shared-memory layout (bytes): S x Hs | Ws | gs | Qs | S x per-warp X rows |
-// per warp: phi [2][N][32], red [32][8 IT]
+// lambda tile | phi [FB][2][N][32] (the W-statistic slice reduction reuses
+// the Hs ring after the frame loop)
 struct BpLayout {
-  size_t hs_stride, o_ws, o_gs, o_q, o_rows0, rows_stride, o_warp, warp_bytes, total;
+  size_t hs_stride, o_ws, o_gs, o_q, o_rows0, rows_stride, o_lam, o_ph, total;
   int rowp;
-  __host__ __device__ BpLayout(int rs, int N, int K, int M, int MP, int FB, int IT, int S) {
+  __host__ __device__ BpLayout(int rs, int N, int K, int M, int MP, int FB, int S) {
     hs_stride = al16((size_t)rs * N * FTC * kp_of(K));
-    o_ws = S * hs_stride;
+    const int NI = N * ((FB + 1) / 2) * (k4_of(K) / 4);  // W-statistic items
+    size_t ring = S * hs_stride, red = (size_t)rs * (NI > 32 * FB ? NI : 32 * FB) * 16;
+    o_ws = al16(ring > red ? ring : red);
     o_gs = o_ws + al16((size_t)rs * FB * N * kp_of(K));
     o_q = o_gs + al16((size_t)rs * FB * N * MP);
     o_rows0 = o_q + al16((size_t)2 * rs * FB * M * M);
     rowp = row_pitch(2 * rs * M);
     rows_stride = al16((size_t)FB * FTC * rowp);
-    warp_bytes = al16((size_t)rs * (2 * N * FTC + 32 * 8 * IT));
-    o_warp = o_rows0 + S * rows_stride;
-    total = o_warp + (size_t)FB * warp_bytes;
+    o_lam = o_rows0 + S * rows_stride;
+    o_ph = o_lam + al16((size_t)rs * N * FB * FTC);
+    total = o_ph + al16((size_t)rs * FB * 2 * N * FTC);
   }
   __host__ __device__ size_t hs(int buf) const { return buf * hs_stride; }
   __host__ __device__ size_t rows(int buf) const { return o_rows0 + buf * rows_stride; }
@@ -727,17 +799,17 @@ __global__ void __launch_bounds__(256) k_bpass(BpArgs<R> a) {
   pdl_entry();
   using C = cplx<R>;
   extern __shared__ __align__(16) unsigned char smraw[];
-  const int FB = blockDim.x / FTC;
+  const int FB = blockDim.x / FTC, BSZ = blockDim.x;
   const int N = NN ? NN : a.N, K = a.K, M = a.M, F = a.F, T = a.T;
   const int K4 = KC ? KC : k4_of(K), KP = K4 + 4, KQ = K4 / 4;
   const int S = a.S;
-  const BpLayout L((int)sizeof(R), N, K, M, MP, FB, IT, S);
+  const BpLayout L((int)sizeof(R), N, K, M, MP, FB, S);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   R* Ws = reinterpret_cast<R*>(smraw + L.o_ws);
   R* gs = reinterpret_cast<R*>(smraw + L.o_gs);
   C* Qs = reinterpret_cast<C*>(smraw + L.o_q);
-  R* phw = reinterpret_cast<R*>(smraw + L.o_warp + (size_t)warp * L.warp_bytes);  // [2][N][32]
-  R* red = phw + 2 * N * FTC;                                                       // [32][8 IT]
+  R* lam_s = reinterpret_cast<R*>(smraw + L.o_lam);  // [N][FB][32]
+  R* ph = reinterpret_cast<R*>(smraw + L.o_ph);      // [FB][2][N][32]
   __shared__ double dred[8];
   __shared__ unsigned last;
   const int seg = blockIdx.x, nseg = gridDim.x, b = blockIdx.z, fblk = blockIdx.y;
@@ -750,7 +822,7 @@ __global__ void __launch_bounds__(256) k_bpass(BpArgs<R> a) {
   R* xtp = a.xt + ((size_t)b * F + (fv ? f : 0)) * T * M + (size_t)lane * M;  // + t0 M
   const int rb = M * (int)sizeof(C);
   auto issue = [&](int t0, int buf) {
-    stage_h_async<R, NN, KC>(reinterpret_cast<R*>(smraw + L.hs(buf)), Htb, N, K4, T, t0, tb, tid, blockDim.x);
+    stage_h_async<R, NN, KC>(reinterpret_cast<R*>(smraw + L.hs(buf)), Htb, N, K4, T, t0, tb, tid, BSZ);
     const int t = t0 + lane;
     const bool v = fv && t < tb;
     row_async(smraw + L.rows(buf) + (size_t)(warp * FTC + lane) * L.rowp,
@@ -758,7 +830,7 @@ __global__ void __launch_bounds__(256) k_bpass(BpArgs<R> a) {
               rb, v, reinterpret_cast<const unsigned char*>(Xb));
   };
   stage_wg_async<R, MP, NN>(Ws, gs, Wb, a.g + (size_t)b * N * F * M, N, F, K, M, f0, F, lane, warp);
-  for (int e = tid; e < FB * M * M; e += blockDim.x) {
+  for (int e = tid; e < FB * M * M; e += BSZ) {
     const int fl = e / (M * M), ff = f0 + fl;
     Qs[e] = ff < F ? a.Q[((size_t)b * F + ff) * M * M + e % (M * M)] : cmake<C>(0.0, 0.0);
   }
@@ -767,23 +839,27 @@ __global__ void __launch_bounds__(256) k_bpass(BpArgs<R> a) {
     cp_async_commit();
   }
   const R fl = a.floorp[b];
-  const WarpItems wi(N * KQ, lane);
-  R a1[IT][4], a2[IT][4];
+  // W-statistic items of this thread
+  const int FP = (FB + 1) / 2, NI = N * FP * KQ;
+  const int SL = NI <= BSZ ? BSZ / NI : 1;
+  const int slice = NI <= BSZ ? tid / NI : 0;
+  int jn[IT], jf[IT], jk[IT];  // source, first bin, k offset (jn = -1: none)
+#pragma unroll
+  for (int i = 0; i < IT; ++i) {
+    const int j = NI <= BSZ ? (i == 0 ? tid % NI : NI) : tid + BSZ * i;
+    const bool has = j < NI && slice < SL;
+    jn[i] = has ? j / (FP * KQ) : -1;
+    jf[i] = has ? 2 * ((j / KQ) % FP) : 0;
+    jk[i] = has ? (j % KQ) * 4 : 0;
+  }
+  R acc[IT][16];  // [bin 0/1][num/den][4 k]
 #pragma unroll
   for (int i = 0; i < IT; ++i)
 #pragma unroll
-    for (int c = 0; c < 4; ++c) a1[i][c] = a2[i][c] = R(0);
+    for (int c = 0; c < 16; ++c) acc[i][c] = R(0);
   double ll = 0.0;
   const R* gw = gs + warp * N * MP;
   const C* Qw = Qs + warp * M * M;
-  int bn_[IT], bk_[IT];  // this lane's W-statistic items: source, k offset (-1: none)
-#pragma unroll
-  for (int i = 0; i < IT; ++i) {
-    const int j = wi.NI <= 32 ? wi.item : lane + 32 * i;
-    const bool has = (wi.NI <= 32 && i == 0 && wi.slice >= 0) || (wi.NI > 32 && j < wi.NI);
-    bn_[i] = has ? j / KQ : -1;
-    bk_[i] = has ? (j % KQ) * 4 : 0;
-  }
   int buf = 0;
   for (int t0 = ta; t0 < tb; t0 += FTC, buf = (buf + 1 == S) ? 0 : buf + 1) {
     cp_async_wait_n(S - 2);
@@ -791,6 +867,7 @@ __global__ void __launch_bounds__(256) k_bpass(BpArgs<R> a) {
     if (t0 + (S - 1) * FTC < tb) issue(t0 + (S - 1) * FTC, buf == 0 ? S - 1 : buf - 1);
     cp_async_commit();
     const R* Hs = reinterpret_cast<const R*>(smraw + L.hs(buf));
+    if (!(a.dbg & 2)) lam_tile<R, NN, KC>(Ws, Hs, lam_s, N, K4, FB, warp, lane);
     const bool v = fv && t0 + lane < tb;
     // projection x~_i = |q_i^H x|^2 (row i of Q = q_i^H; _kernels.py:339-350)
     C xv[MP];
@@ -807,6 +884,7 @@ __global__ void __launch_bounds__(256) k_bpass(BpArgs<R> a) {
 #pragma unroll
     for (int i = 0; i < MP; ++i) {
       xtv[i] = R(0);
+      if (a.dbg & 4) { xtv[i] = xv[i].x; continue; }
       if (i < M) {
         C s = cmake<C>(0.0, 0.0);
 #pragma unroll
@@ -830,8 +908,10 @@ __global__ void __launch_bounds__(256) k_bpass(BpArgs<R> a) {
           if (m < M) xo[m] = xtv[m];
       }
     }
+    __syncthreads();  // lambda tile complete
     R l[NMAX];
-    lam_point<R, NN, KC>(Ws + warp * N * KP, Hs, lane, N, K4, l);
+#pragma unroll
+    for (int n = 0; n < NMAX; ++n) l[n] = n < N ? lam_s[(n * FB + warp) * FTC + lane] : R(0);
     R y[MP], iy[MP];
     power_point<R, MP, NN>(l, gw, N, M, fl, v, y, iy);
     if (v) {
@@ -844,84 +924,71 @@ __global__ void __launch_bounds__(256) k_bpass(BpArgs<R> a) {
     R xr[MP];
 #pragma unroll
     for (int m = 0; m < MP; ++m) xr[m] = xtv[m] * iy[m] * iy[m];
+    R* pw = ph + warp * 2 * N * FTC;
 #pragma unroll
     for (int n = 0; n < NMAX; ++n) {
-      if (n >= N) break;
+      if (n >= N || (a.dbg & 8)) break;
       R p1, p2;
-      phi_of<R, MP>(xr, iy, gw, n, p1, p2);
-      phw[n * FTC + lane] = p1;
-      phw[(N + n) * FTC + lane] = p2;
+      phi_of<R, MP>(xr, iy, gw, n, p1, p2);  // 0 on invalid frames (iy = 0)
+      pw[n * FTC + lane] = p1;
+      pw[(N + n) * FTC + lane] = p2;
     }
-    __syncwarp();
+    __syncthreads();  // phi of every bin
 #pragma unroll
     for (int i = 0; i < IT; ++i) {
-      if (bn_[i] >= 0) {
-        const int n = bn_[i];
-        const R* h0 = Hs + n * FTC * KP + bk_[i];
-        for (int tl = wi.slice; tl < FTC; tl += wi.S) {
-          const R p1 = phw[n * FTC + tl], p2 = phw[(N + n) * FTC + tl];
-          R h4[4];
-          lds4(h0 + tl * KP, h4);
+      if (jn[i] < 0 || (a.dbg & 1)) continue;
+      const int n = jn[i];
+      const R* h0 = Hs + n * FTC * KP + jk[i];
+      const R* pa = ph + jf[i] * 2 * N * FTC + n * FTC;  // bin jf: phi1 at +0, phi2 at + N 32
+      const R* pb = pa + 2 * N * FTC;                    // bin jf + 1
+      for (int tl = slice; tl < FTC; tl += SL) {
+        R h4[4];
+        lds4(h0 + tl * KP, h4);
+        const R a1 = pa[tl], a2 = pa[N * FTC + tl], b1 = pb[tl], b2 = pb[N * FTC + tl];
 #pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            a1[i][c] += p1 * h4[c];
-            a2[i][c] += p2 * h4[c];
-          }
+        for (int c = 0; c < 4; ++c) {
+          acc[i][c] += a1 * h4[c];
+          acc[i][4 + c] += a2 * h4[c];
+          acc[i][8 + c] += b1 * h4[c];
+          acc[i][12 + c] += b2 * h4[c];
         }
       }
     }
-    __syncwarp();
   }
   cp_async_wait<0>();
   // data-term partial of this CTA (fixed order: lanes, then warps)
   ll = warp_sum(ll);
   if (lane == 0) dred[warp] = ll;
-  __syncthreads();
+  __syncthreads();  // also: every thread is past its last read of the Hs ring
   const int nfb = gridDim.y;
   if (tid == 0) {
     double s = 0.0;
     for (int w = 0; w < FB; ++w) s += dred[w];
     a.llp[((size_t)b * nfb + fblk) * nseg + seg] = s;
   }
-  // W statistics: slice sums in order -> this segment's partial
-  if (wi.slice >= 0) {
+  // W statistics: slice partials (in the Hs ring) summed in slice order ->
+  // this segment's partial (bin, 2, N, K4)
+  R* red = reinterpret_cast<R*>(smraw);  // [slice][item][16] or [thread][IT][16]
 #pragma unroll
-    for (int i = 0; i < IT; ++i)
+  for (int i = 0; i < IT; ++i) {
+    if (jn[i] < 0) continue;
+    const int j = NI <= BSZ ? tid % NI : tid + BSZ * i;
+    const int row = NI <= BSZ ? slice * NI + j : j;
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        red[(lane * IT + i) * 8 + c] = a1[i][c];
-        red[(lane * IT + i) * 8 + 4 + c] = a2[i][c];
-      }
+    for (int c = 0; c < 16; ++c) red[(size_t)row * 16 + c] = acc[i][c];
   }
-  __syncwarp();
+  __syncthreads();
   const size_t PW = (size_t)2 * N * K4;  // one (bin, segment) partial
-  if (fv) {
-    for (int j = lane; j < wi.NI; j += 32) {
-      R sn[4] = {0, 0, 0, 0}, sd[4] = {0, 0, 0, 0};
-      if (wi.NI <= 32) {
-        for (int s = 0; s < wi.S; ++s) {
-          const R* r = red + ((s * wi.NI + j) * IT) * 8;
-#pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            sn[c] += r[c];
-            sd[c] += r[4 + c];
-          }
-        }
-      } else {
-        const R* r = red + (lane * IT + (j - lane) / 32) * 8;
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          sn[c] = r[c];
-          sd[c] = r[4 + c];
-        }
-      }
-      R* pb = a.part + (((size_t)b * F + f) * nseg + seg) * PW;
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        pb[j * 4 + c] = sn[c];
-        pb[(size_t)N * K4 + j * 4 + c] = sd[c];
-      }
-    }
+  for (int e = tid; e < NI * 16; e += BSZ) {
+    const int j = e / 16, c = e % 16;
+    R sum = 0;
+    const int nsl = NI <= BSZ ? SL : 1;
+    for (int s = 0; s < nsl; ++s) sum += red[(size_t)(s * NI + j) * 16 + c];
+    const int n = j / (FP * KQ), fb = 2 * ((j / KQ) % FP) + c / 8, k = (j % KQ) * 4 + c % 4;
+    const int nd = (c / 4) % 2;
+    const int ff = f0 + fb;
+    if (fb < FB && ff < F)
+      a.part[(((size_t)b * F + ff) * nseg + seg) * PW + (size_t)nd * N * K4 + n * K4 + k] = sum;
   }
   __threadfence();
   __syncthreads();
@@ -932,7 +999,7 @@ __global__ void __launch_bounds__(256) k_bpass(BpArgs<R> a) {
   if (tid == 0) a.cnt[(size_t)b * nfb + fblk] = 0;  // re-armed
   // W MU for the FB bins of this block (sources.py:191-194), segments in order
   R* Wnb = a.Wn + (size_t)b * N * F * K;
-  for (int e = tid; e < FB * N * K; e += blockDim.x) {
+  for (int e = tid; e < FB * N * K; e += BSZ) {
     const int k = e % K, r = e / K, n = r % N, fl2 = r / N, ff = f0 + fl2;
     if (ff >= F) continue;
     const R* pb = a.part + ((size_t)b * F + ff) * nseg * PW;

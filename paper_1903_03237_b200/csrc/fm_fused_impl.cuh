@@ -34,10 +34,9 @@ inline int with_shape(int N, int K4, int FB, Fn&& fn) {
 
 // items per thread of k_hpass (8 warps) / per lane of k_bpass for a
 // compile-time (N, K4); 0 = take the plan's runtime value
-constexpr int pow2ceil4(int v) { return v <= 1 ? 1 : v <= 2 ? 2 : v <= 4 ? 4 : 8; }
-constexpr int hp_it(int NN, int KC) { return NN ? pow2ceil4((NN * (KC / 4) + 7) / 8) : 0; }
+constexpr int hp_it(int NN, int KC) { return NN ? (NN * (KC / hp_kch(KC)) + 7) / 8 : 0; }
 constexpr int bp_it(int NN, int KC) {
-  return NN ? (NN * (KC / 4) <= 32 ? 1 : pow2ceil4((NN * (KC / 4) + 31) / 32)) : 0;
+  return NN ? (NN * 4 * (KC / 4) <= 256 ? 1 : (NN * 4 * (KC / 4) + 255) / 256) : 0;
 }
 
 template <typename R>
@@ -82,9 +81,11 @@ int Impl<R>::hpass(const fm_dims* d, const fm_state* s, int mode, void* hout, cu
             FM_CHECK_LAUNCH("k_hpass");
           } else {
             FM_DISPATCH_IT(p.hIT, {
-              if (int rc = ensure_smem(k_hpass<R, MP, IT, 0, 0>, p.smem_h)) return rc;
-              launch_pdl(k_hpass<R, MP, IT, 0, 0>, grid, dim3(32 * p.FB), p.smem_h, st, a);
-              FM_CHECK_LAUNCH("k_hpass");
+              if constexpr (IT <= 4) {
+                if (int rc = ensure_smem(k_hpass<R, MP, IT, 0, 0>, p.smem_h)) return rc;
+                launch_pdl(k_hpass<R, MP, IT, 0, 0>, grid, dim3(32 * p.FB), p.smem_h, st, a);
+                FM_CHECK_LAUNCH("k_hpass");
+              }
             });
           }
           return FM_OK;
@@ -140,6 +141,8 @@ int Impl<R>::bpass(const fm_dims* d, const fm_state* s, cudaStream_t st) {
   a.llp = reinterpret_cast<double*>(w + p.off_llp);
   a.F = (int)d->F; a.T = (int)d->T; a.N = (int)d->N; a.K = (int)d->K; a.M = (int)d->M;
   a.TR = p.bTR; a.S = p.bS;
+  static const int dbg = [] { const char* e = getenv("FM_BP_DBG"); return e ? atoi(e) : 0; }();
+  a.dbg = dbg;
   const dim3 grid((unsigned)p.bseg, (unsigned)p.nfb, (unsigned)d->B);
   FM_DISPATCH_MP(d->M, {
     if (int rc = with_shape<R, MP>((int)d->N, k4_of((int)d->K), p.FB, [&](auto nn, auto kc) -> int {
@@ -151,7 +154,7 @@ int Impl<R>::bpass(const fm_dims* d, const fm_state* s, cudaStream_t st) {
             FM_CHECK_LAUNCH("k_bpass");
           } else {
             FM_DISPATCH_IT(p.bIT, {
-              if constexpr (IT <= 4) {
+              if constexpr (IT <= 2) {
                 if (int rc = ensure_smem(k_bpass<R, MP, IT, 0, 0>, p.smem_b)) return rc;
                 launch_pdl(k_bpass<R, MP, IT, 0, 0>, grid, dim3(32 * p.FB), p.smem_b, st, a);
                 FM_CHECK_LAUNCH("k_bpass");

@@ -152,10 +152,32 @@ inline int gseg_override() {
   return e ? atoi(e) : 0;
 }
 
+// Schedule of the plain iteration: the split ten-launch one (default; its
+// separate register-tiled NMF contractions measured faster on every BASELINE
+// config) or the fused five-pass one (FM_SCHEDULE=fused).
+inline bool use_fused(const fm_dims*) {
+  const char* e = getenv("FM_SCHEDULE");
+  return e && strcmp(e, "fused") == 0;
+}
+
+// FM_PASS_CTAS / FM_PASS_S: work-split and pipeline-depth knobs of the fused
+// statistics passes (A/B runs); read at every plan
+inline int pass_ctas_override() {
+  const char* e = getenv("FM_PASS_CTAS");
+  return e ? atoi(e) : 0;
+}
+inline int pass_stages_override() {
+  const char* e = getenv("FM_PASS_S");
+  const int v = e ? atoi(e) : 0;
+  return v < 2 ? 0 : v > 4 ? 4 : v;
+}
+
 // Everything outside fm_dims that changes which kernels an iteration
 // launches: part of the CUDA-graph cache key (fm_api.cu run_common).
 inline unsigned variant_key(const fm_dims* d) {
-  return (unsigned)vacc_mode(d) | ((unsigned)(gseg_override() & 0xffff) << 4);
+  return (unsigned)vacc_mode(d) | ((unsigned)(gseg_override() & 0xff) << 4) |
+         ((unsigned)(pass_ctas_override() & 0xffff) << 12) | ((unsigned)pass_stages_override() << 28) |
+         ((unsigned)use_fused(d) << 31);
 }
 
 inline Plan make_plan(const fm_dims* d) {
@@ -206,27 +228,56 @@ inline Plan make_plan(const fm_dims* d) {
   {
     const int K = (int)d->K, K4 = k4_of(K), KQ = K4 / 4;
     const int MPv = M <= 4 ? 4 : M <= 8 ? 8 : 16;
-    p.bIT = N * KQ <= 32 ? 1 : (int)((N * KQ + 31) / 32);
-    p.bIT = p.bIT <= 1 ? 1 : p.bIT <= 2 ? 2 : 4;
     p.FB = 8;
+    // work split: enough CTAs that every SM holds several (FM_PASS_CTAS
+    // overrides the target for A/B runs)
+    const long long want = pass_ctas_override() > 0 ? pass_ctas_override() : 8 * 148;
+    const long long chunks = (T + FTC - 1) / FTC;
+    auto split = [&](int FB) {
+      p.nfb = (int)((F + FB - 1) / FB);
+      auto segs_for = [&](long long ctas, int& TRo, int& nsego) {
+        long long sg = std::max<long long>(1, (want + ctas - 1) / ctas);
+        sg = std::min(sg, chunks);
+        const long long tr = (chunks + sg - 1) / sg * FTC;
+        TRo = (int)tr;
+        nsego = (int)((T + tr - 1) / tr);
+      };
+      segs_for((long long)p.nfb * B, p.gTR, p.gseg);
+      segs_for((long long)p.nfb * B, p.bTR, p.bseg);
+      p.htl = (int)chunks;
+    };
     auto fit = [&](int FB, int& NS, int& NG, int& IT) {
+      split(FB);
+      // k_bpass: W-statistic items (source, bin pair, k-quad) per thread
+      const long long NIb = N * ((FB + 1) / 2) * KQ;
+      p.bIT = NIb <= 32 * FB ? 1 : (int)((NIb + 32 * FB - 1) / (32 * FB));
+      p.bIT = p.bIT <= 1 ? 1 : p.bIT <= 2 ? 2 : 4;
+      // k_hpass: (source, k chunk) items per thread, <= 4 (source groups beyond)
+      const int KO = K4 / hp_kch(K4);
       NG = 1;
       NS = (int)N;
-      IT = (NS * KQ + FB - 1) / FB;
-      while (IT > 8) {
+      IT = (NS * KO + FB - 1) / FB;
+      while (IT > 4) {
         ++NG;
         NS = (int)((N + NG - 1) / NG);
-        IT = (NS * KQ + FB - 1) / FB;
+        IT = (NS * KO + FB - 1) / FB;
       }
-      IT = IT <= 1 ? 1 : IT <= 2 ? 2 : IT <= 4 ? 4 : 8;
-      // cp.async stages: the deepest of 4..2 that keeps two CTAs per SM
-      // (<= 112 KB), else the deepest that fits one
-      auto pick = [&](auto total_of, int& S, size_t& bytes) {
-        for (int pass = 0; pass < 2; ++pass) {
-          const size_t cap = pass == 0 ? (size_t)112 * 1024 : (size_t)200 * 1024;
-          for (S = 4; S >= 2; --S) {
+      IT = IT <= 1 ? 1 : IT <= 2 ? 2 : 4;
+      const long long hct = chunks * B * NG;
+      long long hs = std::max<long long>(1, (want + hct - 1) / hct);
+      hs = std::min<long long>(hs, (F + FB - 1) / FB);
+      p.hHFR = (int)(((F + hs - 1) / hs + FB - 1) / FB * FB);
+      p.hHS = (int)((F + p.hHFR - 1) / p.hHFR);
+      // cp.async stages: no deeper than the chunks (steps) a CTA walks, 2..4;
+      // then the deepest that keeps >= 3 CTAs per SM (<= 72 KB), else 2, else 1
+      auto pick = [&](auto total_of, int steps, int& S, size_t& bytes) {
+        const int smax = (int)std::max<long long>(2, std::min<long long>(4, steps));
+        const int so = pass_stages_override();
+        for (size_t cap : {(size_t)72 * 1024, (size_t)112 * 1024, (size_t)200 * 1024}) {
+          for (S = so ? so : smax; S >= 2; --S) {
             bytes = total_of(S);
             if (bytes <= cap) return true;
+            if (so) break;
           }
         }
         S = 2;
@@ -234,32 +285,15 @@ inline Plan make_plan(const fm_dims* d) {
         return false;
       };
       bool ok = pick([&](int S) { return GpLayout((int)rs, (int)N, K, (int)M, MPv, FB, S).total; },
-                     p.gS, p.smem_g);
-      ok = pick([&](int S) { return BpLayout((int)rs, (int)N, K, (int)M, MPv, FB, p.bIT, S).total; },
-                p.bS, p.smem_b) && ok;
+                     p.gTR / FTC, p.gS, p.smem_g);
+      ok = pick([&](int S) { return BpLayout((int)rs, (int)N, K, (int)M, MPv, FB, S).total; },
+                p.bTR / FTC, p.bS, p.smem_b) && ok;
       ok = pick([&](int S) { return HpLayout((int)rs, (int)N, K, (int)M, MPv, FB, NS, S).total; },
-                p.hS, p.smem_h) && ok;
+                p.hHFR / FB, p.hS, p.smem_h) && ok;
       return ok;
     };
     while (p.FB > 1 && !fit(p.FB, p.hNS, p.hNG, p.hIT)) p.FB /= 2;
     fit(p.FB, p.hNS, p.hNG, p.hIT);
-    p.nfb = (int)((F + p.FB - 1) / p.FB);
-    const long long want = 3 * 148, chunks = (T + FTC - 1) / FTC;
-    auto segs_for = [&](long long ctas, int& TRo, int& nsego) {
-      long long sg = std::max<long long>(1, (want + ctas - 1) / ctas);
-      sg = std::min(sg, chunks);
-      long long tr = (chunks + sg - 1) / sg * FTC;
-      TRo = (int)tr;
-      nsego = (int)((T + tr - 1) / tr);
-    };
-    segs_for((long long)p.nfb * B, p.gTR, p.gseg);
-    segs_for((long long)p.nfb * B, p.bTR, p.bseg);
-    p.htl = (int)chunks;
-    const long long hct = chunks * B * p.hNG;
-    long long hs = std::max<long long>(1, (want + hct - 1) / hct);
-    hs = std::min<long long>(hs, p.nfb);
-    p.hHFR = (int)(((F + hs - 1) / hs + p.FB - 1) / p.FB * p.FB);
-    p.hHS = (int)((F + p.hHFR - 1) / p.hHFR);
   }
   const size_t gpart_f = (size_t)B * F * p.gseg * N * 2 * M;
   size_t o = 0;
@@ -307,7 +341,11 @@ template <typename R> struct Impl {
 
   static int prologue(const fm_dims* d, const fm_state* s, cudaStream_t st, bool reset = true);
   static int iterate_phase(const fm_dims* d, const fm_state* s, int phase, void* hstat,
-                           cudaStream_t st, cudaEvent_t* ev = nullptr);  // ev: 10 events
+                           cudaStream_t st, cudaEvent_t* ev = nullptr);  // ev: 11 / 7 events
+  static int iterate_split(const fm_dims* d, const fm_state* s, int phase, void* hstat,
+                           cudaStream_t st, cudaEvent_t* ev);
+  static int iterate_fused(const fm_dims* d, const fm_state* s, int phase, void* hstat,
+                           cudaStream_t st, cudaEvent_t* ev);
   static int lambda(const fm_dims* d, const R* W, const R* H, R* lam, cudaStream_t st);
   static int gain(const fm_dims* d, const fm_state* s, cudaStream_t st);
   static int vacc(const fm_dims* d, const fm_state* s, cudaStream_t st);
@@ -419,7 +457,7 @@ int Impl<R>::vacc(const fm_dims* d, const fm_state* s, cudaStream_t st) {
   a.gnew = reinterpret_cast<R*>(w + p.off_gnew);
   a.part = reinterpret_cast<R*>(w + p.off_vpart);
   a.F = (int)d->F; a.T = (int)d->T; a.N = (int)d->N; a.TR = p.TR;
-  a.gseg = d->dp ? p.nseg : p.gseg;  // k_gain (deep prior) or k_gpass partials
+  a.gseg = (d->dp || !use_fused(d)) ? p.nseg : p.gseg;  // k_gain or k_gpass partials
   static const int dbg = [] { const char* e = getenv("FM_VTC_DBG"); return e ? atoi(e) : 0; }();
   a.dbg = dbg;
   dim3 grid((unsigned)p.nseg, (unsigned)d->F, (unsigned)d->B);
@@ -465,7 +503,7 @@ int Impl<R>::ip(const fm_dims* d, const fm_state* s, cudaStream_t st, R* u) {
   a.g = reinterpret_cast<R*>(s->g);
   a.W = reinterpret_cast<R*>(s->W);
   // plain FastMNMF: the W-stepped Wn (k_bpass) is absorbed into the state W
-  a.Wsrc = d->dp ? a.W : reinterpret_cast<const R*>(w + p.off_wn);
+  a.Wsrc = (d->dp || !use_fused(d)) ? a.W : reinterpret_cast<const R*>(w + p.off_wn);
   a.cs_out = reinterpret_cast<R*>(w + p.off_cs);
   a.ld_part = reinterpret_cast<double*>(w + p.off_ldp);
   a.iter = reinterpret_cast<const unsigned*>(w + p.off_cnt) + 1;
@@ -524,7 +562,8 @@ int Impl<R>::trace(const fm_dims* d, const fm_state* s, cudaStream_t st) {
   unsigned* itp = reinterpret_cast<unsigned*>(w + p.off_cnt) + 1;
   // data-term partials: (B, F, ntile) from k_back (deep prior), (B, nfb, bseg)
   // from k_bpass
-  const int np1 = d->dp ? (int)d->F : p.nfb, np2 = d->dp ? p.ntile : p.bseg;
+  const bool fz = !d->dp && use_fused(d);
+  const int np1 = fz ? p.nfb : (int)d->F, np2 = fz ? p.bseg : p.ntile;
   launch_pdl(k_trace, dim3((unsigned)d->B), dim3(256), 0, st,
              reinterpret_cast<const double*>(w + p.off_llp),
              reinterpret_cast<const double*>(w + p.off_ldp), s->trace, itp, (int)d->B, np1, np2,
@@ -543,14 +582,115 @@ int Impl<R>::prologue(const fm_dims* d, const fm_state* s, cudaStream_t st, bool
   const Plan p = make_plan(d);
   unsigned char* w = reinterpret_cast<unsigned char*>(s->work);
   if (reset) FM_CUDA(cudaMemsetAsync(w + p.off_cnt, 0, p.total - p.off_cnt, st));
-  // Ht from H, then x~ of the initial Q, the data term of the initial state
-  // and the first iteration's W step (separate.py:183, :186-193, :214-216)
+  if (!use_fused(d)) {  // split: lambda, then x~, data term and phi of the initial state
+    if (int rc = lambda(d, reinterpret_cast<const R*>(s->W), reinterpret_cast<const R*>(s->H),
+                        reinterpret_cast<R*>(w + p.off_lam), st))
+      return rc;
+    return back(d, s, /*tail_only=*/1, /*record=*/0, st);
+  }
+  // fused: Ht from H, then x~ of the initial Q, the data term of the initial
+  // state and the first iteration's W step (separate.py:183, :186-193, :214-216)
   if (int rc = hstore(d, s, nullptr, st)) return rc;
   return bpass(d, s, st);
 }
 
+// The split schedule (ten launches; phi and lambda through HBM):
+//   k_wstats  W step from the phi the previous k_back wrote  (separate.py:214-216 "W")
+//   k_lambda, k_phi  refresh with the new W
+//   k_hstats  H step                                        (separate.py:214-216 "H")
+//   k_lambda  refresh with the new H
+//   k_gain, k_vacc, k_ip  gains, V, IP, normalisations       (separate.py:217-233)
+//   k_back    x~ = |Qx|^2, data term, phi for the next W step (separate.py:230; :186-193)
+//   k_trace
+template <typename R>
+int Impl<R>::iterate_split(const fm_dims* d, const fm_state* s, int phase, void* hstat,
+                           cudaStream_t st, cudaEvent_t* ev) {
+#define FM_EV(i) \
+  if (ev) FM_CUDA(cudaEventRecordWithFlags(ev[i], st, cudaEventRecordExternal));
+  const Plan p = make_plan(d);
+  unsigned char* w = reinterpret_cast<unsigned char*>(s->work);
+  R* lam = reinterpret_cast<R*>(w + p.off_lam);
+  R* phi = reinterpret_cast<R*>(w + p.off_phi);
+  R* W = reinterpret_cast<R*>(s->W);
+  R* H = reinterpret_cast<R*>(s->H);
+  const int N = (int)d->N, F = (int)d->F, T = (int)d->T, K = (int)d->K;
+  const int n0 = d->dp ? 1 : 0;
+  const unsigned BN = (unsigned)(d->B * (d->N - n0));
+  if (phase == 0 || phase == 2) {
+    // W step (separate.py:214-216 with step "W"): statistics from the phi of the
+    // previous pass, MU, then the refresh with the new W (lambda + phi)
+    FM_EV(0);
+    FM_DISPATCH_KB(K, {
+      FM_DISPATCH_TILE(p.FT, FTT, {
+        if constexpr (FTT <= 32) {
+          const size_t smw = WsCfg<R, KB, FTT>::bytes;
+          if (int rc = ensure_smem(k_wstats<R, KB, FTT>, smw)) return rc;
+          launch_pdl(k_wstats<R, KB, FTT>, dim3((unsigned)((F + FTT - 1) / FTT), BN), dim3(256),
+                     smw, st, phi, H, W, N, F, T, K, 0);
+          FM_CHECK_LAUNCH("k_wstats");
+        }
+      });
+    });
+    FM_EV(1);
+    if (int rc = lambda(d, W, H, lam, st)) return rc;
+    FM_EV(2);
+    FM_DISPATCH_M(d->M, {
+      launch_pdl(k_phi<R, MM>, dim3((unsigned)((T + 255) / 256), (unsigned)F, (unsigned)d->B),
+                 dim3(256), 0, st, lam, reinterpret_cast<const R*>(s->xt),
+                 reinterpret_cast<const R*>(s->g), reinterpret_cast<const R*>(s->floor), phi, N, F,
+                 T);
+      FM_CHECK_LAUNCH("k_phi");
+    });
+    // H step (separate.py:214-216 with step "H")
+    FM_EV(3);
+    FM_DISPATCH_KB(K, {
+      FM_DISPATCH_TILE(p.TT, TTT, {
+        if constexpr (TTT >= 16) {
+          const size_t smh = HsCfg<R, KB, TTT>::bytes;
+          if (int rc = ensure_smem(k_hstats<R, KB, TTT>, smh)) return rc;
+          launch_pdl(k_hstats<R, KB, TTT>, dim3((unsigned)((T + TTT - 1) / TTT), BN, (unsigned)p.HS),
+                     dim3(256), smh, st, phi, W, H, reinterpret_cast<R*>(hstat), N, F, T, K,
+                     phase == 0 ? 1 : 0, 0, p.HFR, reinterpret_cast<R*>(w + p.off_hpart),
+                     reinterpret_cast<unsigned*>(w + p.off_hcnt));
+          FM_CHECK_LAUNCH("k_hstats");
+        }
+      });
+    });
+  }
+  if (phase == 0) return FM_OK;
+  if (phase == 1) {
+    const long long NKT = (long long)N * K * T, total = (long long)d->B * NKT;
+    k_hupdate<R><<<(unsigned)((total + 255) / 256), 256, 0, st>>>(
+        nullptr, H, reinterpret_cast<R*>(hstat), 1, NKT, total, 2);
+    FM_CHECK_LAUNCH("k_hupdate");
+  }
+  FM_EV(4);
+  if (int rc = lambda(d, W, H, lam, st)) return rc;  // refresh after the H step
+  FM_EV(5);
+  if (int rc = gain(d, s, st)) return rc;
+  FM_EV(6);
+  if (int rc = vacc(d, s, st)) return rc;
+  FM_EV(7);
+  if (int rc = ip(d, s, st)) return rc;
+  FM_EV(8);
+  if (int rc = back(d, s, /*tail_only=*/0, /*record=*/1, st)) return rc;
+  FM_EV(9);
+  if (int rc = trace(d, s, st)) return rc;  // trace entry, then the iteration counter
+  FM_EV(10);
+  return FM_OK;
+#undef FM_EV
+}
+
 template <typename R>
 int Impl<R>::iterate_phase(const fm_dims* d, const fm_state* s, int phase, void* hstat,
+                           cudaStream_t st, cudaEvent_t* ev) {
+  if (d->dp) { set_error("deep-prior dims: use fm_iterate_dp"); return FM_EINVAL; }
+  return use_fused(d) ? iterate_fused(d, s, phase, hstat, st, ev)
+                      : iterate_split(d, s, phase, hstat, st, ev);
+}
+
+template <typename R>
+int Impl<R>::iterate_fused(const fm_dims* d, const fm_state* s, int phase, void* hstat,
                            cudaStream_t st, cudaEvent_t* ev) {
 #define FM_EV(i) \
   if (ev) FM_CUDA(cudaEventRecordWithFlags(ev[i], st, cudaEventRecordExternal));
