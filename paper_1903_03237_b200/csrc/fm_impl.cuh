@@ -23,6 +23,7 @@
 #include "fm_stft.cuh"
 #include "fm_fullrank.cuh"
 #include "fm_fused.cuh"
+#include "fm_ipw.cuh"
 
 namespace fm {
 
@@ -160,6 +161,15 @@ inline bool use_fused(const fm_dims*) {
   return e && strcmp(e, "fused") == 0;
 }
 
+// IP kernel: one warp per bin (k_ip_w, M <= 8) for many bins, the multi-warp
+// k_ip otherwise; FM_IP=w|cta forces one (A/B runs, tests)
+inline bool ip_warp_mode(const fm_dims* d) {
+  const char* e = getenv("FM_IP");
+  if (e && strcmp(e, "w") == 0) return d->M <= 8;
+  if (e && strcmp(e, "cta") == 0) return false;
+  return d->M <= 8 && d->B * d->F >= 4 * 148 * 4;
+}
+
 // FM_PASS_CTAS / FM_PASS_S: work-split and pipeline-depth knobs of the fused
 // statistics passes (A/B runs); read at every plan
 inline int pass_ctas_override() {
@@ -177,7 +187,7 @@ inline int pass_stages_override() {
 inline unsigned variant_key(const fm_dims* d) {
   return (unsigned)vacc_mode(d) | ((unsigned)(gseg_override() & 0xff) << 4) |
          ((unsigned)(pass_ctas_override() & 0xffff) << 12) | ((unsigned)pass_stages_override() << 28) |
-         ((unsigned)use_fused(d) << 31);
+         ((unsigned)use_fused(d) << 31) | ((unsigned)ip_warp_mode(d) << 3);
 }
 
 inline Plan make_plan(const fm_dims* d) {
@@ -514,12 +524,29 @@ int Impl<R>::ip(const fm_dims* d, const fm_state* s, cudaStream_t st, R* u) {
   a.f_offset = d->f_offset;
   a.normalize = d->normalize;
   a.ip_sweeps = d->ip_sweeps;
+  a.B = (int)d->B;
   dim3 grid((unsigned)d->F, (unsigned)d->B);
   FM_DISPATCH_M(d->M, {
-    const size_t sm = IpSmem<R, MM>::bytes;
-    if (int rc = ensure_smem(k_ip<R, MM>, sm)) return rc;
-    launch_pdl(k_ip<R, MM>, grid, dim3(IpCfg<MM>::BS), sm, st, a);
-    FM_CHECK_LAUNCH("k_ip");
+    // many bins (batches): one warp per bin (fm_ipw.cuh) -- c2 k_ip 1.20 ->
+    // 0.53 ms; few bins: the multi-warp k_ip, whose per-bin chain is shorter
+    // (c1: 24.6 vs 36.9 us)
+    if constexpr (MM <= 8) {
+      if (ip_warp_mode(d)) {
+        const size_t sm = IpwSmem<R, MM>::bytes * IPW_WARPS;
+        if (int rc = ensure_smem(k_ip_w<R, MM>, sm)) return rc;
+        const long long nb = d->B * d->F;
+        launch_pdl(k_ip_w<R, MM>, dim3((unsigned)((nb + IPW_WARPS - 1) / IPW_WARPS)),
+                   dim3(32 * IPW_WARPS), sm, st, a);
+        FM_CHECK_LAUNCH("k_ip_w");
+        return FM_OK;
+      }
+    }
+    {
+      const size_t sm = IpSmem<R, MM>::bytes;
+      if (int rc = ensure_smem(k_ip<R, MM>, sm)) return rc;
+      launch_pdl(k_ip<R, MM>, grid, dim3(IpCfg<MM>::BS), sm, st, a);
+      FM_CHECK_LAUNCH("k_ip");
+    }
   });
   return FM_OK;
 }

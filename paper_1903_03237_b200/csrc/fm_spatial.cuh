@@ -391,6 +391,7 @@ template <typename R> struct IpArgs {
   int F, N, K;
   long long f_offset;
   int normalize, ip_sweeps;
+  int B;  // mixtures (k_ip_w's flat (mixture, bin) grid)
 };
 
 template <int M> struct IpCfg {
