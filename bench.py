@@ -31,6 +31,7 @@ import time
 import numpy as np
 
 REPO = os.path.dirname(os.path.abspath(__file__))
+os.environ.setdefault("NCCL_DEBUG", "WARN")  # keep stdout to the one JSON line
 sys.path.insert(0, REPO)
 
 CONFIGS = {
@@ -46,6 +47,14 @@ CONFIGS = {
 }
 METRIC = "FastMNMF TF-bin*ch updates/s (F*T*M*mixtures*iterations/s)"
 UNIT = "TF-bin*ch/s"
+
+
+def _free_port():
+    import socket
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
 
 
 def dist_env():
@@ -266,16 +275,27 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--config", default="c1", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default=None, choices=sorted(CONFIGS))
+    ap.add_argument("--shard", action="store_true",
+                    help="c3: frequency-sharded path even at one rank (NCCL group of 1)")
     ap.add_argument("--iters", type=int, default=None, help="override iterations per step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
+    args.config_given = args.config is not None
+    args.config = args.config or "c1"
     args.warmup = max(args.warmup, 3)
     cfg = dict(CONFIGS[args.config])
     if args.iters:
         cfg["iters"] = args.iters
     world, rank, local = dist_env()
+    if world > 1 and not args.config_given:
+        # N > 1 measures the config that shards with an exchange: the long
+        # recording (config 3) split by frequency (strong scaling)
+        args.config = "c3"
+        cfg = dict(CONFIGS["c3"])
+        if args.iters:
+            cfg["iters"] = args.iters
 
     if args.impl == "reference":
         run_reference(args, cfg, world, rank)
@@ -298,7 +318,10 @@ def main():
 
     F, T, M, N, K, iters = cfg["F"], cfg["T"], cfg["M"], cfg["N"], cfg["K"], cfg["iters"]
     B_total = cfg["B"]
-    sharded_f = args.config == "c3" and world > 1
+    sharded_f = args.config == "c3" and (world > 1 or args.shard)
+    if sharded_f and world == 1:
+        dist.init_process_group("nccl", device_id=dev, rank=0, world_size=1,
+                                init_method=f"tcp://127.0.0.1:{_free_port()}")
     if args.config == "c2":
         b0, b1 = shard_batch(B_total, rank, world)
         cfg["B"] = b1 - b0
@@ -354,7 +377,7 @@ def main():
             loop.dp.v2.zero_()
             loop.dp.step.zero_()
 
-    use_graph = not sharded_f
+    use_graph = True  # sharded: phase 0 + NCCL all-reduce + phase 1 in one graph
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
 
     def step():
@@ -575,7 +598,7 @@ def main():
             "gpu_launches": launches, "clocks": clk,
         }
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if world > 1 or sharded_f:
         dist.barrier()
         dist.destroy_process_group()
 

@@ -72,6 +72,17 @@ class DeviceShardBackend:
                           ip_sweeps, n_trace=n_trace, f_offset=f_offset, hstat_allreduce=allreduce)
 
 
+class _Reducer:
+    """The H-statistic all-reduce callable, tagged with whether it may be
+    captured into a CUDA graph."""
+
+    def __init__(self, fn, capturable):
+        self.fn, self.capturable = fn, capturable
+
+    def __call__(self, buf):
+        self.fn(buf)
+
+
 class FrequencyShardedRun:
     """Frequency-sharded fast-mnmf over ``world`` ranks (config 3).
 
@@ -104,7 +115,8 @@ class FrequencyShardedRun:
         self.floor = 1e-12 * mx.cpu().numpy()
         Q, g, W, H = init_local
         self.loop = self.backend.make_loop(X_local, Q, g, W, H, self.floor, normalize, ip_sweeps,
-                                           n_iterations, self.f0, self._allreduce)
+                                           n_iterations, self.f0,
+                                           _Reducer(self._allreduce, self.capturable))
         self.n_iterations = n_iterations
 
     @staticmethod
@@ -114,9 +126,24 @@ class FrequencyShardedRun:
     def _allreduce(self, buf):
         self.dist.all_reduce(buf, group=self.group)
 
-    def run(self, n=None):
+    @property
+    def capturable(self):
+        """NCCL collectives can be captured into a CUDA graph with the
+        kernels around them; gloo's cannot."""
+        try:
+            return self.dist.get_backend(self.group) == "nccl"
+        except Exception:
+            return False
+
+    def run(self, n=None, use_graph=True):
+        """prologue + n iterations; with NCCL the per-iteration phase 0 ->
+        all-reduce -> phase 1 is one captured CUDA graph replayed n times."""
+        n = self.n_iterations if n is None else n
         self.loop.prologue()
-        self.loop.run(self.n_iterations if n is None else n)
+        if hasattr(self.loop, "hstat"):  # DeviceLoop
+            self.loop.run(n, use_graph=use_graph)
+        else:
+            self.loop.run(n)
 
     def trace(self):
         """Global likelihood trace (B, iterations): sum of the shard partials."""

@@ -264,6 +264,7 @@ class DeviceLoop:
                       if hstat_allreduce is not None else None)
         self.iterations_done = 0
         self._prologue_done = False
+        self._shard_graph = None
         self.dp = None
         if dp is not None:
             from .dp import DeviceDP
@@ -409,16 +410,30 @@ class DeviceLoop:
         elif self.hstat_allreduce is None:
             _lib.check(lib.fm_run(ctypes.byref(self.dims), ctypes.byref(self.state), int(n),
                                   int(bool(use_graph)), _lib.stream_ptr()), "fm_run")
+        elif use_graph and getattr(self.hstat_allreduce, "capturable", False):
+            # frequency shard: phase 0, the all-reduce (NCCL, graph-capturable)
+            # and phase 1 captured once into one CUDA graph, replayed per iteration
+            if self._shard_graph is None:
+                torch = self.torch
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g):
+                    self._shard_iteration(lib)
+                self._shard_graph = g
+            for _ in range(n):
+                self._shard_graph.replay()
         else:
             for _ in range(n):
-                _lib.check(lib.fm_iterate_phase(ctypes.byref(self.dims), ctypes.byref(self.state),
-                                                0, _lib.ptr(self.hstat), _lib.stream_ptr()),
-                           "fm_iterate_phase(0)")
-                self.hstat_allreduce(self.hstat)
-                _lib.check(lib.fm_iterate_phase(ctypes.byref(self.dims), ctypes.byref(self.state),
-                                                1, _lib.ptr(self.hstat), _lib.stream_ptr()),
-                           "fm_iterate_phase(1)")
+                self._shard_iteration(lib)
         self.iterations_done += n
+
+    def _shard_iteration(self, lib):
+        """One frequency-sharded iteration: phase 0 (this shard's H
+        statistics), the cross-shard sum, phase 1 (H update + the per-bin rest)."""
+        _lib.check(lib.fm_iterate_phase(ctypes.byref(self.dims), ctypes.byref(self.state), 0,
+                                        _lib.ptr(self.hstat), _lib.stream_ptr()), "fm_iterate_phase(0)")
+        self.hstat_allreduce(self.hstat)
+        _lib.check(lib.fm_iterate_phase(ctypes.byref(self.dims), ctypes.byref(self.state), 1,
+                                        _lib.ptr(self.hstat), _lib.stream_ptr()), "fm_iterate_phase(1)")
 
     def status_error(self, prefix=True):
         """The first numerical failure as the reference's exception, or None;
