@@ -24,6 +24,7 @@
 #include "fm_fullrank.cuh"
 #include "fm_fused.cuh"
 #include "fm_ipw.cuh"
+#include "fm_small.cuh"
 
 namespace fm {
 
@@ -161,6 +162,13 @@ inline bool use_fused(const fm_dims*) {
   return e && strcmp(e, "fused") == 0;
 }
 
+// M <= 4: register-accumulating gain / V kernels (fm_small.cuh) with
+// FM_SMALL=1 (measured slower than the staged ones at config 2; A/B runs)
+inline bool small_m_mode() {
+  const char* e = getenv("FM_SMALL");
+  return e && strcmp(e, "1") == 0;
+}
+
 // IP kernel: one warp per bin (k_ip_w, M <= 8) for many bins, the multi-warp
 // k_ip otherwise; FM_IP=w|cta forces one (A/B runs, tests)
 inline bool ip_warp_mode(const fm_dims* d) {
@@ -187,7 +195,8 @@ inline int pass_stages_override() {
 inline unsigned variant_key(const fm_dims* d) {
   return (unsigned)vacc_mode(d) | ((unsigned)(gseg_override() & 0xff) << 4) |
          ((unsigned)(pass_ctas_override() & 0xffff) << 12) | ((unsigned)pass_stages_override() << 28) |
-         ((unsigned)use_fused(d) << 31) | ((unsigned)ip_warp_mode(d) << 3);
+         ((unsigned)use_fused(d) << 31) | ((unsigned)ip_warp_mode(d) << 3) |
+         ((unsigned)small_m_mode() << 2);
 }
 
 inline Plan make_plan(const fm_dims* d) {
@@ -448,6 +457,15 @@ int Impl<R>::gain(const fm_dims* d, const fm_state* s, cudaStream_t st) {
   a.F = (int)d->F; a.T = (int)d->T; a.N = (int)d->N; a.TR = p.TR;
   dim3 grid((unsigned)p.nseg, (unsigned)d->F, (unsigned)d->B);
   FM_DISPATCH_M(d->M, {
+    if constexpr (MM <= 4) {  // register-accumulating, four bins per CTA (fm_small.cuh)
+      if (small_m_mode()) {
+        launch_pdl(k_gain_r<R, MM>, dim3((unsigned)p.nseg, (unsigned)((d->F + SMALL_BPB - 1) / SMALL_BPB),
+                                         (unsigned)d->B),
+                   dim3(SMALL_BS), 0, st, a);
+        FM_CHECK_LAUNCH("k_gain_r");
+        return FM_OK;
+      }
+    }
     launch_pdl(k_gain<R, MM>, grid, dim3(256), 0, st, a);
     FM_CHECK_LAUNCH("k_gain");
   });
@@ -491,6 +509,15 @@ int Impl<R>::vacc(const fm_dims* d, const fm_state* s, cudaStream_t st) {
         launch_pdl(k_vacc_blk<MM>, dim3((unsigned)p.vnseg, (unsigned)d->F, (unsigned)d->B),
                    dim3(VbCfg<MM>::BS), smb, st, ab);
         FM_CHECK_LAUNCH("k_vacc_blk");
+        return FM_OK;
+      }
+    }
+    if constexpr (MM <= 4) {  // register-accumulating, four bins per CTA (fm_small.cuh)
+      if (small_m_mode()) {
+        launch_pdl(k_vacc_r<R, MM>, dim3((unsigned)p.nseg, (unsigned)((d->F + SMALL_BPB - 1) / SMALL_BPB),
+                                         (unsigned)d->B),
+                   dim3(SMALL_BS), 0, st, a);
+        FM_CHECK_LAUNCH("k_vacc_r");
         return FM_OK;
       }
     }

@@ -1,5 +1,6 @@
 """k_ip_w (fm_ipw.cuh: one warp per bin, batched HPD Gauss-Jordan) -- the IP
-kernel of large batches (config 2) -- forced on small problems with FM_IP=w:
+kernel of large batches (config 2) -- forced on small problems with FM_IP=w
+(and the opt-in register-accumulating M <= 4 gain / V kernels, FM_SMALL=1):
 every channel count M = 1..8 in both precisions against the oracle, the
 rank-deficient T < M error with the reference's message and row, and an
 ill-conditioned V_fm whose fp32 pivots fail and are retried in fp64."""
@@ -68,3 +69,24 @@ def test_ipw_ill_conditioned_v_complex64():
     tr = ref["likelihood_trace"]
     assert np.all(np.isfinite(res.likelihood_trace))
     assert np.max(np.abs(res.likelihood_trace - tr) / np.abs(tr)) <= 1e-2
+
+
+@pytest.mark.parametrize("prec,tol", [("complex128", 1e-9), ("complex64", 1e-3)])
+@pytest.mark.parametrize("M", [1, 3, 4])
+def test_small_m_register_kernels_vs_oracle(M, prec, tol, monkeypatch):
+    """k_gain_r / k_vacc_r (fm_small.cuh, FM_SMALL=1): ragged bin count (not a
+    multiple of the 4 bins per CTA) and frames (not a multiple of 64)."""
+    monkeypatch.setenv("FM_SMALL", "1")
+    monkeypatch.setenv("FM_IP", "cta")
+    from paper_1903_03237_b200 import SeparatorConfig, run
+    F, T, N, K, it, seed = 10, 150, 3, 4, 3, 60 + M
+    X = make_mixture(F, T, M, N, K, seed)
+    if prec == "complex64":
+        X = X.astype(np.complex64)
+    init = baseline_init(F, T, M, N, K, seed)
+    ref = O.run_fastmnmf(X.astype(np.complex128), *init, n_iterations=it)
+    res = run(SeparatorConfig(n_sources=N, n_basis=K, n_iterations=it, precision=prec), X, init=init)
+    tr = ref["likelihood_trace"]
+    assert np.max(np.abs(res.likelihood_trace - tr) / np.abs(tr)) <= tol
+    assert rel(res.loop.g[0].cpu().numpy(), ref["g"]) <= tol
+    assert rel(res.images_NFTM, ref["images"]) <= tol
