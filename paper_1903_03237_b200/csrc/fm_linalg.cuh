@@ -201,8 +201,8 @@ __device__ bool warp_inv_hpd_f32(float2* A, int lane) {
   for (int k = 0; k < M; ++k) {
     const float2 p = A[k * M + k];
     if (!(p.x > 0.0f) || !isfinite(p.x)) return false;
-    const float inv = 1.0f / (p.x * p.x + p.y * p.y);
-    const float2 rp = make_float2(p.x * inv, -p.y * inv);
+    // HPD: the pivot is real; 1/Re p (no |p|^2, which halves the fp32 range)
+    const float2 rp = make_float2(1.0f / p.x, 0.0f);
     float2 nv[NE];
 #pragma unroll
     for (int r = 0; r < NE; ++r) {

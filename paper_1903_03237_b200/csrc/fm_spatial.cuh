@@ -505,18 +505,45 @@ __global__ void __launch_bounds__(IpCfg<M>::BS) k_ip(IpArgs<R> a) {
         }
         __syncwarp();
         ok = warp_inv_hpd_f32<M>(Vf, lane);
+        if (ok) {
 #pragma unroll
-        for (int r = 0; r < NE; ++r) {
-          const int e = lane + 32 * r;
-          if (e < M * M) tv[r] = Vf[e];
-        }
-        __syncwarp();
+          for (int r = 0; r < NE; ++r) {
+            const int e = lane + 32 * r;
+            if (e < M * M) tv[r] = Vf[e];
+          }
+          __syncwarp();
 #pragma unroll
-        for (int r = 0; r < NE; ++r) {
-          const int e = lane + 32 * r;
-          if (e < M * M) Vm[e] = make_double2((double)tv[r].x, (double)tv[r].y);
+          for (int r = 0; r < NE; ++r) {
+            const int e = lane + 32 * r;
+            if (e < M * M) Vm[e] = make_double2((double)tv[r].x, (double)tv[r].y);
+          }
+          __syncwarp();
+        } else {
+          // an fp32 pivot that is not positive (ill-conditioned V_m): rebuild
+          // V_m in fp64 from the partials and retry before the reference's
+          // error is raised
+          constexpr int P = M * (M + 1) / 2;
+          const C* vp = a.Vpart + ((size_t)b * F + f) * a.nseg * M * P + (size_t)m * P;
+          for (int e = lane; e < P; e += 32) {
+            double2 acc = make_double2(0.0, 0.0);
+            for (int q = 0; q < a.nseg; ++q) {
+              const C c = vp[(size_t)q * M * P + e];
+              acc.x += (double)c.x;
+              acc.y += (double)c.y;
+            }
+            int i = 0, r = e;
+            while (r >= M - i) {
+              r -= M - i;
+              ++i;
+            }
+            const int j = i + r;
+            const double2 d = make_double2(acc.x / (double)a.T, acc.y / (double)a.T);
+            Vm[i * M + j] = d;
+            if (i != j) Vm[j * M + i] = make_double2(d.x, -d.y);
+          }
+          __syncwarp();
+          ok = warp_inv_hpd<M>(Vm, lane);
         }
-        __syncwarp();
       } else {
         ok = warp_inv_hpd<M>(Vm, lane);
       }

@@ -48,13 +48,15 @@ def test_ipw_singular_prefix():
     assert "m=0)" in str(got.value)
 
 
-def test_ipw_ill_conditioned_v_complex64():
+@pytest.mark.parametrize("ip", ["w", "cta"])
+def test_ipw_ill_conditioned_v_complex64(ip, monkeypatch):
     """Two nearly collinear channels make V_fm ill-conditioned (condition
     number ~1e5, still representable in the fp32-accumulated V): the fp32
     Gauss-Jordan loses most digits of a pivot; the kernel must fall back to
     fp64 and finish like the oracle instead of raising. (Collinearity beyond
     fp32 resolution makes the complex64 V itself indefinite -- a limit of the
-    precision mode, not of the solver.)"""
+    precision mode, not of the solver.) Both IP kernels (k_ip_w, k_ip)."""
+    monkeypatch.setenv("FM_IP", ip)
     from paper_1903_03237_b200 import SeparatorConfig, run
     F, T, M, N, K, it = 6, 200, 4, 2, 3, 2
     rng = np.random.default_rng(7)
