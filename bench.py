@@ -31,7 +31,6 @@ import time
 import numpy as np
 
 REPO = os.path.dirname(os.path.abspath(__file__))
-os.environ.setdefault("NCCL_DEBUG", "WARN")  # keep stdout to the one JSON line
 sys.path.insert(0, REPO)
 
 CONFIGS = {
