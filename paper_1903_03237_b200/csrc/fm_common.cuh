@@ -5,6 +5,8 @@
 #include <float.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 namespace fm {
 
 constexpr int NMAX = 8;  // sources per mixture supported by the fused kernels
@@ -74,6 +76,22 @@ __device__ __forceinline__ double2 crcp(double2 p) {
   const double inv = drcp(p.x * p.x + p.y * p.y);
   return make_double2(p.x * inv, -p.y * inv);
 }
+// fp32 complex arithmetic (the complex64 IP path at M <= 8, fm_spatial.cuh)
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
+  return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ float cabs1(float2 a) { return fabsf(a.x) + fabsf(a.y); }
+__device__ __forceinline__ float2 crcp(float2 p) {
+  const float inv = 1.0f / (p.x * p.x + p.y * p.y);
+  return make_float2(p.x * inv, -p.y * inv);
+}
+__device__ __forceinline__ float drsqrt(float x) { return rsqrtf(x); }
+__device__ __forceinline__ float2 to_c2(double2 a, float2) { return make_float2((float)a.x, (float)a.y); }
+__device__ __forceinline__ double2 to_c2(double2 a, double2) { return a; }
+__device__ __forceinline__ float2 to_c2(float2 a, float2) { return a; }
+__device__ __forceinline__ double2 to_c2(float2 a, double2) { return make_double2(a.x, a.y); }
 __device__ __forceinline__ double2 to_d2(float2 a) { return make_double2(a.x, a.y); }
 __device__ __forceinline__ double2 to_d2(double2 a) { return a; }
 

@@ -91,6 +91,21 @@ void set_error(const char* fmt, ...);
   else if ((ITrt) <= 4) { constexpr int IT = 4; __VA_ARGS__; }                         \
   else { constexpr int IT = 8; __VA_ARGS__; }
 
+// The device's default stream-ordered pool returns freed blocks to the OS at
+// every synchronisation (release threshold 0), so a per-call
+// cudaMallocAsync / cudaFreeAsync re-maps memory each time; keep it mapped.
+inline void keep_pool_mapped() {
+  static thread_local int done_dev = -1;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev == done_dev) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  done_dev = dev;
+}
+
 inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 // Launch with programmatic stream serialisation (PDL): the kernel may begin
@@ -1161,14 +1176,30 @@ int Impl<R>::wiener(int64_t N, int64_t F, int64_t T, int64_t M, const void* lam,
                     const void* g, const void* X, void* out, uint64_t* status, cudaStream_t st) {
   if (N > 8) { set_error("N=%lld outside 1..8", (long long)N); return FM_EINVAL; }
   if (F == 0) return FM_OK;
+  // Q^-1 per bin (k_qinv), then one frame per thread (k_wiener_t); the
+  // scratch comes from the device's stream-ordered pool (kept mapped: see
+  // keep_pool_mapped)
+  keep_pool_mapped();
+  unsigned char* scratch = nullptr;
+  const size_t qbytes = align256(sizeof(C) * (size_t)F * M * M);
+  FM_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&scratch), qbytes + sizeof(int) * (size_t)F, st));
+  C* Qi = reinterpret_cast<C*>(scratch);
+  int* bad = reinterpret_cast<int*>(scratch + qbytes);
+  int rc = FM_OK;
   FM_DISPATCH_M(M, {
-    k_wiener<R, MM><<<(unsigned)F, 256, 0, st>>>(
-        reinterpret_cast<const R*>(lam), reinterpret_cast<const C*>(Q),
+    k_qinv<R, MM><<<(unsigned)((F + 3) / 4), 128, 0, st>>>(
+        reinterpret_cast<const C*>(Q), (int)F, Qi, bad, reinterpret_cast<unsigned long long*>(status));
+    k_wiener_t<R, MM><<<dim3((unsigned)((T + 127) / 128), (unsigned)F), 128, 0, st>>>(
+        reinterpret_cast<const R*>(lam), reinterpret_cast<const C*>(Q), Qi, bad,
         reinterpret_cast<const R*>(g), reinterpret_cast<const C*>(X), (int)N, (int)F, (int)T,
-        reinterpret_cast<C*>(out), reinterpret_cast<unsigned long long*>(status));
-    FM_CHECK_LAUNCH("k_wiener");
+        reinterpret_cast<C*>(out));
   });
-  return FM_OK;
+  if (cudaGetLastError() != cudaSuccess) {
+    set_error("k_qinv / k_wiener_t launch failed");
+    rc = FM_ECUDA;
+  }
+  FM_CUDA(cudaFreeAsync(scratch, st));
+  return rc;
 }
 
 // Small persistent device + pinned host scratch for the synchronous prologue

@@ -235,46 +235,47 @@ __device__ bool warp_inv_hpd_f32(float2* A, int lane) {
 // the augmented [Q | I] (M x 2M, row-major) by one warp; on success the
 // right half holds Q^-1 and *logabs = sum_k log|pivot_k| = log|det Q|
 // (the LU pivots; slogdet, separate.py:238).
-template <int M>
-__device__ bool warp_inv_pivot(double2* A, int lane, double* logabs) {
+template <int M, typename C2>
+__device__ bool warp_inv_pivot(C2* A, int lane, double* logabs) {
+  using Rc = decltype(C2().x);
   constexpr int W2 = 2 * M;
   constexpr int NE = (M * W2 + 31) / 32;
   double la = 0.0;
   for (int k = 0; k < M; ++k) {
-    double v = -1.0;
+    Rc v = Rc(-1);
     int idx = lane;
     if (lane >= k && lane < M) v = cabs1(A[lane * W2 + k]);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
-      const double ov = __shfl_xor_sync(FM_FULL, v, o);
+      const Rc ov = __shfl_xor_sync(FM_FULL, v, o);
       const int oi = __shfl_xor_sync(FM_FULL, idx, o);
       if (ov > v || (ov == v && oi < idx)) {
         v = ov;
         idx = oi;
       }
     }
-    if (!(v > 0.0)) {
+    if (!(v > Rc(0))) {
       *logabs = -INFINITY;
       return false;
     }
     if (idx != k) {
       for (int c = lane; c < W2; c += 32) {
-        const double2 t = A[k * W2 + c];
+        const C2 t = A[k * W2 + c];
         A[k * W2 + c] = A[idx * W2 + c];
         A[idx * W2 + c] = t;
       }
     }
     __syncwarp();
-    const double2 piv = A[k * W2 + k];
-    la += 0.5 * log(piv.x * piv.x + piv.y * piv.y);
-    const double2 rp = crcp(piv);
-    double2 nv[NE];
+    const C2 piv = A[k * W2 + k];
+    la += 0.5 * log((double)piv.x * piv.x + (double)piv.y * piv.y);
+    const C2 rp = crcp(piv);
+    C2 nv[NE];
 #pragma unroll
     for (int r = 0; r < NE; ++r) {
       const int e = lane + 32 * r;
       if (e < M * W2) {
         const int i = e / W2, j = e % W2;
-        const double2 akj = cmul(A[k * W2 + j], rp);
+        const C2 akj = cmul(A[k * W2 + j], rp);
         nv[r] = (i == k) ? akj : csub(A[e], cmul(A[i * W2 + k], akj));
       }
     }

@@ -311,6 +311,109 @@ __global__ void __launch_bounds__(256) k_wiener(const R* __restrict__ lam, const
   }
 }
 
+// separate.wiener_fast in two launches (the single-CTA-per-bin k_wiener
+// above hoists Q and Q^-1 into 254 registers: 12% occupancy, c1 176 us).
+// k_qinv: one warp per bin inverts Q_f (LU against I, numpy.linalg.inv,
+// separate.py:122) into Qi; a singular bin sets its flag and the status.
+template <typename R, int M>
+__global__ void __launch_bounds__(128) k_qinv(const cplx<R>* __restrict__ Q, int F, cplx<R>* __restrict__ Qi,
+                                              int* __restrict__ bad, unsigned long long* status) {
+  using C = cplx<R>;
+  constexpr int LD = 2 * M;
+  __shared__ double2 As[4][M * LD];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int f = blockIdx.x * 4 + warp;
+  if (f >= F) return;
+  double2* A = As[warp];
+  const C* Qf = Q + (size_t)f * M * M;
+  for (int e = lane; e < M * M; e += 32) {
+    const int r = e / M, c = e % M;
+    A[r * LD + c] = to_d2(Qf[e]);
+    A[r * LD + M + c] = make_double2(r == c ? 1.0 : 0.0, 0.0);
+  }
+  __syncwarp();
+  const bool ok = warp_lu<M>(A, LD, 2 * M, lane, nullptr);
+  if (ok) warp_backsubM<M>(A, LD, lane);
+  __syncwarp();
+  if (lane == 0) {
+    bad[f] = ok ? 0 : 1;
+    if (!ok) report_status(status, 0, 0, f, 3);
+  }
+  for (int e = lane; e < M * M; e += 32) {
+    const double2 v = A[(e / M) * LD + M + e % M];
+    Qi[(size_t)f * M * M + e] = cmake<C>(v.x, v.y);
+  }
+}
+
+// k_wiener_t: one frame per thread, grid (ceil(T/128), F), block 128; Q, Q^-1
+// and the gains of the bin in shared memory; image_n = Q^-1 (gain_n . Q x),
+// gain_n = lam_n g_n / sum_n' lam_n' g_n' (1/N where the sum is 0).
+template <typename R, int M>
+__global__ void __launch_bounds__(128, 4) k_wiener_t(const R* __restrict__ lam, const cplx<R>* __restrict__ Q,
+                                                     const cplx<R>* __restrict__ Qi, const int* __restrict__ bad,
+                                                     const R* __restrict__ g, const cplx<R>* __restrict__ X,
+                                                     int N, int F, int T, cplx<R>* __restrict__ out) {
+  using C = cplx<R>;
+  __shared__ __align__(16) C Qs[M * M];
+  __shared__ __align__(16) C Qis[M * M];
+  __shared__ R gs[8 * M];
+  const int f = blockIdx.y, tid = threadIdx.x;
+  if (bad[f]) return;
+  for (int e = tid; e < M * M; e += 128) {
+    Qs[e] = Q[(size_t)f * M * M + e];
+    Qis[e] = Qi[(size_t)f * M * M + e];
+  }
+  for (int e = tid; e < N * M; e += 128) gs[e] = g[((size_t)(e / M) * F + f) * M + e % M];
+  __syncthreads();
+  const int t = blockIdx.x * 128 + tid;
+  if (t >= T) return;
+  const size_t FT = (size_t)F * T;
+  C xv[M];
+  CRowIO<R, M>::load(X + ((size_t)f * T + t) * M, xv);
+  C qx[M];
+#pragma unroll
+  for (int r = 0; r < M; ++r) {
+    R sr = 0, si = 0;
+#pragma unroll
+    for (int j = 0; j < M; ++j) {
+      const C q = Qs[r * M + j];
+      sr += q.x * xv[j].x - q.y * xv[j].y;
+      si += q.x * xv[j].y + q.y * xv[j].x;
+    }
+    qx[r] = cmake<C>(sr, si);
+  }
+  R den[M];
+#pragma unroll
+  for (int m = 0; m < M; ++m) den[m] = 0;
+  for (int n = 0; n < N; ++n) {
+    const R l = lam[n * FT + (size_t)f * T + t];
+#pragma unroll
+    for (int m = 0; m < M; ++m) den[m] += l * gs[n * M + m];
+  }
+  for (int n = 0; n < N; ++n) {
+    const R l = lam[n * FT + (size_t)f * T + t];
+    C z[M];
+#pragma unroll
+    for (int m = 0; m < M; ++m) {
+      const R gain = den[m] > R(0) ? (l * gs[n * M + m]) / den[m] : R(1) / R(N);
+      z[m] = cmake<C>(gain * qx[m].x, gain * qx[m].y);
+    }
+    C o[M];
+#pragma unroll
+    for (int r = 0; r < M; ++r) {
+      R sr = 0, si = 0;
+#pragma unroll
+      for (int j = 0; j < M; ++j) {
+        const C q = Qis[r * M + j];
+        sr += q.x * z[j].x - q.y * z[j].y;
+        si += q.x * z[j].y + q.y * z[j].x;
+      }
+      o[r] = cmake<C>(sr, si);
+    }
+    CRowIO<R, M>::store(out + ((size_t)n * FT + (size_t)f * T + t) * M, o);
+  }
+}
+
 // sum |X|^2 and max |X|^2 per mixture: partials (B, nblk) of fp64.
 template <typename R>
 __global__ void __launch_bounds__(256) k_obs_stats(const cplx<R>* __restrict__ X, long long n_per_b,

@@ -417,14 +417,21 @@ __global__ void __launch_bounds__(IpCfg<M>::BS) k_ip(IpArgs<R> a) {
   pdl_entry();
   using C = cplx<R>;
   using L = IpSmem<R, M>;
+  // complex64 at M <= 8: the whole IP (Q inverse, V inverses, row updates,
+  // normalisation) in fp32 -- the reference is fp64, but the fp32-accumulated
+  // V already bounds the accuracy there (parity: profiles/parity_r2.json);
+  // the log-determinant still accumulates in fp64. Otherwise fp64.
+  constexpr bool F32 = sizeof(R) == 4 && M <= 8;
+  using C2 = typename std::conditional<F32, float2, double2>::type;
+  using Rc = typename std::conditional<F32, float, double>::type;
   constexpr int NW = IpCfg<M>::NW, BS = IpCfg<M>::BS;
   extern __shared__ __align__(16) unsigned char sm[];
   double2* Vd = reinterpret_cast<double2*>(sm + L::o_Vd);
-  double2* Qd = reinterpret_cast<double2*>(sm + L::o_Qd);
-  double2* Ai = reinterpret_cast<double2*>(sm + L::o_Ai);
-  double2* ub = reinterpret_cast<double2*>(sm + L::o_vec);
-  double2* qb = ub + M;
-  double2* sk = qb + M;
+  C2* Qd = reinterpret_cast<C2*>(sm + L::o_Qd);
+  C2* Ai = reinterpret_cast<C2*>(sm + L::o_Ai);
+  C2* ub = reinterpret_cast<C2*>(sm + L::o_vec);
+  C2* qb = ub + M;
+  C2* sk = qb + M;
   R* gs = reinterpret_cast<R*>(sm + L::o_gs);
   R* cs = reinterpret_cast<R*>(sm + L::o_cs);
   double* rown = reinterpret_cast<double*>(sm + L::o_rown);
@@ -463,7 +470,7 @@ __global__ void __launch_bounds__(IpCfg<M>::BS) k_ip(IpArgs<R> a) {
       if (i != j) Vd[((size_t)m * M + j) * M + i] = make_double2(d.x, -d.y);
     }
   }
-  for (int e = tid; e < M * M; e += BS) Qd[e] = to_d2(Qg[e]);
+  for (int e = tid; e < M * M; e += BS) Qd[e] = to_c2(Qg[e], C2());
   for (int e = tid; e < N * M; e += BS)
     gs[e] = a.gnew[(size_t)b * N * F * M + (size_t)(e / M) * F * M + (size_t)f * M + (e % M)];
   if (tid < NMAX) cs[tid] = R(1);
@@ -475,7 +482,7 @@ __global__ void __launch_bounds__(IpCfg<M>::BS) k_ip(IpArgs<R> a) {
       // [Q | I] -> Q^-1 and log|det Q|
       for (int e = lane; e < M * 2 * M; e += 32) {
         const int r = e / (2 * M), c = e % (2 * M);
-        Ai[e] = c < M ? Qd[r * M + c] : make_double2(c - M == r ? 1.0 : 0.0, 0.0);
+        Ai[e] = c < M ? Qd[r * M + c] : to_c2(make_double2(c - M == r ? 1.0 : 0.0, 0.0), C2());
       }
       __syncwarp();
       double la = 0.0;
@@ -504,21 +511,8 @@ __global__ void __launch_bounds__(IpCfg<M>::BS) k_ip(IpArgs<R> a) {
           if (e < M * M) Vf[e] = tv[r];
         }
         __syncwarp();
-        ok = warp_inv_hpd_f32<M>(Vf, lane);
-        if (ok) {
-#pragma unroll
-          for (int r = 0; r < NE; ++r) {
-            const int e = lane + 32 * r;
-            if (e < M * M) tv[r] = Vf[e];
-          }
-          __syncwarp();
-#pragma unroll
-          for (int r = 0; r < NE; ++r) {
-            const int e = lane + 32 * r;
-            if (e < M * M) Vm[e] = make_double2((double)tv[r].x, (double)tv[r].y);
-          }
-          __syncwarp();
-        } else {
+        ok = warp_inv_hpd_f32<M>(Vf, lane);  // stays fp32 in place (the F32 row updates read it)
+        if (!ok) {
           // an fp32 pivot that is not positive (ill-conditioned V_m): rebuild
           // V_m in fp64 from the partials and retry before the reference's
           // error is raised
@@ -543,6 +537,20 @@ __global__ void __launch_bounds__(IpCfg<M>::BS) k_ip(IpArgs<R> a) {
           }
           __syncwarp();
           ok = warp_inv_hpd<M>(Vm, lane);
+          if (ok) {  // fp64 inverse -> the fp32 layout the row updates read
+#pragma unroll
+            for (int r = 0; r < NE; ++r) {
+              const int e = lane + 32 * r;
+              if (e < M * M) tv[r] = make_float2((float)Vm[e].x, (float)Vm[e].y);
+            }
+            __syncwarp();
+#pragma unroll
+            for (int r = 0; r < NE; ++r) {
+              const int e = lane + 32 * r;
+              if (e < M * M) Vf[e] = tv[r];
+            }
+          }
+          __syncwarp();
         }
       } else {
         ok = warp_inv_hpd<M>(Vm, lane);
@@ -564,11 +572,11 @@ __global__ void __launch_bounds__(IpCfg<M>::BS) k_ip(IpArgs<R> a) {
             bad_m = m;
             break;
           }
-          const double2* Vi = Vd + (size_t)m * M * M;
+          const C2* Vi = reinterpret_cast<const C2*>(Vd + (size_t)m * M * M);
           if (lane < M) ub[lane] = Ai[lane * 2 * M + M + m];  // u = Q^-1 e_m
           __syncwarp();
           // q = V_m^-1 u: GL lanes per row, strided partial dots + xor reduce
-          double2 q = make_double2(0.0, 0.0);
+          C2 q = to_c2(make_double2(0.0, 0.0), C2());
           if (rv) {
 #pragma unroll
             for (int j = sub; j < M; j += GL) q = cadd(q, cmul(Vi[ri * M + j], ub[j]));
@@ -578,26 +586,28 @@ __global__ void __launch_bounds__(IpCfg<M>::BS) k_ip(IpArgs<R> a) {
             q.x += __shfl_xor_sync(FM_FULL, q.x, o);
             q.y += __shfl_xor_sync(FM_FULL, q.y, o);
           }
-          double part = 0.0;
+          Rc part = Rc(0);
           if (rv && sub == 0) {
-            const double2 u = ub[ri];
+            const C2 u = ub[ri];
             part = q.x * u.x + q.y * u.y;  // Re(conj(q_i) u_i)
           }
-          const double nrm = warp_sum(part);  // = q^H V q  (spatial.py:193)
-          if (!(nrm > 0.0) || !isfinite(nrm)) {
+          const Rc nrm = warp_sum(part);  // = q^H V q  (spatial.py:193)
+          if (!(nrm > Rc(0)) || !isfinite(nrm)) {
             code = 1;
             bad_m = m;
             break;
           }
-          const double isn = drsqrt(nrm);  // 1 / sqrt(norm)
+          const Rc isn = drsqrt(nrm);  // 1 / sqrt(norm)
           if (rv && sub == 0) {  // new row r = conj(q / sqrt(norm))  (spatial.py:199)
-            const double2 r = make_double2(q.x * isn, -(q.y * isn));
+            C2 r = q;
+            r.x = q.x * isn;
+            r.y = -(q.y * isn);
             qb[ri] = r;
             Qd[m * M + ri] = r;
           }
           __syncwarp();
           // s = (r Q^-1 - e_m^T) / sqrt(norm), column ri per lane group
-          double2 sv = make_double2(0.0, 0.0);
+          C2 sv = to_c2(make_double2(0.0, 0.0), C2());
           if (rv) {
 #pragma unroll
             for (int j = sub; j < M; j += GL) sv = cadd(sv, cmul(qb[j], Ai[j * 2 * M + M + ri]));
@@ -608,16 +618,18 @@ __global__ void __launch_bounds__(IpCfg<M>::BS) k_ip(IpArgs<R> a) {
             sv.y += __shfl_xor_sync(FM_FULL, sv.y, o);
           }
           if (rv && sub == 0) {
-            if (ri == m) sv.x -= 1.0;
-            sk[ri] = make_double2(sv.x * isn, sv.y * isn);
+            if (ri == m) sv.x -= Rc(1);
+            sv.x *= isn;
+            sv.y *= isn;
+            sk[ri] = sv;
           }
           __syncwarp();
           for (int e = lane; e < M * M; e += 32) {  // Q^-1 -= u s / sqrt(norm)
             const int i = e / M, k = e % M;
-            double2* d = Ai + i * 2 * M + M + k;
+            C2* d = Ai + i * 2 * M + M + k;
             *d = csub(*d, cmul(ub[i], sk[k]));
           }
-          nprod *= nrm;  // log|det Q| += log sqrt(norm) (determinant lemma)
+          nprod *= (double)nrm;  // log|det Q| += log sqrt(norm) (determinant lemma)
           if (nprod > 1e150 || nprod < 1e-150) {
             ldet += 0.5 * log(nprod);
             nprod = 1.0;
@@ -642,15 +654,18 @@ __global__ void __launch_bounds__(IpCfg<M>::BS) k_ip(IpArgs<R> a) {
       double s = 0.0;
 #pragma unroll
       for (int j = 0; j < M; ++j) {
-        const double2 q = Qd[tid * M + j];
-        s += q.x * q.x + q.y * q.y;
+        const C2 q = Qd[tid * M + j];
+        s += (double)q.x * q.x + (double)q.y * q.y;
       }
       rown[tid] = sqrt(s);
     }
     __syncthreads();
     for (int e = tid; e < M * M; e += BS) {
-      const double r = rown[e / M];
-      Qd[e] = make_double2(Qd[e].x / r, Qd[e].y / r);
+      const Rc r = (Rc)rown[e / M];
+      C2 v = Qd[e];
+      v.x = v.x / r;
+      v.y = v.y / r;
+      Qd[e] = v;
     }
     for (int e = tid; e < N * M; e += BS) {
       const double r = rown[e % M];
