@@ -67,7 +67,9 @@ template <typename R, int M> struct GaCfg {
   // when M % 4 == 0 and M >= 8, else 1 (measured: c3 M = 16 660 -> 490 us,
   // c1 M = 8 unchanged, c2 M = 4 917 -> 956 us with 4)
   static constexpr int MQ = (M % 4 == 0 && M >= 8) ? 4 : 1;
-  static constexpr int RED = 512 * MQ;  // >= slices x N x M x 2 partial sums
+  // source pairs per accumulating thread (fp32, MQ = 4, even N): 2x the slices
+  static constexpr bool PAIRS = sizeof(R) == 4 && MQ == 4;
+  static constexpr int RED = (PAIRS ? 1024 : 512) * MQ;  // >= slices x N x M x 2 partial sums
   static constexpr bool ALIAS = RED <= 2 * TB * M;  // reduction reuses the staged rows
 };
 
@@ -107,14 +109,20 @@ __global__ void __launch_bounds__(256) k_gain(GainArgs<R> a) {
     RowIO<R, M>::load(xtb + (size_t)tc * M, xp);
   };
   if (tid < TB) fetch(ta);
-  // accumulate mapping: thread = (source n, MQ consecutive channels, slice)
+  // accumulate mapping: thread = (NP sources from n1, MQ consecutive
+  // channels, slice); with MQ = 4 and N even a thread takes a source pair, so
+  // one pair of 16-B loads of x~/y^2 and 1/y feeds 16 FMAs (c3: the loop was
+  // shared-memory bound, 90% of the pipe)
   constexpr int Q = M / MQ;
-  const int E = N * Q, S = 256 / E;
+  // (only when enough items remain that the slice reduction stays short:
+  // c3 k_gain 489 -> 418 us; c1, 4 pair items, 18.4 -> 20.5 us, so not there)
+  const int NP = (Cf::PAIRS && (N % 2) == 0 && (N / 2) * Q >= 8) ? 2 : 1;
+  const int E = (N / NP) * Q, S = 256 / E;
   const int e1 = tid % E, s1 = tid / E;
-  const int n1 = e1 / Q, m0 = (e1 % Q) * MQ;
-  R num[MQ], den[MQ];
+  const int n1 = (e1 / Q) * NP, m0 = (e1 % Q) * MQ;
+  R num[2][MQ], den[2][MQ];
 #pragma unroll
-  for (int k = 0; k < MQ; ++k) num[k] = den[k] = R(0);
+  for (int k = 0; k < MQ; ++k) num[0][k] = den[0][k] = num[1][k] = den[1][k] = R(0);
   __syncthreads();
   for (int c0 = ta; c0 < tb; c0 += TB) {
     if (tid < TB) {
@@ -142,20 +150,41 @@ __global__ void __launch_bounds__(256) k_gain(GainArgs<R> a) {
     }
     __syncthreads();
     if (s1 < S) {
-      for (int tl = s1; tl < TB; tl += S) {
-        const R lv = lams[n1 * (TB + 1) + tl];
-        R xv[MQ], iv[MQ];
-        if constexpr (MQ == 4) {
-          lds4(xrs + tl * M + m0, xv);
-          lds4(iys + tl * M + m0, iv);
-        } else {
-          xv[0] = xrs[tl * M + m0];
-          iv[0] = iys[tl * M + m0];
-        }
+      if (NP == 2) {
+        for (int tl = s1; tl < TB; tl += S) {
+          const R lv0 = lams[n1 * (TB + 1) + tl], lv1 = lams[(n1 + 1) * (TB + 1) + tl];
+          R xv[MQ], iv[MQ];
+          if constexpr (MQ == 4) {
+            lds4(xrs + tl * M + m0, xv);
+            lds4(iys + tl * M + m0, iv);
+          } else {
+            xv[0] = xrs[tl * M + m0];
+            iv[0] = iys[tl * M + m0];
+          }
 #pragma unroll
-        for (int k = 0; k < MQ; ++k) {
-          num[k] += lv * xv[k];
-          den[k] += lv * iv[k];
+          for (int k = 0; k < MQ; ++k) {
+            num[0][k] += lv0 * xv[k];
+            den[0][k] += lv0 * iv[k];
+            num[1][k] += lv1 * xv[k];
+            den[1][k] += lv1 * iv[k];
+          }
+        }
+      } else {
+        for (int tl = s1; tl < TB; tl += S) {
+          const R lv = lams[n1 * (TB + 1) + tl];
+          R xv[MQ], iv[MQ];
+          if constexpr (MQ == 4) {
+            lds4(xrs + tl * M + m0, xv);
+            lds4(iys + tl * M + m0, iv);
+          } else {
+            xv[0] = xrs[tl * M + m0];
+            iv[0] = iys[tl * M + m0];
+          }
+#pragma unroll
+          for (int k = 0; k < MQ; ++k) {
+            num[0][k] += lv * xv[k];
+            den[0][k] += lv * iv[k];
+          }
         }
       }
     }
@@ -163,11 +192,13 @@ __global__ void __launch_bounds__(256) k_gain(GainArgs<R> a) {
   }
   // fixed-order slice sums: partial (slice, n, m) pairs, then one thread per (n, m)
   if (s1 < S) {
+    for (int pp = 0; pp < NP; ++pp) {
 #pragma unroll
-    for (int k = 0; k < MQ; ++k) {
-      const int en = n1 * M + m0 + k;
-      redb[(s1 * N * M + en) * 2] = num[k];
-      redb[(s1 * N * M + en) * 2 + 1] = den[k];
+      for (int k = 0; k < MQ; ++k) {
+        const int en = (n1 + pp) * M + m0 + k;
+        redb[(s1 * N * M + en) * 2] = num[pp][k];
+        redb[(s1 * N * M + en) * 2 + 1] = den[pp][k];
+      }
     }
   }
   __syncthreads();
