@@ -220,7 +220,10 @@ inline Plan make_plan(const fm_dims* d) {
   const long long B = d->B, F = d->F, T = d->T, N = d->N, M = d->M;
   const long long target = 2 * 148;  // >= 2 CTAs per SM
   // largest tile that still gives ~2 CTAs per SM
-  p.ntile = (int)((T + 255) / 256);
+  {  // k_back frame tiles per bin (data-term partials per bin)
+    const long long fr = 256 * back_ppt(M, T);
+    p.ntile = (int)((T + fr - 1) / fr);
+  }
   p.FT = 32;
   while (p.FT > 8 && ((F + p.FT - 1) / p.FT) * B * N < target) p.FT /= 2;
   p.TT = 64;
@@ -614,9 +617,15 @@ int Impl<R>::back(const fm_dims* d, const fm_state* s, int tail_only, int record
   a.iter = a.counter + 1;
   a.B = (int)d->B; a.F = (int)d->F; a.T = (int)d->T; a.N = (int)d->N;
   a.record = record && s->trace != nullptr;
-  dim3 grid((unsigned)((d->T + 255) / 256), (unsigned)d->F, (unsigned)d->B);
   FM_DISPATCH_M(d->M, {
-    launch_pdl(k_back<R, MM>, grid, dim3(256), 0, st, a);
+    const int ppt = back_ppt(d->M, d->T);
+    const dim3 grid((unsigned)((d->T + 256 * ppt - 1) / (256 * ppt)), (unsigned)d->F, (unsigned)d->B);
+    if constexpr (MM <= 4) {
+      if (ppt == 2) launch_pdl(k_back<R, MM, 2>, grid, dim3(256), 0, st, a);
+      else launch_pdl(k_back<R, MM, 1>, grid, dim3(256), 0, st, a);
+    } else {
+      launch_pdl(k_back<R, MM, 1>, grid, dim3(256), 0, st, a);
+    }
     FM_CHECK_LAUNCH("k_back");
   });
   return FM_OK;

@@ -763,7 +763,13 @@ template <typename R> struct BackArgs {
 // ll_part is (B, F, tiles) and reduced in fixed order by the last tile.
 // 3 CTAs per SM (<= 85 registers) up to M = 8; 2 above, where the 16-channel
 // rows would otherwise spill
-template <typename R, int M>
+// points (frames) per thread of k_back: 2 for M <= 4 and long recordings,
+// whose CTAs otherwise spend half their life at the staging barrier with too
+// few bytes in flight (c2: 52% barrier stalls, 44% of DRAM bandwidth; k_back
+// 1.57 -> 1.34 ms); 1 otherwise (c0, T = 128: 8.2 -> 9.7 us with 2)
+inline int back_ppt(long long M, long long T) { return (M <= 4 && T >= 512) ? 2 : 1; }
+
+template <typename R, int M, int PPT>
 __global__ void __launch_bounds__(256, (M > 8 ? 2 : 3)) k_back(BackArgs<R> a) {
   pdl_entry();
   using C = cplx<R>;
@@ -775,31 +781,36 @@ __global__ void __launch_bounds__(256, (M > 8 ? 2 : 3)) k_back(BackArgs<R> a) {
   const int ntile = gridDim.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int N = a.N, T = a.T, F = a.F;
-  const int t = tile * 256 + tid;
   const size_t FT = (size_t)F * T;
   for (int e = tid; e < M * M; e += 256) Qr[e] = a.Q[((size_t)b * F + f) * M * M + e];
   for (int e = tid; e < N * M; e += 256)
     gs[e] = a.g[(size_t)b * N * F * M + (size_t)(e / M) * F * M + (size_t)f * M + (e % M)];
   if (tid < NMAX) cs[tid] = a.cs ? a.cs[((size_t)b * F + f) * NMAX + tid] : R(1);
   double ll = 0.0;
-  C xv[M];
-  R l[NMAX];
-  const bool tv = t < T;
-  if (tv) {
-    CRowIO<R, M>::load(a.X + (((size_t)b * F + f) * T + t) * M, xv);
-    const R* lb = a.lam + (size_t)b * N * FT + (size_t)f * T + t;
+  C xv[PPT][M];
+  R l[PPT][NMAX];
 #pragma unroll
-    for (int n = 0; n < NMAX; ++n) {
-      l[n] = R(0);
-      if (n >= N) break;
-      l[n] = lb[(size_t)n * FT];
+  for (int u = 0; u < PPT; ++u) {  // every point's loads issued before the barrier
+    const int t = tile * 256 * PPT + u * 256 + tid;
+    if (t < T) {
+      CRowIO<R, M>::load(a.X + (((size_t)b * F + f) * T + t) * M, xv[u]);
+      const R* lb = a.lam + (size_t)b * N * FT + (size_t)f * T + t;
+#pragma unroll
+      for (int n = 0; n < NMAX; ++n) {
+        l[u][n] = R(0);
+        if (n >= N) break;
+        l[u][n] = lb[(size_t)n * FT];
+      }
     }
   }
   __syncthreads();
-  if (tv) {
-    const R fl = a.floorp[b];
+  const R fl = a.floorp[b];
 #pragma unroll
-    for (int n = 0; n < NMAX; ++n) l[n] *= cs[n];
+  for (int u = 0; u < PPT; ++u) {
+    const int t = tile * 256 * PPT + u * 256 + tid;
+    if (t >= T) continue;
+#pragma unroll
+    for (int n = 0; n < NMAX; ++n) l[u][n] *= cs[n];
     R xtv[M];
 #pragma unroll
     for (int i = 0; i < M; ++i) {
@@ -807,18 +818,18 @@ __global__ void __launch_bounds__(256, (M > 8 ? 2 : 3)) k_back(BackArgs<R> a) {
 #pragma unroll
       for (int j = 0; j < M; ++j) {
         const C q = Qr[i * M + j];
-        s = fma2(cmake<C>(q.x, q.x), xv[j], s);
-        s = fma2(cmake<C>(-q.y, q.y), cmake<C>(xv[j].y, xv[j].x), s);
+        s = fma2(cmake<C>(q.x, q.x), xv[u][j], s);
+        s = fma2(cmake<C>(-q.y, q.y), cmake<C>(xv[u][j].y, xv[u][j].x), s);
       }
       xtv[i] = s.x * s.x + s.y * s.y;
     }
     RowIO<R, M>::store(a.xt + (((size_t)b * F + f) * T + t) * M, xtv);
     R iy[M], y[M];
-    model_power<R, M>(l, gs, N, fl, iy, y);
+    model_power<R, M>(l[u], gs, N, fl, iy, y);
     R llt = 0;
 #pragma unroll
     for (int m = 0; m < M; ++m) llt += -xtv[m] * iy[m] - log_fast(y[m]);
-    ll = (double)llt;
+    ll += (double)llt;
     phi_point<R, M>(xtv, iy, gs, N, a.phi + (size_t)b * 2 * N * FT, FT, (size_t)f * T + t);
   }
   ll = warp_sum(ll);
