@@ -6,7 +6,7 @@ CSRC := paper_1903_03237_b200/csrc
 OBJ := build/obj
 LIB := paper_1903_03237_b200/libfastmnmf.so
 HDRS := $(wildcard $(CSRC)/*.cuh) include/fastmnmf.h
-SRCS := $(CSRC)/fm_api.cu $(CSRC)/fm_f32.cu $(CSRC)/fm_f64.cu $(CSRC)/fm_fused_f32.cu $(CSRC)/fm_fused_f64.cu
+SRCS := $(CSRC)/fm_api.cu $(CSRC)/fm_f32.cu $(CSRC)/fm_f64.cu $(CSRC)/fm_fused_f32.cu $(CSRC)/fm_fused_f64.cu $(CSRC)/fm_bin.cu
 OBJS := $(patsubst $(CSRC)/%.cu,$(OBJ)/%.o,$(SRCS))
 
 all: $(LIB)

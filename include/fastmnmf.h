@@ -197,6 +197,18 @@ int fm_prologue(const fm_dims* d, const fm_state* s, void* stream);
  * assignable arrays, separate.py:178-184); the trace index continues. */
 int fm_refresh(const fm_dims* d, const fm_state* s, void* stream);
 
+/* Iteration schedules (fm_schedule). The environment variable
+ * FM_SCHEDULE=split|fused|bin selects one (bin only where eligible). */
+#define FM_SCHED_SPLIT 0
+#define FM_SCHED_FUSED 1
+#define FM_SCHED_BIN 2
+
+/* The schedule fm_iterate / fm_run use for these dims: FM_SCHED_*, or -1
+ * for invalid dims. The per-bin schedule (FM_SCHED_BIN) is three launches
+ * per iteration (k_hstats, k_binw, k_trace) for complex64 with M <= 4,
+ * 2 <= N <= 4, K <= 8. */
+int fm_schedule(const fm_dims* d);
+
 /* One full iteration (separate.py:201-234) on one process. Split schedule
  * (default): ten launches (k_wstats, k_lambda, k_phi, k_hstats, k_lambda,
  * k_gain, k_vacc, k_ip, k_back, k_trace). Fused schedule (FM_SCHEDULE=fused):
@@ -222,7 +234,8 @@ int fm_iterate_phase(const fm_dims* d, const fm_state* s, int phase, void* hstat
  * replay, *n_intervals their count -- split schedule (default, 10): k_wstats,
  * k_lambda, k_phi, k_hstats, k_lambda, k_gain, k_vacc, k_ip, k_back, k_trace;
  * fused schedule (FM_SCHEDULE=fused, 6): k_hpass, k_gpass, k_vacc, k_ip,
- * k_bpass, k_trace. Used by bench.py for the per-kernel roofline. */
+ * k_bpass, k_trace; per-bin schedule (3): k_hstats, k_binw, k_trace. Used by
+ * bench.py for the per-kernel roofline. */
 int fm_iterate_profiled(const fm_dims* d, const fm_state* s, float* ms_host, int* n_intervals,
                         void* stream);
 

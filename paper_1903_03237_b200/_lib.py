@@ -96,6 +96,7 @@ SIGNATURES = [
     ("fm_workspace_bytes", ctypes.c_size_t, [ctypes.POINTER(FmDims)]),
     ("fm_prologue", ctypes.c_int, [ctypes.POINTER(FmDims), ctypes.POINTER(FmState), _vp]),
     ("fm_refresh", ctypes.c_int, [ctypes.POINTER(FmDims), ctypes.POINTER(FmState), _vp]),
+    ("fm_schedule", ctypes.c_int, [ctypes.POINTER(FmDims)]),
     ("fm_iterate", ctypes.c_int, [ctypes.POINTER(FmDims), ctypes.POINTER(FmState), _vp]),
     ("fm_iterate_phase", ctypes.c_int,
      [ctypes.POINTER(FmDims), ctypes.POINTER(FmState), ctypes.c_int, _vp, _vp]),
@@ -115,6 +116,10 @@ SIGNATURES = [
 ]
 
 _lib = None
+
+
+# fm_schedule() values (fastmnmf.h FM_SCHED_*)
+SCHEDULES = {0: "split", 1: "fused", 2: "bin"}
 
 
 def load():

@@ -219,6 +219,11 @@ int fm_refresh(const fm_dims* d, const fm_state* s, void* stream) {
   return FM_BY_DTYPE(d->dtype, prologue(d, s, (cudaStream_t)stream, false));
 }
 
+int fm_schedule(const fm_dims* d) {
+  if (validate_dims(d)) return -1;
+  return d->dp ? FM_SCHED_SPLIT : schedule_of(d);
+}
+
 int fm_iterate(const fm_dims* d, const fm_state* s, void* stream) {
   if (int rc = validate_dims(d)) return rc;
   if (d->dp) { set_error("dims.dp set: use fm_iterate_dp"); return FM_EINVAL; }
@@ -241,7 +246,7 @@ int fm_iterate_profiled(const fm_dims* d, const fm_state* s, float* ms_host, int
   if (d->dp) { set_error("fm_iterate_profiled: plain FastMNMF only"); return FM_EINVAL; }
   cudaStream_t st = (cudaStream_t)stream;
   constexpr int NEV = 11;
-  const int nint = use_fused(d) ? 6 : 10;
+  const int nint = use_bin(d) ? 3 : use_fused(d) ? 6 : 10;
   cudaEvent_t ev[NEV];
   for (int i = 0; i < NEV; ++i) FM_CUDA(cudaEventCreate(&ev[i]));
   cudaStream_t cap = nullptr;

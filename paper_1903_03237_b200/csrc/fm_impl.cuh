@@ -169,13 +169,26 @@ inline int gseg_override() {
   return e ? atoi(e) : 0;
 }
 
-// Schedule of the plain iteration: the split ten-launch one (default; its
-// separate register-tiled NMF contractions measured faster on every BASELINE
-// config) or the fused five-pass one (FM_SCHEDULE=fused).
-inline bool use_fused(const fm_dims*) {
-  const char* e = getenv("FM_SCHEDULE");
-  return e && strcmp(e, "fused") == 0;
+// Schedule of the plain iteration (fastmnmf.h FM_SCHED_*):
+//   split  ten launches, the register-tiled NMF contractions separate
+//   fused  five statistics passes with on-chip lambda (FM_SCHEDULE=fused, §4a)
+//   bin    k_hstats + the per-bin kernel k_binw + k_trace (fm_bin.cuh, §4c):
+//          complex64, M <= 4, N in 2..4, K <= 8, H of a mixture in shared memory
+// FM_SCHEDULE=split|fused|bin forces one (bin only where it is eligible).
+inline bool bin_eligible(const fm_dims* d) {
+  if (d->dtype != FM_F32 || d->dp || d->M > 4 || d->N < 2 || d->N > 4 || d->K > 8) return false;
+  const long long hs = d->N * 8LL * d->T * 4LL;  // staged H (KK = 8 rows per source)
+  return hs + 8LL * 4096 <= 200LL * 1024;
 }
+inline int schedule_of(const fm_dims* d) {
+  const char* e = getenv("FM_SCHEDULE");
+  if (e && strcmp(e, "fused") == 0) return FM_SCHED_FUSED;
+  if (e && strcmp(e, "split") == 0) return FM_SCHED_SPLIT;
+  if (e && strcmp(e, "bin") == 0) return bin_eligible(d) ? FM_SCHED_BIN : FM_SCHED_SPLIT;
+  return FM_SCHED_SPLIT;
+}
+inline bool use_fused(const fm_dims* d) { return schedule_of(d) == FM_SCHED_FUSED; }
+inline bool use_bin(const fm_dims* d) { return !d->dp && schedule_of(d) == FM_SCHED_BIN; }
 
 // M <= 4: register-accumulating gain / V kernels (fm_small.cuh) with
 // FM_SMALL=1 (measured slower than the staged ones at config 2; A/B runs)
@@ -211,6 +224,7 @@ inline unsigned variant_key(const fm_dims* d) {
   return (unsigned)vacc_mode(d) | ((unsigned)(gseg_override() & 0xff) << 4) |
          ((unsigned)(pass_ctas_override() & 0xffff) << 12) | ((unsigned)pass_stages_override() << 28) |
          ((unsigned)use_fused(d) << 31) | ((unsigned)ip_warp_mode(d) << 3) |
+         ((unsigned)use_bin(d) << 30) |
          ((unsigned)small_m_mode() << 2);
 }
 
@@ -383,6 +397,12 @@ template <typename R> struct Impl {
                            cudaStream_t st, cudaEvent_t* ev);
   static int iterate_fused(const fm_dims* d, const fm_state* s, int phase, void* hstat,
                            cudaStream_t st, cudaEvent_t* ev);
+  static int iterate_bin(const fm_dims* d, const fm_state* s, int phase, void* hstat,
+                         cudaStream_t st, cudaEvent_t* ev);
+  static int prologue_bin(const fm_dims* d, const fm_state* s, cudaStream_t st);
+  static int binw(const fm_dims* d, const fm_state* s, cudaStream_t st);
+  static int hstats(const fm_dims* d, const fm_state* s, const R* Wsrc, int mode, void* hstat,
+                    cudaStream_t st);
   static int lambda(const fm_dims* d, const R* W, const R* H, R* lam, cudaStream_t st);
   static int gain(const fm_dims* d, const fm_state* s, cudaStream_t st);
   static int vacc(const fm_dims* d, const fm_state* s, cudaStream_t st);
@@ -660,6 +680,7 @@ int Impl<R>::prologue(const fm_dims* d, const fm_state* s, cudaStream_t st, bool
   const Plan p = make_plan(d);
   unsigned char* w = reinterpret_cast<unsigned char*>(s->work);
   if (reset) FM_CUDA(cudaMemsetAsync(w + p.off_cnt, 0, p.total - p.off_cnt, st));
+  if (use_bin(d)) return prologue_bin(d, s, st);
   if (!use_fused(d)) {  // split: lambda, then x~, data term and phi of the initial state
     if (int rc = lambda(d, reinterpret_cast<const R*>(s->W), reinterpret_cast<const R*>(s->H),
                         reinterpret_cast<R*>(w + p.off_lam), st))
@@ -721,19 +742,7 @@ int Impl<R>::iterate_split(const fm_dims* d, const fm_state* s, int phase, void*
     });
     // H step (separate.py:214-216 with step "H")
     FM_EV(3);
-    FM_DISPATCH_KB(K, {
-      FM_DISPATCH_TILE(p.TT, TTT, {
-        if constexpr (TTT >= 16) {
-          const size_t smh = HsCfg<R, KB, TTT>::bytes;
-          if (int rc = ensure_smem(k_hstats<R, KB, TTT>, smh)) return rc;
-          launch_pdl(k_hstats<R, KB, TTT>, dim3((unsigned)((T + TTT - 1) / TTT), BN, (unsigned)p.HS),
-                     dim3(256), smh, st, phi, W, H, reinterpret_cast<R*>(hstat), N, F, T, K,
-                     phase == 0 ? 1 : 0, 0, p.HFR, reinterpret_cast<R*>(w + p.off_hpart),
-                     reinterpret_cast<unsigned*>(w + p.off_hcnt));
-          FM_CHECK_LAUNCH("k_hstats");
-        }
-      });
-    });
+    if (int rc = hstats(d, s, W, phase == 0 ? 1 : 0, hstat, st)) return rc;
   }
   if (phase == 0) return FM_OK;
   if (phase == 1) {
@@ -759,10 +768,110 @@ int Impl<R>::iterate_split(const fm_dims* d, const fm_state* s, int phase, void*
 #undef FM_EV
 }
 
+// H statistics + MU (mode 0) or the statistics for the all-reduce (mode 1)
+// from the phi in the workspace and the W given (k_hstats, fm_nmf.cuh)
+template <typename R>
+int Impl<R>::hstats(const fm_dims* d, const fm_state* s, const R* Wsrc, int mode, void* hstat,
+                    cudaStream_t st) {
+  const Plan p = make_plan(d);
+  unsigned char* w = reinterpret_cast<unsigned char*>(s->work);
+  const R* phi = reinterpret_cast<const R*>(w + p.off_phi);
+  R* H = reinterpret_cast<R*>(s->H);
+  const int N = (int)d->N, F = (int)d->F, T = (int)d->T, K = (int)d->K;
+  const unsigned BN = (unsigned)(d->B * (d->N - (d->dp ? 1 : 0)));
+  FM_DISPATCH_KB(K, {
+    FM_DISPATCH_TILE(p.TT, TTT, {
+      if constexpr (TTT >= 16) {
+        const size_t smh = HsCfg<R, KB, TTT>::bytes;
+        if (int rc = ensure_smem(k_hstats<R, KB, TTT>, smh)) return rc;
+        launch_pdl(k_hstats<R, KB, TTT>, dim3((unsigned)((T + TTT - 1) / TTT), BN, (unsigned)p.HS),
+                   dim3(256), smh, st, phi, Wsrc, H, reinterpret_cast<R*>(hstat), N, F, T, K,
+                   mode, 0, p.HFR, reinterpret_cast<R*>(w + p.off_hpart),
+                   reinterpret_cast<unsigned*>(w + p.off_hcnt));
+        FM_CHECK_LAUNCH("k_hstats");
+      }
+    });
+  });
+  return FM_OK;
+}
+
+// The per-bin schedule (fm_bin.cuh): the W step of the first iteration and
+// the refresh after it run here (k_lambda, k_back, k_wstats on Wn, k_lambda,
+// k_phi), leaving x~, Wn and phi; each iteration is then
+//   k_hstats  H step from phi(Wn, H)                        (separate.py:214-216 "H")
+//   k_binw    gains, V, IP, normalisations, W = Wn c, x~, data term, the
+//             next W step -> Wn and its refresh -> phi      (separate.py:217-234,
+//                                                           :186-193, :214-216 "W")
+//   k_trace
+// The state W stays the reference's (after the absorb); fm_refresh re-runs
+// this prologue after a caller assigns state.
+template <typename R>
+int Impl<R>::prologue_bin(const fm_dims* d, const fm_state* s, cudaStream_t st) {
+  const Plan p = make_plan(d);
+  unsigned char* w = reinterpret_cast<unsigned char*>(s->work);
+  R* lam = reinterpret_cast<R*>(w + p.off_lam);
+  R* phi = reinterpret_cast<R*>(w + p.off_phi);
+  R* Wn = reinterpret_cast<R*>(w + p.off_wn);
+  const R* H = reinterpret_cast<const R*>(s->H);
+  const int N = (int)d->N, F = (int)d->F, T = (int)d->T, K = (int)d->K;
+  if (int rc = lambda(d, reinterpret_cast<const R*>(s->W), H, lam, st)) return rc;
+  if (int rc = back(d, s, /*tail_only=*/1, /*record=*/0, st)) return rc;  // x~, data term, phi
+  FM_CUDA(cudaMemcpyAsync(Wn, s->W, (size_t)d->B * N * F * K * sizeof(R), cudaMemcpyDeviceToDevice, st));
+  FM_DISPATCH_KB(K, {
+    FM_DISPATCH_TILE(p.FT, FTT, {
+      if constexpr (FTT <= 32) {
+        const size_t smw = WsCfg<R, KB, FTT>::bytes;
+        if (int rc = ensure_smem(k_wstats<R, KB, FTT>, smw)) return rc;
+        launch_pdl(k_wstats<R, KB, FTT>, dim3((unsigned)((F + FTT - 1) / FTT), (unsigned)(d->B * N)),
+                   dim3(256), smw, st, phi, H, Wn, N, F, T, K, 0);
+        FM_CHECK_LAUNCH("k_wstats");
+      }
+    });
+  });
+  if (int rc = lambda(d, Wn, H, lam, st)) return rc;
+  FM_DISPATCH_M(d->M, {
+    launch_pdl(k_phi<R, MM>, dim3((unsigned)((T + 255) / 256), (unsigned)F, (unsigned)d->B),
+               dim3(256), 0, st, lam, reinterpret_cast<const R*>(s->xt),
+               reinterpret_cast<const R*>(s->g), reinterpret_cast<const R*>(s->floor), phi, N, F, T);
+    FM_CHECK_LAUNCH("k_phi");
+  });
+  return FM_OK;
+}
+
+template <typename R>
+int Impl<R>::iterate_bin(const fm_dims* d, const fm_state* s, int phase, void* hstat,
+                         cudaStream_t st, cudaEvent_t* ev) {
+#define FM_EV(i) \
+  if (ev) FM_CUDA(cudaEventRecordWithFlags(ev[i], st, cudaEventRecordExternal));
+  const Plan p = make_plan(d);
+  unsigned char* w = reinterpret_cast<unsigned char*>(s->work);
+  R* H = reinterpret_cast<R*>(s->H);
+  FM_EV(0);
+  if (phase == 0 || phase == 2) {
+    if (int rc = hstats(d, s, reinterpret_cast<const R*>(w + p.off_wn), phase == 0 ? 1 : 0, hstat, st))
+      return rc;
+  }
+  if (phase == 0) return FM_OK;
+  if (phase == 1) {
+    const long long NKT = d->N * d->K * d->T, total = d->B * NKT;
+    k_hupdate<R><<<(unsigned)((total + 255) / 256), 256, 0, st>>>(
+        nullptr, H, reinterpret_cast<R*>(hstat), 1, NKT, total, 2);
+    FM_CHECK_LAUNCH("k_hupdate");
+  }
+  FM_EV(1);
+  if (int rc = binw(d, s, st)) return rc;
+  FM_EV(2);
+  if (int rc = trace(d, s, st)) return rc;
+  FM_EV(3);
+  return FM_OK;
+#undef FM_EV
+}
+
 template <typename R>
 int Impl<R>::iterate_phase(const fm_dims* d, const fm_state* s, int phase, void* hstat,
                            cudaStream_t st, cudaEvent_t* ev) {
   if (d->dp) { set_error("deep-prior dims: use fm_iterate_dp"); return FM_EINVAL; }
+  if (use_bin(d)) return iterate_bin(d, s, phase, hstat, st, ev);
   return use_fused(d) ? iterate_fused(d, s, phase, hstat, st, ev)
                       : iterate_split(d, s, phase, hstat, st, ev);
 }

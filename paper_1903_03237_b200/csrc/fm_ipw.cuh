@@ -79,19 +79,20 @@ __device__ void warp_inv_hpd_batch(C* A, int* fail, float* d0, float ratio, int 
   }
 }
 
-template <typename R, int M>
-__global__ void __launch_bounds__(32 * IPW_WARPS) k_ip_w(IpArgs<R> a) {
-  pdl_entry();
-  using C = cplx<R>;
+// The warp-private IP of one bin (A3 + the A4 row / gain normalisation) on
+// the warp's IpwSmem region: Vi holds the M V_m (fp32 for complex64, else
+// fp64 in Vd), Qd the bin's Q, gs its gains after the MU. fill64(m, Vm)
+// writes V_m in fp64 into Vm for the fp32-pivot retry. Leaves the new Q in
+// Qd, the normalised gains in gs, the gain scales in cs, and returns the
+// status code (0 ok, 1 non-positive norm at bad_m, 2 singular Q) and
+// log|det Q| of the result. Shared by k_ip_w and the per-bin schedule's
+// k_binw (fm_bin.cuh).
+template <typename R, int M, typename Fill64>
+__device__ __forceinline__ void ipw_core(unsigned char* sm, int lane, int N, int ip_sweeps,
+                                         int normalize, Fill64&& fill64, double& ldet, int& code,
+                                         int& bad_m) {
   using L = IpwSmem<R, M>;
   using VC = typename L::VC;
-  extern __shared__ __align__(16) unsigned char small[];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const long long gbf = (long long)blockIdx.x * IPW_WARPS + warp;  // b * F + f
-  if (gbf >= (long long)a.B * a.F) return;  // warp-uniform: no CTA barrier below
-  const int F = a.F, N = a.N, K = a.K;
-  const int b = (int)(gbf / F), f = (int)(gbf % F);
-  unsigned char* sm = small + (size_t)warp * L::bytes;
   double2* Vd = reinterpret_cast<double2*>(sm + L::o_Vd);
   VC* Vi = sizeof(R) == 4 ? reinterpret_cast<VC*>(sm + L::o_Vi) : reinterpret_cast<VC*>(Vd);
   double2* Qd = reinterpret_cast<double2*>(sm + L::o_Qd);
@@ -105,43 +106,6 @@ __global__ void __launch_bounds__(32 * IPW_WARPS) k_ip_w(IpArgs<R> a) {
   int* vfail = reinterpret_cast<int*>(rown + M);
   int* v64 = vfail + M;  // complex64: V_m^-1 kept in fp64 (Vd) after a retry
   float* d0 = reinterpret_cast<float*>(sm + L::o_d0);
-  C* Qg = a.Q + ((size_t)b * F + f) * M * M;
-  R* gg = a.g + (size_t)b * N * F * M + (size_t)f * M;
-  R* Wg = a.W + (size_t)b * (N - a.n0) * F * K + (size_t)f * K;
-  const R* Wsg = a.Wsrc + (size_t)b * (N - a.n0) * F * K + (size_t)f * K;
-  const unsigned it = *a.iter;
-  const long long fglob = a.f_offset + f;
-  {  // V_f = (1/T) sum over the segment partials (fixed order, fp64), mirrored
-    constexpr int P = M * (M + 1) / 2;
-    const C* vp = a.Vpart + ((size_t)b * F + f) * a.nseg * M * P;
-    const double invT = 1.0 / (double)a.T;
-    for (int e = lane; e < M * P; e += 32) {
-      double2 acc = make_double2(0.0, 0.0);
-      for (int q = 0; q < a.nseg; ++q) {
-        const C c = vp[(size_t)q * M * P + e];
-        acc.x += (double)c.x;
-        acc.y += (double)c.y;
-      }
-      const int m = e / P;
-      int i = 0, r = e % P;
-      while (r >= M - i) {
-        r -= M - i;
-        ++i;
-      }
-      const int j = i + r;
-      const double2 d = make_double2(acc.x * invT, acc.y * invT);
-      if constexpr (sizeof(R) == 4) {
-        Vi[((size_t)m * M + i) * M + j] = make_float2((float)d.x, (float)d.y);
-        if (i != j) Vi[((size_t)m * M + j) * M + i] = make_float2((float)d.x, (float)-d.y);
-      } else {
-        Vd[((size_t)m * M + i) * M + j] = d;
-        if (i != j) Vd[((size_t)m * M + j) * M + i] = make_double2(d.x, -d.y);
-      }
-    }
-  }
-  for (int e = lane; e < M * M; e += 32) Qd[e] = to_d2(Qg[e]);
-  for (int e = lane; e < N * M; e += 32)
-    gs[e] = a.gnew[(size_t)b * N * F * M + (size_t)(e / M) * F * M + (size_t)f * M + (e % M)];
   if (lane < NMAX) cs[lane] = R(1);
   __syncwarp();
   // ---- A3: iterative projection (spatial.py:181-199) -------------------------
@@ -150,7 +114,7 @@ __global__ void __launch_bounds__(32 * IPW_WARPS) k_ip_w(IpArgs<R> a) {
     Ai[e] = c < M ? Qd[r * M + c] : make_double2(c - M == r ? 1.0 : 0.0, 0.0);
   }
   __syncwarp();
-  double ldet = 0.0;
+  ldet = 0.0;
   const bool qok = warp_inv_pivot<M>(Ai, lane, &ldet);
   if (lane < M) v64[lane] = 0;
   warp_inv_hpd_batch<VC, M>(Vi, vfail, d0, sizeof(R) == 4 ? 1e-3f : 0.0f, lane);  // V_m^-1, all m
@@ -159,26 +123,8 @@ __global__ void __launch_bounds__(32 * IPW_WARPS) k_ip_w(IpArgs<R> a) {
     // fp64 from the partials before the reference's error is raised
     for (int m = 0; m < M; ++m) {
       if (!vfail[m]) continue;  // warp-uniform
-      constexpr int P = M * (M + 1) / 2;
-      const C* vp = a.Vpart + ((size_t)b * F + f) * a.nseg * M * P + (size_t)m * P;
       double2* Vm = Vd + (size_t)m * M * M;
-      for (int e = lane; e < P; e += 32) {
-        double2 acc = make_double2(0.0, 0.0);
-        for (int q = 0; q < a.nseg; ++q) {
-          const C c = vp[(size_t)q * M * P + e];
-          acc.x += (double)c.x;
-          acc.y += (double)c.y;
-        }
-        int i = 0, r = e;
-        while (r >= M - i) {
-          r -= M - i;
-          ++i;
-        }
-        const int j = i + r;
-        const double2 d = make_double2(acc.x / (double)a.T, acc.y / (double)a.T);
-        Vm[i * M + j] = d;
-        if (i != j) Vm[j * M + i] = make_double2(d.x, -d.y);
-      }
+      fill64(m, Vm);  // V_m in fp64 (the caller's sums)
       __syncwarp();
       const bool ok = warp_inv_hpd<M>(Vm, lane);
       __syncwarp();
@@ -190,11 +136,12 @@ __global__ void __launch_bounds__(32 * IPW_WARPS) k_ip_w(IpArgs<R> a) {
     }
   }
   double nprod = 1.0;
-  int code = qok ? 0 : 2, bad_m = 0;  // singular Q -> singular Q V at m = 0
+  code = qok ? 0 : 2;
+  bad_m = 0;  // singular Q -> singular Q V at m = 0
   constexpr int GL = M <= 1 ? 32 : M <= 2 ? 16 : M <= 4 ? 8 : 4;  // lanes per row
   const int ri = lane / GL, sub = lane % GL;
   const bool rv = ri < M;
-  for (int sw = 0; sw < a.ip_sweeps && code == 0; ++sw) {
+  for (int sw = 0; sw < ip_sweeps && code == 0; ++sw) {
     for (int m = 0; m < M; ++m) {
       if (vfail[m]) {
         code = 1;
@@ -266,10 +213,9 @@ __global__ void __launch_bounds__(32 * IPW_WARPS) k_ip_w(IpArgs<R> a) {
       __syncwarp();
     }
   }
-  if (code && lane == 0) report_status(a.status, it, bad_m, fglob, code);
   ldet += 0.5 * log(nprod);
   // ---- A4: row normalisation, gain normalisation + absorb ---------------------
-  if (a.normalize) {
+  if (normalize) {
     if (lane < M) {
       double s = 0.0;
 #pragma unroll
@@ -302,6 +248,93 @@ __global__ void __launch_bounds__(32 * IPW_WARPS) k_ip_w(IpArgs<R> a) {
       for (int m = 0; m < M; ++m) gs[lane * M + m] = gs[lane * M + m] * scl;
       cs[lane] = s / R(M);
     }
+    __syncwarp();
+  }
+}
+
+template <typename R, int M>
+__global__ void __launch_bounds__(32 * IPW_WARPS) k_ip_w(IpArgs<R> a) {
+  pdl_entry();
+  using C = cplx<R>;
+  using L = IpwSmem<R, M>;
+  using VC = typename L::VC;
+  extern __shared__ __align__(16) unsigned char small[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const long long gbf = (long long)blockIdx.x * IPW_WARPS + warp;  // b * F + f
+  if (gbf >= (long long)a.B * a.F) return;  // warp-uniform: no CTA barrier below
+  const int F = a.F, N = a.N, K = a.K;
+  const int b = (int)(gbf / F), f = (int)(gbf % F);
+  unsigned char* sm = small + (size_t)warp * L::bytes;
+  double2* Vd = reinterpret_cast<double2*>(sm + L::o_Vd);
+  VC* Vi = sizeof(R) == 4 ? reinterpret_cast<VC*>(sm + L::o_Vi) : reinterpret_cast<VC*>(Vd);
+  double2* Qd = reinterpret_cast<double2*>(sm + L::o_Qd);
+  R* gs = reinterpret_cast<R*>(sm + L::o_gs);
+  R* cs = reinterpret_cast<R*>(sm + L::o_cs);
+  C* Qg = a.Q + ((size_t)b * F + f) * M * M;
+  R* gg = a.g + (size_t)b * N * F * M + (size_t)f * M;
+  R* Wg = a.W + (size_t)b * (N - a.n0) * F * K + (size_t)f * K;
+  const R* Wsg = a.Wsrc + (size_t)b * (N - a.n0) * F * K + (size_t)f * K;
+  const unsigned it = *a.iter;
+  const long long fglob = a.f_offset + f;
+  {  // V_f = (1/T) sum over the segment partials (fixed order, fp64), mirrored
+    constexpr int P = M * (M + 1) / 2;
+    const C* vp = a.Vpart + ((size_t)b * F + f) * a.nseg * M * P;
+    const double invT = 1.0 / (double)a.T;
+    for (int e = lane; e < M * P; e += 32) {
+      double2 acc = make_double2(0.0, 0.0);
+      for (int q = 0; q < a.nseg; ++q) {
+        const C c = vp[(size_t)q * M * P + e];
+        acc.x += (double)c.x;
+        acc.y += (double)c.y;
+      }
+      const int m = e / P;
+      int i = 0, r = e % P;
+      while (r >= M - i) {
+        r -= M - i;
+        ++i;
+      }
+      const int j = i + r;
+      const double2 d = make_double2(acc.x * invT, acc.y * invT);
+      if constexpr (sizeof(R) == 4) {
+        Vi[((size_t)m * M + i) * M + j] = make_float2((float)d.x, (float)d.y);
+        if (i != j) Vi[((size_t)m * M + j) * M + i] = make_float2((float)d.x, (float)-d.y);
+      } else {
+        Vd[((size_t)m * M + i) * M + j] = d;
+        if (i != j) Vd[((size_t)m * M + j) * M + i] = make_double2(d.x, -d.y);
+      }
+    }
+  }
+  for (int e = lane; e < M * M; e += 32) Qd[e] = to_d2(Qg[e]);
+  for (int e = lane; e < N * M; e += 32)
+    gs[e] = a.gnew[(size_t)b * N * F * M + (size_t)(e / M) * F * M + (size_t)f * M + (e % M)];
+  __syncwarp();
+  double ldet = 0.0;
+  int code = 0, bad_m = 0;
+  ipw_core<R, M>(sm, lane, N, a.ip_sweeps, a.normalize,
+                 [&](int m, double2* Vm) {  // V_m from the partials in fp64
+                   constexpr int P = M * (M + 1) / 2;
+                   const C* vp = a.Vpart + ((size_t)b * F + f) * a.nseg * M * P + (size_t)m * P;
+                   for (int e = lane; e < P; e += 32) {
+                     double2 acc = make_double2(0.0, 0.0);
+                     for (int q = 0; q < a.nseg; ++q) {
+                       const C c = vp[(size_t)q * M * P + e];
+                       acc.x += (double)c.x;
+                       acc.y += (double)c.y;
+                     }
+                     int i = 0, r = e;
+                     while (r >= M - i) {
+                       r -= M - i;
+                       ++i;
+                     }
+                     const int j = i + r;
+                     const double2 d = make_double2(acc.x / (double)a.T, acc.y / (double)a.T);
+                     Vm[i * M + j] = d;
+                     if (i != j) Vm[j * M + i] = make_double2(d.x, -d.y);
+                   }
+                 },
+                 ldet, code, bad_m);
+  if (code && lane == 0) report_status(a.status, it, bad_m, fglob, code);
+  if (a.normalize) {
     __syncwarp();
     const int Nn = N - a.n0;
     for (int e = lane; e < Nn * K; e += 32) {

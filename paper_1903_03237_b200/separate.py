@@ -352,6 +352,12 @@ class DeviceLoop:
 
     # ---- batched device helpers ----
     @property
+    def schedule(self):
+        """The iteration schedule the library runs for these dims: "split",
+        "fused" or "bin" (fastmnmf.h fm_schedule)."""
+        return _lib.SCHEDULES[_lib.load().fm_schedule(ctypes.byref(self.dims))]
+
+    @property
     def xt_FTM(self):
         return self.xt_dev[0]
 

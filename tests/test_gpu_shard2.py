@@ -17,7 +17,7 @@ from paper_1903_03237_b200.synth import baseline_init, make_mixture
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("schedule", ["split", "fused"])
+@pytest.mark.parametrize("schedule", ["split", "fused", "bin"])
 @pytest.mark.parametrize("precision,tol", [("complex64", 1e-5), ("complex128", 1e-11)])
 def test_two_shards_equal_unsharded(precision, tol, schedule, monkeypatch):
     import torch
