@@ -155,7 +155,7 @@ struct Plan {
 inline int vacc_mode(const fm_dims* d) {
   const char* e = getenv("FM_VACC");
   if (e && strcmp(e, "simt") == 0) return 1;
-  if (e && strcmp(e, "tc") == 0) return d->M >= 12 ? 2 : 1;
+  if (e && strcmp(e, "tc") == 0) return (d->M >= 10 && d->M % 2 == 0) ? 2 : 1;
   if (e && strcmp(e, "blk") == 0) return 0;
   // measured on B200: pair-per-thread wins at M = 4 (c2: 1.13 vs 1.89 ms) and
   // M = 8 (c1: 39.1 vs 40.8 us); the blocked kernel at M = 16 (c3: 2.00 ms vs
@@ -270,6 +270,16 @@ inline Plan make_plan(const fm_dims* d) {
     const long long vs = std::max<long long>(1, (slots + F * B - 1) / (F * B));
     long long vtr = (T + vs - 1) / vs;
     vtr = std::max<long long>(tbv, (vtr + tbv - 1) / tbv * tbv);
+    p.VTR = (int)vtr;
+    p.vnseg = (int)((T + vtr - 1) / vtr);
+  }
+  if (d->dtype == FM_F32 && vacc_mode(d) == 2) {
+    // k_vacc_tc: two CTAs per SM; segments of whole 128-frame blocks, at least
+    // eight blocks each, until the (bin, segment) CTAs make ~6 waves
+    const long long slots = 2 * 148, blocks = (T + 127) / 128;
+    long long vs = std::max<long long>(1, (6 * slots + F * B - 1) / (F * B));
+    vs = std::max<long long>(1, std::min(vs, blocks / 8));
+    const long long vtr = (blocks + vs - 1) / vs * 128;
     p.VTR = (int)vtr;
     p.vnseg = (int)((T + vtr - 1) / vtr);
   }
@@ -530,11 +540,14 @@ int Impl<R>::vacc(const fm_dims* d, const fm_state* s, cudaStream_t st) {
   const int mode = vacc_mode(d);
   FM_DISPATCH_M(d->M, {
     if constexpr (sizeof(R) == 4) {
-      if constexpr (MM >= 12) {
+      if constexpr (MM >= 10 && MM % 2 == 0) {
         if (mode == 2) {
           const size_t smv = VtcCfg<MM>::SMEM;
           if (int rc = ensure_smem(k_vacc_tc<MM>, smv)) return rc;
-          launch_pdl(k_vacc_tc<MM>, grid, dim3(VtcCfg<MM>::BS), smv, st, a);
+          VaccArgs<float> at = *reinterpret_cast<VaccArgs<float>*>(&a);
+          at.TR = p.VTR;
+          launch_pdl(k_vacc_tc<MM>, dim3((unsigned)p.vnseg, (unsigned)d->F, (unsigned)d->B),
+                     dim3(VtcCfg<MM>::BS), smv, st, at);
           FM_CHECK_LAUNCH("k_vacc_tc");
           return FM_OK;
         }

@@ -239,7 +239,7 @@ template <typename R> struct VaccArgs {
   R* part;         // (B, F, nseg, M, P) complex partial V sums
   int F, T, N, TR;
   int gseg;        // k_gain segments per bin (k_vacc_blk's own segmentation may differ)
-  int dbg;         // timing experiments only (k_vacc_tc): 1 skip MMAs, 2 skip operand builds
+  int dbg;         // timing experiments only (k_vacc_tc), bits: 1 skip MMAs, 2 skip operand builds, 4 one MMA of three
 };
 
 // g MU (separate.py:218-220) + V_fm = (1/T) sum_t x x^H / y_ftm with y from

@@ -1,59 +1,68 @@
 // fm_vacc_tc.cuh -- the V_fm accumulation on the 5th-generation tensor cores
-// (complex64 path, _kernels.py:276-293, spatial.py:182).
+// (complex64 path, even M >= 12, _kernels.py:276-293,
+// spatial.py:182).
 //
 // V_fm[i,k] = sum_t iy[t,m] x_i(t) conj(x_k(t)) is, per bin f, one small GEMM
 //   D[j][m] = sum_t A[j][t] B[m][t]
 // with A[j][t] the M*M real components of the Hermitian outer product
-// x(t) x(t)^H (rows j < P = M(M+1)/2: Re of pair p = j in the k_vacc/k_ip pair
-// order; rows j >= P: Im of the (j-P)-th off-diagonal pair) and B[m][t] =
-// 1/y(t, m). The SIMT threads build A and B for a chunk of KC frames (the
-// outer products are M-fold cheaper than the weighted accumulation they
-// replace), one thread issues tcgen05.mma.kind::tf32 into a TMEM accumulator
-// (128-lane tiles), and tcgen05.commit on a per-stage mbarrier hands the
-// stage back. Precision: 3xTF32 (A_hi B_hi + A_hi B_lo + A_lo B_hi with
-// hi = rna-rounded TF32, lo = residual), i.e. fp32-level products with fp32
-// accumulation -- the same arithmetic class as the SIMT k_vacc.
+// x(t) x(t)^H and B[m][t] = 1/y(t, m). Building A costs O(M^2) per frame, M
+// times less than the weighted SIMT accumulation it replaces.
 //
-// Shared-memory operand layout: UMMA K-major, no swizzle: 8-row x 16-byte
-// core matrices, LBO = 128 B between the K-adjacent cores, SBO = (KC/4)*128 B
-// between 8-row groups. The gain MU that k_vacc finishes is done identically.
-// grid (nseg, F, B), block 256; fp32 only.
+// Warp-specialised, mbarrier-pipelined, no CTA barrier in the frame loop:
+//   loader warps (4)  X of a 128-frame block by one bulk async copy
+//                     (cp.async.bulk, the block is contiguous in (B,F,T,M));
+//                     1/y from lambda and the updated gains, rounded and split
+//                     into TF32 hi / lo planes written straight into the UMMA
+//                     K-major layout of the block (rows 0..15 hi, 16..31 lo)
+//   producer warps (8) a thread owns accumulator lane L of BOTH 128-lane
+//                     tiles: Re (tile 0) and Im (tile 1) of off-diagonal pair L
+//                     (L < M(M-1)/2), or |x_d|^2 of two diagonal entries (lanes
+//                     120..127); per 16-frame chunk it forms its products for 8
+//                     frames from shared x rows, splits them hi / lo and
+//                     stores them to TMEM (tcgen05.st) as the A operand
+//   MMA warp (1 lane)  per chunk and tile, per 8-frame k-step:
+//                     D0 += A_hi [B_hi | B_lo]  (one N = 32 MMA) and
+//                     D1 += A_lo B_hi           (N = 16); tcgen05.commit hands
+//                     the operand stage (and, per block, the block buffers) back
+// Precision: 3xTF32 (A_hi B_hi + A_hi B_lo + A_lo B_hi, fp32 accumulation in
+// TMEM; D0's halves and D1 are summed in the epilogue) -- fp32-class products,
+// the same arithmetic class as the SIMT k_vacc. The gain MU that k_vacc
+// finishes is done identically. grid (nseg, F, B), block 416; fp32 only.
 #pragma once
 #include "fm_spatial.cuh"
 
 namespace fm {
 
 template <int M> struct VtcCfg {
+  // used for even M in 10..16 (Impl::vacc); instantiable for every M
   static constexpr int P = M * (M + 1) / 2;
-  static constexpr int J = M * M;                  // real rows of A
-  static constexpr int NTILE = (J + 127) / 128;    // 128-lane tiles (A and accumulator)
-  static constexpr int NB = (M + 7) / 8 * 8;       // MMA N (weights per m, padded)
-  static constexpr int KC = 16;                    // frames per chunk (KC/8 MMA k-steps)
-  static constexpr int BS = 256;
-  static constexpr int WG = 8 / (4 * NTILE);       // warp groups sharing a tile's rows (split frames)
-  static constexpr int KW = KC / WG;               // frames per thread per chunk
-  static constexpr int SBO = (KC / 4) * 128;       // B plane: bytes between 8-row core groups
-  static constexpr int BBYTES = NB * KC * 4;       // one B plane (hi or lo)
-  static constexpr int TBLK = M <= 8 ? 256 : 128;  // frames staged per block (x, 1/y)
-  static constexpr int STAGE = 2 * BBYTES;
-  static constexpr int XS = 2 * STAGE;             // x block (M x TBLK complex, padded rows)
-  static constexpr int XLD = TBLK + 2;             // x row pitch (complex): rows land on distinct banks
-  static constexpr int IYS = XS + XLD * M * 8;     // 1/y block (M x TBLK)
-  static constexpr int SMEM = IYS + TBLK * M * 4;
-  // TMEM columns: accumulator [0, NTILE*NB), then per stage, tile and plane (hi, lo) KC columns
-  static constexpr int ACOL = 32;
-  static constexpr int TCOLS_USED = ACOL + 2 * NTILE * 2 * KC;
-  static constexpr int TCOLS = TCOLS_USED <= 128 ? 128 : TCOLS_USED <= 256 ? 256 : 512;
-  static_assert(NTILE * NB <= ACOL, "accumulator columns");
-  static_assert(WG >= 1 && KC % WG == 0, "warp groups");
+  static constexpr int PO = M * (M - 1) / 2;       // off-diagonal pairs (<= 120): lanes [0, PO)
+  static constexpr int DL = 120;                   // first diagonal lane (8 per tile)
+  static constexpr int NB = 16;                    // weight rows per plane (m, zero-padded)
+  static constexpr int KC = 16;                    // frames per chunk (two MMA k-steps)
+  static constexpr int TBLK = 128;                 // frames per staged block
+  static constexpr int NPROD = 8, NLOAD = 4;       // warps
+  static constexpr int MMAW = NPROD;               // the MMA warp
+  static constexpr int BS = (NPROD + 1 + NLOAD) * 32;
+  static constexpr int XB = TBLK * M * 8;          // x block (frames x channels, complex)
+  static constexpr int WB = 2 * NB * TBLK * 4;     // weight block: hi rows then lo rows
+  static constexpr int SBO = (TBLK / 4) * 128;     // bytes between 8-row core groups
+  static constexpr int OFF_W = 2 * XB;
+  static constexpr int OFF_L = OFF_W + 2 * WB;     // loader warps' lambda rows (cp.async)
+  static constexpr int SMEM = OFF_L + NLOAD * 2 * NMAX * 8 * 16;
+  static constexpr int S = 2;                      // operand stages in TMEM
+  // TMEM columns: per tile D0 (32) and D1 (16); then per stage, tile and plane KC columns
+  static constexpr int DCOLS = 48, ACOL = 2 * DCOLS;
+  static constexpr int TCOLS = 256;
+  static_assert(ACOL + S * 2 * 2 * KC <= TCOLS, "tensor memory columns");
 };
-__host__ __device__ constexpr int vtc_acol(int stage, int tile, int plane, int ntile, int kc) {
-  return 32 + ((stage * ntile + tile) * 2 + plane) * kc;
+__host__ __device__ constexpr int vtc_acol(int stage, int tile, int plane) {
+  return 96 + ((stage * 2 + tile) * 2 + plane) * 16;
 }
 
-// byte offset of element (row, k) in a K-major no-swizzle operand plane
+// byte offset of element (row, k) in the block's K-major no-swizzle weight plane
 template <int M> __device__ __forceinline__ uint32_t vtc_off(int row, int k) {
-  return (uint32_t)((((row >> 3) * (VtcCfg<M>::KC / 4) + (k >> 2)) * 128) + ((row & 7) * 16) +
+  return (uint32_t)((((row >> 3) * (VtcCfg<M>::TBLK / 4) + (k >> 2)) * 128) + ((row & 7) * 16) +
                     ((k & 3) * 4));
 }
 
@@ -65,10 +74,12 @@ __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint
   return d;                // base offset 0, layout SWIZZLE_NONE
 }
 
+// Round to TF32 (10 mantissa bits), nearest with ties away from zero -- what
+// cvt.rna.tf32.f32 returns for finite normal inputs -- with two integer
+// operations: the conversion instruction issues at 16 lanes per clock per SM
+// and was the limit of the operand build (8192 per 16-frame chunk).
 __device__ __forceinline__ float tf32_rna(float v) {
-  uint32_t r;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(v));
-  return __uint_as_float(r);
+  return __uint_as_float((__float_as_uint(v) + 0x1000u) & 0xFFFFE000u);
 }
 
 __device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
@@ -149,247 +160,341 @@ template <int NB> __device__ __forceinline__ void tmem_ld_row(uint32_t taddr, fl
   for (int i = 0; i < NB; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"((unsigned)__cvta_generic_to_shared(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                   (unsigned)__cvta_generic_to_shared(bar)),
+               "r"(bytes)
+               : "memory");
+}
+// global -> shared bulk async copy (TMA engine, no tensor map); completes on the mbarrier
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          (unsigned)__cvta_generic_to_shared(dst)),
+      "l"(src), "r"(bytes), "r"((unsigned)__cvta_generic_to_shared(bar))
+      : "memory");
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   (unsigned)__cvta_generic_to_shared(bar))
+               : "memory");
+}
+// 16 accumulator columns of this thread's lane, no wait
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, "
+      "[%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
 template <int M>
-__global__ void __launch_bounds__(256) k_vacc_tc(VaccArgs<float> a) {
+__global__ void __launch_bounds__(VtcCfg<M>::BS, 2) k_vacc_tc(VaccArgs<float> a) {
   pdl_entry();
   using Cf = VtcCfg<M>;
   using C = float2;
-  constexpr int P = Cf::P, J = Cf::J, NTILE = Cf::NTILE, NB = Cf::NB, KC = Cf::KC, BS = Cf::BS;
-  constexpr int KW = Cf::KW;
+  constexpr int P = Cf::P, PO = Cf::PO, DL = Cf::DL, KC = Cf::KC, TBLK = Cf::TBLK, S = Cf::S;
+  constexpr int BS = Cf::BS;
   extern __shared__ __align__(1024) unsigned char smv[];
-  __shared__ __align__(8) uint64_t mbar[2];
+  // mbarriers: block buffers full (x landed + weights written) / empty (producers and
+  // MMAs done with them), operand stages full / empty, all MMAs done
+  __shared__ __align__(8) uint64_t bfull[2], bempty[2], sfull[S], sempty[S], done;
   __shared__ uint32_t tmem_base;
-  __shared__ __align__(16) float gs[NMAX * M];
-  __shared__ unsigned char pairI[P], pairK[P];
-  __shared__ short pairIm[P];  // A row of Im(pair), -1 on the diagonal
+  __shared__ __align__(16) float gs[NMAX * 16];  // updated gains, m padded to 16 with zeros
   const int seg = blockIdx.x, f = blockIdx.y, b = blockIdx.z, nseg = gridDim.x;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int N = a.N, T = a.T, F = a.F;
   const size_t FT = (size_t)F * T;
   const int ta = seg * a.TR, tb = min(T, ta + a.TR);
+  const int nblk = (tb - ta + TBLK - 1) / TBLK;
 
   // gain MU from the k_gain segment partials (fixed order; as k_vacc)
-  for (int e = tid; e < N * M; e += BS) {
-    const int n = e / M, m = e % M;
-    const float* gp = a.gpart + ((size_t)b * F + f) * a.gseg * N * 2 * M + n * 2 * M;
-    float sn = 0, sd = 0;
-    for (int q = 0; q < a.gseg; ++q) {
-      sn += gp[(size_t)q * N * 2 * M + m];
-      sd += gp[(size_t)q * N * 2 * M + M + m];
+  for (int e = tid; e < NMAX * 16; e += BS) {
+    const int n = e >> 4, m = e & 15;
+    float gv = 0.f;
+    if (n < N && m < M) {
+      const float* gp = a.gpart + ((size_t)b * F + f) * a.gseg * N * 2 * M + n * 2 * M;
+      float sn = 0, sd = 0;
+      for (int q = 0; q < a.gseg; ++q) {
+        sn += gp[(size_t)q * N * 2 * M + m];
+        sd += gp[(size_t)q * N * 2 * M + M + m];
+      }
+      const size_t gi = (size_t)b * N * F * M + (size_t)n * F * M + (size_t)f * M + m;
+      gv = a.g[gi] * mu_factor(sn, sd);
+      if (seg == 0) a.gnew[gi] = gv;
     }
-    const size_t gi = (size_t)b * N * F * M + (size_t)n * F * M + (size_t)f * M + m;
-    const float gv = a.g[gi] * mu_factor(sn, sd);
     gs[e] = gv;
-    if (seg == 0) a.gnew[gi] = gv;
   }
-  // pair p = (i <= k) in the k_vacc / k_ip order; its Re is A row p, its Im
-  // (off-diagonal pairs only) A row P + (index among the off-diagonal pairs)
-  for (int p = tid; p < P; p += BS) {
-    int i = 0, r = p;
-    while (r >= M - i) {
-      r -= M - i;
-      ++i;
-    }
-    pairI[p] = (unsigned char)i;
-    pairK[p] = (unsigned char)(i + r);
-    pairIm[p] = r == 0 ? (short)-1 : (short)(P + p - i - 1);  // off-diagonals before p: p - (i + 1)
-  }
-  if (warp == 0) {
+  // x buffers start as zeros: the frames of a ragged last chunk beyond the copied
+  // ones are read with zero weights and must hold finite values
+  for (int e = tid; e < 2 * Cf::XB / 16; e += BS)
+    reinterpret_cast<float4*>(smv)[e] = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (warp == Cf::MMAW) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      (unsigned)__cvta_generic_to_shared(&tmem_base)),
                  "r"(Cf::TCOLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (tid == 0) {
-    mbar_init(&mbar[0], 1);
-    mbar_init(&mbar[1], 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&bfull[i], Cf::NLOAD + 1);   // loader warps + the expect_tx arrive
+      mbar_init(&bempty[i], Cf::NPROD + 1);  // producer warps + the MMA commit
+    }
+    for (int i = 0; i < S; ++i) {
+      mbar_init(&sfull[i], Cf::NPROD);
+      mbar_init(&sempty[i], 1);
+    }
+    mbar_init(&done, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // zero fill before the bulk copies
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = tmem_base;
-  const uint32_t sbase = (unsigned)__cvta_generic_to_shared(smv);
-  // operand descriptors of stage 0 (A hi plane, B hi plane); per-MMA offsets are
-  // added to the 14-bit start-address field (16-byte units, no carry out: < 256 KB)
-  const uint64_t dB = umma_desc(sbase, 128, Cf::SBO);
-  // this thread's A row: tile (warp / 4 when two tiles), lane quadrant (warp % 4), frame group
-  const int tile = NTILE == 2 ? warp >> 2 : 0, wg = NTILE == 2 ? 0 : warp >> 2;
-  const int arow = tile * 128 + (warp & 3) * 32 + lane;  // A row j (rows >= J are padding)
-  int ai = 0, ak = 0;
-  {
-    const int j = arow < J ? arow : 0;
-    int p = j, q = j - P;
-    if (j >= P) {  // Im of the q-th off-diagonal pair
-      int i = 0, rem = q;
+
+  if (warp < Cf::NPROD) {
+    // ---------------- producers: A rows -> TMEM ----------------
+    const int q = warp & 3, h = warp >> 2;  // lane quadrant, 8-frame half of the chunk
+    const int L = q * 32 + lane;
+    int ai = 0, ak = 0;
+    const bool isdiag = L >= DL;
+    if (L < PO) {  // L-th off-diagonal pair (i < k), i-major
+      int i = 0, rem = L;
       while (rem >= M - 1 - i) {
         rem -= M - 1 - i;
         ++i;
       }
       ai = i;
       ak = i + 1 + rem;
-    } else {
-      int i = 0, rem = p;
-      while (rem >= M - i) {
-        rem -= M - i;
-        ++i;
-      }
-      ai = i;
-      ak = i + rem;
+    } else if (isdiag) {  // |x_d|^2 for d = L - DL (tile 0) and d + 8 (tile 1)
+      ai = L - DL < M ? L - DL : 0;
+      ak = L - DL + 8 < M ? L - DL + 8 : 0;
     }
-  }
-  constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(NB >> 3) << 17) |
-                             ((uint32_t)(128 >> 4) << 24);
-
-  const float fl = a.floorp[b];
-  const float* lamb = a.lam + (size_t)b * N * FT + (size_t)f * T;
-  const C* Xb = a.X + ((size_t)b * F + f) * T * M;
-  float lp[NMAX];
-  C xp[M];
-  auto fetch = [&](int c0) {
-    const int t = c0 + tid;
-    const int tc = t < tb ? t : tb - 1;
+    const uint32_t lanes = (uint32_t)(q * 32) << 16;
+    int c = 0;
+    for (int blk = 0; blk < nblk; ++blk) {
+      const int bb = blk & 1;
+      mbar_wait(&bfull[bb], (unsigned)((blk >> 1) & 1));
+      const C* Xs = reinterpret_cast<const C*>(smv + bb * Cf::XB);
+      const int nfr = min(TBLK, tb - ta - blk * TBLK);
+      const int nchb = (nfr + KC - 1) / KC;
+      for (int cb = 0; cb < nchb; ++cb, ++c) {
+        const int s = c % S;
+        const C* xr = Xs + (cb * KC + h * 8) * M;
+        float h0[8], l0[8], h1[8], l1[8];
+        if (!(a.dbg & 2)) {
 #pragma unroll
-    for (int n = 0; n < NMAX; ++n) {
-      lp[n] = 0.f;
-      if (n >= N) break;
-      lp[n] = lamb[(size_t)n * FT + tc];
-    }
-    CRowIO<float, M>::load(Xb + (size_t)tc * M, xp);
-  };
-  // x and 1/y are staged TBLK frames at a time by all threads (one frame each,
-  // the next block prefetched into registers); each block feeds TBLK/KC
-  // tensor-core chunks through the two operand stages
-  C* Xs = reinterpret_cast<C*>(smv + Cf::XS);
-  float* Ys = reinterpret_cast<float*>(smv + Cf::IYS);
-  constexpr int TBLK = Cf::TBLK;
-  if (tid < TBLK) fetch(ta);
-  int c = 0;  // chunk counter (stage = c & 1)
-  for (int b0 = ta; b0 < tb; b0 += TBLK) {
-    __syncthreads();  // previous block's x / 1/y consumed
-    if (tid < TBLK) {
-      const bool tv = b0 + tid < tb;
-      float l[NMAX];
-      C xv[M];
-#pragma unroll
-      for (int n = 0; n < NMAX; ++n) l[n] = lp[n];
-#pragma unroll
-      for (int m = 0; m < M; ++m) xv[m] = tv ? xp[m] : make_float2(0.f, 0.f);
-      if (b0 + TBLK < tb) fetch(b0 + TBLK);
-      float iy[M], y[M];
-      model_power<float, M>(l, gs, N, fl, iy, y);
-#pragma unroll
-      for (int m = 0; m < M; ++m)
-        if (!tv) iy[m] = 0.f;
-#pragma unroll
-      for (int m = 0; m < M; ++m) {  // [m][t]: 4 consecutive frames of one channel are 16/32 B
-        Xs[m * Cf::XLD + tid] = xv[m];
-        Ys[m * TBLK + tid] = iy[m];
-      }
-    }
-    __syncthreads();
-    const int nchb = min(TBLK, tb - b0 + KC - 1) / KC;
-    for (int cb = 0; cb < nchb; ++cb, ++c) {
-      const int s = c & 1;
-      unsigned char* Bhi = smv + s * Cf::STAGE;
-      unsigned char* Blo = Bhi + Cf::BBYTES;
-      if (c >= 2) mbar_wait(&mbar[s], (unsigned)(((c >> 1) - 1) & 1));  // MMAs of chunk c-2 done
-      const int k0 = cb * KC;  // chunk's first frame inside the block
-      // B rows: 1/y of the chunk's frames, 4 frames per item (smem, UMMA K-major)
-      for (int e = a.dbg == 2 ? BS : tid; e < M * (KC / 4); e += BS) {
-        const int m = e / (KC / 4), kq = e % (KC / 4);
-        const float4 v = *reinterpret_cast<const float4*>(Ys + m * TBLK + k0 + kq * 4);
-        float4 h;
-        h.x = tf32_rna(v.x); h.y = tf32_rna(v.y); h.z = tf32_rna(v.z); h.w = tf32_rna(v.w);
-        const uint32_t o = vtc_off<M>(m, kq * 4);
-        *reinterpret_cast<float4*>(Bhi + o) = h;
-        *reinterpret_cast<float4*>(Blo + o) = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
-      }
-      // A rows -> TMEM: this thread's row (lane) for its KW frames, hi and lo planes
-      if (a.dbg != 2) {
-        const bool im = arow >= P;
-        const C* xi = Xs + ai * Cf::XLD + k0 + wg * KW;
-        const C* xk = Xs + ak * Cf::XLD + k0 + wg * KW;
-        float hv[KW], lv[KW];
-#pragma unroll
-        for (int u = 0; u < KW; u += 2) {
-          const float4 pi = *reinterpret_cast<const float4*>(xi + u);
-          const float4 pk = *reinterpret_cast<const float4*>(xk + u);
-          const float v0 = im ? (pi.y * pk.x - pi.x * pk.y) : (pi.x * pk.x + pi.y * pk.y);
-          const float v1 = im ? (pi.w * pk.z - pi.z * pk.w) : (pi.z * pk.z + pi.w * pk.w);
-          hv[u] = tf32_rna(v0);
-          hv[u + 1] = tf32_rna(v1);
-          lv[u] = v0 - hv[u];
-          lv[u + 1] = v1 - hv[u + 1];
+          for (int u = 0; u < 8; ++u) {
+            const C xi = xr[u * M + ai], xk = xr[u * M + ak];
+            const float v0 = isdiag ? (xi.x * xi.x + xi.y * xi.y) : (xi.x * xk.x + xi.y * xk.y);
+            const float v1 = isdiag ? (xk.x * xk.x + xk.y * xk.y) : (xi.y * xk.x - xi.x * xk.y);
+            h0[u] = tf32_rna(v0);
+            l0[u] = v0 - h0[u];
+            h1[u] = tf32_rna(v1);
+            l1[u] = v1 - h1[u];
+          }
         }
-        const uint32_t lanes = (uint32_t)((warp & 3) * 32) << 16;
-        tmem_st_row<KW>(tmem + lanes + vtc_acol(s, tile, 0, NTILE, KC) + wg * KW, hv);
-        tmem_st_row<KW>(tmem + lanes + vtc_acol(s, tile, 1, NTILE, KC) + wg * KW, lv);
-        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        // the products are ready before the stage is: the MMAs of chunk c-S overlap them
+        if (c >= S) mbar_wait(&sempty[s], (unsigned)(((c / S) - 1) & 1));
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        if (!(a.dbg & 2)) {
+          tmem_st_row<8>(tmem + lanes + vtc_acol(s, 0, 0) + h * 8, h0);
+          tmem_st_row<8>(tmem + lanes + vtc_acol(s, 0, 1) + h * 8, l0);
+          tmem_st_row<8>(tmem + lanes + vtc_acol(s, 1, 0) + h * 8, h1);
+          tmem_st_row<8>(tmem + lanes + vtc_acol(s, 1, 1) + h * 8, l1);
+          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sfull[s]);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bempty[bb]);  // this warp has read the block's x
+    }
+  } else if (warp == Cf::MMAW) {
+    // ---------------- MMA issue: one lane ----------------
+    if (lane == 0) {
+      constexpr uint32_t IDESC32 = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(32 >> 3) << 17) |
+                                   ((uint32_t)(128 >> 4) << 24);
+      constexpr uint32_t IDESC16 = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(16 >> 3) << 17) |
+                                   ((uint32_t)(128 >> 4) << 24);
+      const uint32_t sbase = (unsigned)__cvta_generic_to_shared(smv);
+      int c = 0;
+      for (int blk = 0; blk < nblk; ++blk) {
+        const int bb = blk & 1;
+        mbar_wait(&bfull[bb], (unsigned)((blk >> 1) & 1));
+        const uint64_t dB = umma_desc(sbase + Cf::OFF_W + bb * Cf::WB, 128, Cf::SBO);
+        const int nfr = min(TBLK, tb - ta - blk * TBLK);
+        const int nchb = (nfr + KC - 1) / KC;
+        for (int cb = 0; cb < nchb; ++cb, ++c) {
+          const int s = c % S;
+          mbar_wait(&sfull[s], (unsigned)((c / S) & 1));
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          if (!(a.dbg & 1)) {
+#pragma unroll
+            for (int ks = 0; ks < KC / 8; ++ks) {
+              const uint64_t db = dB + (uint64_t)(cb * (KC / 4) * 8 + ks * 16);  // 16-byte units
+#pragma unroll
+              for (int tt = 0; tt < 2; ++tt) {
+                const uint32_t acc = (c > 0 || ks > 0) ? 1u : 0u;
+                umma_tf32_ts(tmem + (uint32_t)(tt * Cf::DCOLS), tmem + (uint32_t)(vtc_acol(s, tt, 0) + ks * 8),
+                             db, IDESC32, acc);
+                umma_tf32_ts(tmem + (uint32_t)(tt * Cf::DCOLS + 32),
+                             tmem + (uint32_t)(vtc_acol(s, tt, 1) + ks * 8), db, IDESC16, acc);
+              }
+            }
+          }
+          umma_commit(&sempty[s]);
+        }
+        umma_commit(&bempty[bb]);  // the block's weight planes are free once these MMAs retire
+      }
+      umma_commit(&done);
+    }
+  } else {
+    // ---------------- loaders: x by bulk copy, weights 1/y as TF32 hi / lo planes ----------------
+    const int lw = warp - Cf::MMAW - 1;  // 0..3
+    const int ml = lane & 7, tql = lane >> 3;
+    const float fl = a.floorp[b];
+    const float* lamb = a.lam + (size_t)b * N * FT + (size_t)f * T;
+    const C* Xb = a.X + ((size_t)b * F + f) * T * M;
+    const bool vec = (T & 3) == 0;
+    // lambda of the next block: cp.async into this warp's private rows
+    // Lw[buf][n][quad] (a warp covers 8 frame quads of a block), so no register
+    // holds a prefetch and no other warp is involved
+    float4* Lw = reinterpret_cast<float4*>(smv + Cf::OFF_L) + lw * 2 * NMAX * 8;
+    auto fetch = [&](int blk) {
+      float4* dstb = Lw + (blk & 1) * NMAX * 8;
+      for (int e = lane; e < N * 8; e += 32) {
+        const int n = e >> 3, qi = e & 7;
+        const int t = ta + blk * TBLK + (((qi >> 2) * 4 + lw) * 4 + (qi & 3)) * 4;
+        const float* lp = lamb + (size_t)n * FT + t;
+        const unsigned dst = (unsigned)__cvta_generic_to_shared(dstb + e);
+        if (vec) {
+          const unsigned sz = t < tb ? 16u : 0u;
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst),
+                       "l"(t < tb ? lp : lamb), "r"(sz)
+                       : "memory");
+        } else {
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const unsigned sz = t + u < tb ? 4u : 0u;
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(dst + 4 * u),
+                         "l"(t + u < tb ? lp + u : lamb), "r"(sz)
+                         : "memory");
+          }
+        }
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    fetch(0);
+    for (int blk = 0; blk < nblk; ++blk) {
+      const int bb = blk & 1;
+      if (blk + 1 < nblk) {
+        fetch(blk + 1);
+        asm volatile("cp.async.wait_group 1;" ::: "memory");
+      } else {
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+      }
+      __syncwarp();
+      if (blk >= 2) mbar_wait(&bempty[bb], (unsigned)(((blk >> 1) - 1) & 1));
+      const int t0 = ta + blk * TBLK;
+      const int nfr = min(TBLK, tb - t0);
+      if (lw == 0 && lane == 0) {
+        const unsigned bytes = (unsigned)(nfr * M * 8);
+        mbar_arrive_expect_tx(&bfull[bb], bytes);
+        bulk_g2s(smv + bb * Cf::XB, Xb + (size_t)t0 * M, bytes, &bfull[bb]);
+      }
+      unsigned char* Wp = smv + Cf::OFF_W + bb * Cf::WB;
+      const float4* Lb = Lw + bb * NMAX * 8;
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int kq = (j * 4 + lw) * 4 + tql;  // frame quad inside the block
+        const int t = t0 + kq * 4;
+#pragma unroll
+        for (int mh = 0; mh < 2; ++mh) {
+          const int m = mh * 8 + ml;
+          float y0 = 0.f, y1 = 0.f, y2 = 0.f, y3 = 0.f;
+#pragma unroll
+          for (int n = 0; n < NMAX; ++n) {
+            if (n >= N) break;
+            const float gv = gs[n * 16 + m];
+            const float4 l4 = Lb[n * 8 + j * 4 + tql];
+            y0 += l4.x * gv;
+            y1 += l4.y * gv;
+            y2 += l4.z * gv;
+            y3 += l4.w * gv;
+          }
+          float4 v;
+          v.x = (m < M && t < tb) ? rcp_r(floor_max(y0, fl)) : 0.f;
+          v.y = (m < M && t + 1 < tb) ? rcp_r(floor_max(y1, fl)) : 0.f;
+          v.z = (m < M && t + 2 < tb) ? rcp_r(floor_max(y2, fl)) : 0.f;
+          v.w = (m < M && t + 3 < tb) ? rcp_r(floor_max(y3, fl)) : 0.f;
+          float4 hi;
+          hi.x = tf32_rna(v.x); hi.y = tf32_rna(v.y); hi.z = tf32_rna(v.z); hi.w = tf32_rna(v.w);
+          *reinterpret_cast<float4*>(Wp + vtc_off<M>(m, kq * 4)) = hi;
+          *reinterpret_cast<float4*>(Wp + vtc_off<M>(16 + m, kq * 4)) =
+              make_float4(v.x - hi.x, v.y - hi.y, v.z - hi.z, v.w - hi.w);
+        }
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-      __syncthreads();
-      if (tid == 0) {
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint64_t so = (uint64_t)((uint32_t)(s * Cf::STAGE) >> 4);  // stage offset (16-byte units)
-#pragma unroll
-        for (int ks = 0; ks < KC / 8; ++ks) {
-          const uint64_t dbh = dB + so + ks * 16, dbl = dB + so + (Cf::BBYTES >> 4) + ks * 16;
-#pragma unroll
-          for (int tt = 0; tt < NTILE; ++tt) {
-            const uint32_t tah = tmem + (uint32_t)(vtc_acol(s, tt, 0, NTILE, KC) + ks * 8);
-            const uint32_t tal = tmem + (uint32_t)(vtc_acol(s, tt, 1, NTILE, KC) + ks * 8);
-            const uint32_t td = tmem + (uint32_t)(tt * NB);
-            if (a.dbg == 1) continue;
-            umma_tf32_ts(td, tah, dbh, IDESC, (c > 0 || ks > 0) ? 1u : 0u);
-            umma_tf32_ts(td, tah, dbl, IDESC, 1u);
-            umma_tf32_ts(td, tal, dbh, IDESC, 1u);
-          }
-        }
-        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                         (unsigned)__cvta_generic_to_shared(&mbar[s]))
-                     : "memory");
-      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bfull[bb]);
     }
   }
-  const int nch = c;
-  // the last commit covers every MMA of this CTA
-  mbar_wait(&mbar[(nch - 1) & 1], (unsigned)(((nch - 1) >> 1) & 1));
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  C* pb = reinterpret_cast<C*>(a.part) + (((size_t)b * F + f) * nseg + seg) * M * P;
-  if (warp < 4) {
+
+  // ---------------- epilogue: D0 halves + D1 -> the segment's partial V ----------------
+  if (warp < Cf::NPROD) {
+    mbar_wait(&done, 0u);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const int q = warp & 3, tt = warp >> 2;  // warps 0-3 read tile 0 (Re), 4-7 tile 1 (Im)
+    const int L = q * 32 + lane;
+    const uint32_t base = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(tt * Cf::DCOLS);
+    float d0[16], d1[16];
+    tmem_ld16(base, d0);
+    tmem_ld16(base + 16, d1);
 #pragma unroll
-    for (int tt = 0; tt < NTILE; ++tt) {
-      float d[NB];
-      tmem_ld_row<NB>(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(tt * NB), d);
-      const int r = tt * 128 + warp * 32 + lane;
-      if (r < J) {
-        int p = r, part = 0;
-        if (r >= P) {  // Im row: find the off-diagonal pair
-          const int q = r - P;
-          int i = 0, rem = q;
-          while (rem >= M - 1 - i) {
-            rem -= M - 1 - i;
-            ++i;
-          }
-          p = q + i + 1;  // pairs before (i, i+1+rem): q off-diagonals + (i + 1) diagonals
-          part = 1;
-        }
-        float* dst = reinterpret_cast<float*>(pb + p) + part;
-        const bool diag = part == 0 && pairI[p] == pairK[p];
+    for (int m = 0; m < 16; ++m) d0[m] += d1[m];
+    tmem_ld16(base + 32, d1);
+    int p = -1, part = tt;
+    if (L < PO) {
+      int i = 0, rem = L;
+      while (rem >= M - 1 - i) {
+        rem -= M - 1 - i;
+        ++i;
+      }
+      p = i * M - i * (i - 1) / 2 + 1 + rem;  // pairs before row i, then (k - i)
+    } else if (L >= DL) {
+      const int dd = L - DL + 8 * tt;
+      if (dd < M) p = dd * M - dd * (dd - 1) / 2;
+      part = 0;
+    }
+    if (p >= 0) {
+      float* dst = reinterpret_cast<float*>(reinterpret_cast<C*>(a.part) +
+                                            (((size_t)b * F + f) * nseg + seg) * M * P + p) + part;
+      const bool diag = L >= DL;
 #pragma unroll
-        for (int m = 0; m < M; ++m) {
-          if (a.dbg) d[m] = diag ? 1.f : 0.f;  // timing experiments: a valid V
-          dst[(size_t)m * P * 2] = d[m];
-          if (diag) dst[(size_t)m * P * 2 + 1] = 0.f;
-        }
+      for (int m = 0; m < M; ++m) {
+        float v = d0[m] + d1[m];
+        if (a.dbg) v = diag ? 1.f : 0.f;  // timing experiments: a valid V
+        dst[(size_t)m * P * 2] = v;
+        if (diag) dst[(size_t)m * P * 2 + 1] = 0.f;
       }
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
-  if (warp == 0)
+  if (warp == Cf::MMAW)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(Cf::TCOLS));
 }
 

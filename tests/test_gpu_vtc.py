@@ -17,7 +17,7 @@ pytestmark = pytest.mark.gpu
 
 
 @pytest.mark.parametrize("mode", ["tc", "blk", "simt"])
-@pytest.mark.parametrize("M,T", [(12, 301), (16, 200), (16, 517)])
+@pytest.mark.parametrize("M,T", [(12, 301), (16, 200), (16, 517), (10, 130), (14, 256), (16, 2088)])
 def test_vacc_tensor_core_vs_oracle(M, T, mode, monkeypatch):
     monkeypatch.setenv("FM_VACC", mode)
     from paper_1903_03237_b200 import SeparatorConfig, run
