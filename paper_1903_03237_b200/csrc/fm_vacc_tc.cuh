@@ -21,11 +21,11 @@
 //                     frames from shared x rows, splits them hi / lo and
 //                     stores them to TMEM (tcgen05.st) as the A operand
 //   MMA warp (1 lane)  per chunk and tile, per 8-frame k-step:
-//                     D0 += A_hi [B_hi | B_lo]  (one N = 32 MMA) and
-//                     D1 += A_lo B_hi           (N = 16); tcgen05.commit hands
+//                     D[:, 0:32] += A_hi [B_hi | B_lo]  (one N = 32 MMA) and
+//                     D[:, 0:16] += A_lo B_hi           (N = 16); tcgen05.commit hands
 //                     the operand stage (and, per block, the block buffers) back
 // Precision: 3xTF32 (A_hi B_hi + A_hi B_lo + A_lo B_hi, fp32 accumulation in
-// TMEM; D0's halves and D1 are summed in the epilogue) -- fp32-class products,
+// TMEM; the accumulator's two halves are summed in the epilogue) -- fp32-class products,
 // the same arithmetic class as the SIMT k_vacc. The gain MU that k_vacc
 // finishes is done identically. grid (nseg, F, B), block 416; fp32 only.
 #pragma once
@@ -50,14 +50,15 @@ template <int M> struct VtcCfg {
   static constexpr int OFF_W = 2 * XB;
   static constexpr int OFF_L = OFF_W + 2 * WB;     // loader warps' lambda rows (cp.async)
   static constexpr int SMEM = OFF_L + NLOAD * 2 * NMAX * 8 * 16;
-  static constexpr int S = 2;                      // operand stages in TMEM
-  // TMEM columns: per tile D0 (32) and D1 (16); then per stage, tile and plane KC columns
-  static constexpr int DCOLS = 48, ACOL = 2 * DCOLS;
+  static constexpr int S = 2;                      // operand stages in TMEM (one per producer group)
+  // TMEM columns: per tile 32 accumulator columns (A_hi B_hi + A_lo B_hi | A_hi B_lo);
+  // then per stage, tile and plane KC columns
+  static constexpr int DCOLS = 32, ACOL = 2 * DCOLS;
   static constexpr int TCOLS = 256;
   static_assert(ACOL + S * 2 * 2 * KC <= TCOLS, "tensor memory columns");
 };
 __host__ __device__ constexpr int vtc_acol(int stage, int tile, int plane) {
-  return 96 + ((stage * 2 + tile) * 2 + plane) * 16;
+  return 64 + ((stage * 2 + tile) * 2 + plane) * 16;
 }
 
 // byte offset of element (row, k) in the block's K-major no-swizzle weight plane
@@ -251,7 +252,7 @@ __global__ void __launch_bounds__(VtcCfg<M>::BS, 2) k_vacc_tc(VaccArgs<float> a)
       mbar_init(&bempty[i], Cf::NPROD + 1);  // producer warps + the MMA commit
     }
     for (int i = 0; i < S; ++i) {
-      mbar_init(&sfull[i], Cf::NPROD);
+      mbar_init(&sfull[i], Cf::NPROD / 2);
       mbar_init(&sempty[i], 1);
     }
     mbar_init(&done, 1);
@@ -265,7 +266,9 @@ __global__ void __launch_bounds__(VtcCfg<M>::BS, 2) k_vacc_tc(VaccArgs<float> a)
 
   if (warp < Cf::NPROD) {
     // ---------------- producers: A rows -> TMEM ----------------
-    const int q = warp & 3, h = warp >> 2;  // lane quadrant, 8-frame half of the chunk
+    // warps 0-3 build the even chunks in stage 0, warps 4-7 the odd chunks in stage 1:
+    // one handshake per 16 frames x 2 rows per thread
+    const int q = warp & 3, par = warp >> 2;  // lane quadrant, chunk parity (= stage)
     const int L = q * 32 + lane;
     int ai = 0, ak = 0;
     const bool isdiag = L >= DL;
@@ -281,7 +284,7 @@ __global__ void __launch_bounds__(VtcCfg<M>::BS, 2) k_vacc_tc(VaccArgs<float> a)
       ai = L - DL < M ? L - DL : 0;
       ak = L - DL + 8 < M ? L - DL + 8 : 0;
     }
-    const uint32_t lanes = (uint32_t)(q * 32) << 16;
+    const uint32_t tst = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)vtc_acol(par, 0, 0);
     int c = 0;
     for (int blk = 0; blk < nblk; ++blk) {
       const int bb = blk & 1;
@@ -290,34 +293,52 @@ __global__ void __launch_bounds__(VtcCfg<M>::BS, 2) k_vacc_tc(VaccArgs<float> a)
       const int nfr = min(TBLK, tb - ta - blk * TBLK);
       const int nchb = (nfr + KC - 1) / KC;
       for (int cb = 0; cb < nchb; ++cb, ++c) {
-        const int s = c % S;
-        const C* xr = Xs + (cb * KC + h * 8) * M;
-        float h0[8], l0[8], h1[8], l1[8];
-        if (!(a.dbg & 2)) {
+        if ((c & 1) != par) continue;
 #pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            const C xi = xr[u * M + ai], xk = xr[u * M + ak];
-            const float v0 = isdiag ? (xi.x * xi.x + xi.y * xi.y) : (xi.x * xk.x + xi.y * xk.y);
-            const float v1 = isdiag ? (xk.x * xk.x + xk.y * xk.y) : (xi.y * xk.x - xi.x * xk.y);
-            h0[u] = tf32_rna(v0);
-            l0[u] = v0 - h0[u];
-            h1[u] = tf32_rna(v1);
-            l1[u] = v1 - h1[u];
+        for (int hh = 0; hh < 2; ++hh) {
+          const C* xr = Xs + (cb * KC + hh * 8) * M;
+          float h0[8], l0[8], h1[8], l1[8];
+          if (!(a.dbg & 2)) {
+            if (q != 3) {  // warp-uniform: only the last lane quadrant holds diagonal lanes
+#pragma unroll
+              for (int u = 0; u < 8; ++u) {
+                const C xi = xr[u * M + ai], xk = xr[u * M + ak];
+                const float v0 = xi.x * xk.x + xi.y * xk.y;
+                const float v1 = xi.y * xk.x - xi.x * xk.y;
+                h0[u] = tf32_rna(v0);
+                l0[u] = v0 - h0[u];
+                h1[u] = tf32_rna(v1);
+                l1[u] = v1 - h1[u];
+              }
+            } else {
+#pragma unroll
+              for (int u = 0; u < 8; ++u) {
+                const C xi = xr[u * M + ai], xk = xr[u * M + ak];
+                const float v0 = isdiag ? (xi.x * xi.x + xi.y * xi.y) : (xi.x * xk.x + xi.y * xk.y);
+                const float v1 = isdiag ? (xk.x * xk.x + xk.y * xk.y) : (xi.y * xk.x - xi.x * xk.y);
+                h0[u] = tf32_rna(v0);
+                l0[u] = v0 - h0[u];
+                h1[u] = tf32_rna(v1);
+                l1[u] = v1 - h1[u];
+              }
+            }
+          }
+          if (hh == 0) {
+            // the first products are ready before the stage is: the MMAs of chunk c-2 overlap them
+            if (c >= 2) mbar_wait(&sempty[par], (unsigned)(((c >> 1) - 1) & 1));
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          }
+          if (!(a.dbg & 2)) {
+            tmem_st_row<8>(tst + 0 * KC + hh * 8, h0);
+            tmem_st_row<8>(tst + 1 * KC + hh * 8, l0);
+            tmem_st_row<8>(tst + 2 * KC + hh * 8, h1);
+            tmem_st_row<8>(tst + 3 * KC + hh * 8, l1);
           }
         }
-        // the products are ready before the stage is: the MMAs of chunk c-S overlap them
-        if (c >= S) mbar_wait(&sempty[s], (unsigned)(((c / S) - 1) & 1));
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        if (!(a.dbg & 2)) {
-          tmem_st_row<8>(tmem + lanes + vtc_acol(s, 0, 0) + h * 8, h0);
-          tmem_st_row<8>(tmem + lanes + vtc_acol(s, 0, 1) + h * 8, l0);
-          tmem_st_row<8>(tmem + lanes + vtc_acol(s, 1, 0) + h * 8, h1);
-          tmem_st_row<8>(tmem + lanes + vtc_acol(s, 1, 1) + h * 8, l1);
-          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-        }
+        if (!(a.dbg & 2)) asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
         __syncwarp();
-        if (lane == 0) mbar_arrive(&sfull[s]);
+        if (lane == 0) mbar_arrive(&sfull[par]);
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&bempty[bb]);  // this warp has read the block's x
@@ -338,8 +359,8 @@ __global__ void __launch_bounds__(VtcCfg<M>::BS, 2) k_vacc_tc(VaccArgs<float> a)
         const int nfr = min(TBLK, tb - ta - blk * TBLK);
         const int nchb = (nfr + KC - 1) / KC;
         for (int cb = 0; cb < nchb; ++cb, ++c) {
-          const int s = c % S;
-          mbar_wait(&sfull[s], (unsigned)((c / S) & 1));
+          const int s = c & 1;
+          mbar_wait(&sfull[s], (unsigned)((c >> 1) & 1));
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           if (!(a.dbg & 1)) {
 #pragma unroll
@@ -350,8 +371,8 @@ __global__ void __launch_bounds__(VtcCfg<M>::BS, 2) k_vacc_tc(VaccArgs<float> a)
                 const uint32_t acc = (c > 0 || ks > 0) ? 1u : 0u;
                 umma_tf32_ts(tmem + (uint32_t)(tt * Cf::DCOLS), tmem + (uint32_t)(vtc_acol(s, tt, 0) + ks * 8),
                              db, IDESC32, acc);
-                umma_tf32_ts(tmem + (uint32_t)(tt * Cf::DCOLS + 32),
-                             tmem + (uint32_t)(vtc_acol(s, tt, 1) + ks * 8), db, IDESC16, acc);
+                umma_tf32_ts(tmem + (uint32_t)(tt * Cf::DCOLS),
+                             tmem + (uint32_t)(vtc_acol(s, tt, 1) + ks * 8), db, IDESC16, 1u);
               }
             }
           }
@@ -453,7 +474,7 @@ __global__ void __launch_bounds__(VtcCfg<M>::BS, 2) k_vacc_tc(VaccArgs<float> a)
     }
   }
 
-  // ---------------- epilogue: D0 halves + D1 -> the segment's partial V ----------------
+  // ---------------- epilogue: accumulator halves -> the segment's partial V ----------------
   if (warp < Cf::NPROD) {
     mbar_wait(&done, 0u);
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -463,9 +484,6 @@ __global__ void __launch_bounds__(VtcCfg<M>::BS, 2) k_vacc_tc(VaccArgs<float> a)
     float d0[16], d1[16];
     tmem_ld16(base, d0);
     tmem_ld16(base + 16, d1);
-#pragma unroll
-    for (int m = 0; m < 16; ++m) d0[m] += d1[m];
-    tmem_ld16(base + 32, d1);
     int p = -1, part = tt;
     if (L < PO) {
       int i = 0, rem = L;
