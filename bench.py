@@ -278,6 +278,7 @@ def main():
     ap.add_argument("--shard", action="store_true",
                     help="c3: frequency-sharded path even at one rank (NCCL group of 1)")
     ap.add_argument("--iters", type=int, default=None, help="override iterations per step")
+    ap.add_argument("--mixtures", type=int, default=None, help="c2: override the batch size (A/B runs)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
@@ -287,6 +288,8 @@ def main():
     cfg = dict(CONFIGS[args.config])
     if args.iters:
         cfg["iters"] = args.iters
+    if args.mixtures and args.config == "c2":
+        cfg["B"] = args.mixtures
     world, rank, local = dist_env()
     if world > 1 and not args.config_given:
         # N > 1 measures the config that shards with an exchange: the long
@@ -431,8 +434,9 @@ def main():
     ftm = F * T * M * Bl if not sharded_f else (loop.F * T * M)
     nprof = 10
     if loop.dp is None:
-        fused = os.environ.get("FM_SCHEDULE") == "fused"
-        names = (["k_hpass", "k_gpass", "k_vacc", "k_ip", "k_bpass", "k_trace"] if fused else
+        sched = int(lib.fm_schedule(ctypes.byref(loop.dims)))  # 0 split, 1 fused, 2 per-bin
+        names = (["k_hpass", "k_gpass", "k_vacc", "k_ip", "k_bpass", "k_trace"] if sched == 1 else
+                 ["k_hstats", "k_binw", "k_trace"] if sched == 2 else
                  ["k_wstats", "k_lambda", "k_phi", "k_hstats", "k_lambda", "k_gain", "k_vacc",
                   "k_ip", "k_back", "k_trace"])
         samples = []
@@ -478,6 +482,7 @@ def main():
         "k_vacc": ftm * 2 * rs,               # read X (V accumulation)
         "k_bpass": ftm * 3 * rs,              # read X, write x~ (projection + next W step)
         "k_back": ftm * 3 * rs,               # deep prior: read X, write x~
+        "k_binw": ftm * 7 * rs,               # read x~ (gains), X twice (V, projection), write x~
         "k_phi": ftm * rs, "k_gain": ftm * rs,
         "k_dp_latent": ftm * rs + FT * rs,    # x~ and y_rest (F,T) per Adam step
         "k_dp_mh": ftm * rs + FT * rs,
@@ -572,7 +577,9 @@ def main():
     # per iteration, split schedule: k_wstats, k_lambda, k_phi, k_hstats, k_lambda,
     # k_gain, k_vacc, k_ip, k_back, k_trace; fused: k_hpass, k_gpass, k_vacc,
     # k_ip, k_bpass, k_trace (+ the counter advance when B > 1); prologue 2
-    per_it = 6 if os.environ.get("FM_SCHEDULE") == "fused" else 10
+    sched_names = {0: "split", 1: "fused", 2: "bin"}
+    sched = 0 if loop.dp is not None else int(lib.fm_schedule(ctypes.byref(loop.dims)))
+    per_it = {0: 10, 1: 6, 2: 3}[sched]
     launches = args.steps * (2 + (per_it if cfg['B'] == 1 else per_it + 1) * iters)
     if sharded_f:  # + the H update after the all-reduce
         launches = args.steps * (2 + (per_it + 1) * iters)
@@ -592,7 +599,8 @@ def main():
                        "parallelism": ("frequency-sharded" if sharded_f else
                                        "batch-sharded" if args.config == "c2" else "replicas")
                                       + f" x{world}",
-                       "l2": "flushed between steps (256 MiB write)"},
+                       "l2": "flushed between steps (256 MiB write)",
+                       "schedule": sched_names[sched]},
             "iters_per_s": iters_per_s, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches, "clocks": clk,
         }

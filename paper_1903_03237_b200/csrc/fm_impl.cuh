@@ -18,6 +18,7 @@
 #include "fm_dp_latent.cuh"
 #include "fm_dp_mh.cuh"
 #include "fm_vacc_tc.cuh"
+#include "fm_back_tc.cuh"
 #include "fm_vacc_blk.cuh"
 #include "fm_init.cuh"
 #include "fm_stft.cuh"
@@ -148,19 +149,28 @@ struct Plan {
   size_t off_cnt, off_hcnt, off_vcnt, off_bcnt, off_hcnt2, total;
 };
 
-// complex64 V accumulation: 0 register-blocked SIMT (k_vacc_blk, M >= 8),
-// 1 pair-per-thread SIMT (k_vacc), 2 tensor cores (k_vacc_tc, M >= 12).
+// complex64 V accumulation: 0 register-blocked SIMT (k_vacc_blk), 1
+// pair-per-thread SIMT (k_vacc), 2 tensor cores (k_vacc_tc, even M in 10..16).
 // FM_VACC=blk|simt|tc forces one for A/B runs; read at every launch (or graph
 // capture) so tests can switch it within one process.
 inline int vacc_mode(const fm_dims* d) {
+  const bool tc_ok = d->M >= 10 && d->M % 2 == 0;
   const char* e = getenv("FM_VACC");
   if (e && strcmp(e, "simt") == 0) return 1;
-  if (e && strcmp(e, "tc") == 0) return (d->M >= 10 && d->M % 2 == 0) ? 2 : 1;
+  if (e && strcmp(e, "tc") == 0) return tc_ok ? 2 : 1;
   if (e && strcmp(e, "blk") == 0) return 0;
   // measured on B200: pair-per-thread wins at M = 4 (c2: 1.13 vs 1.89 ms) and
-  // M = 8 (c1: 39.1 vs 40.8 us); the blocked kernel at M = 16 (c3: 2.00 ms vs
-  // 2.57 ms tensor cores, 4.67 ms pair-per-thread)
-  return d->M > 8 ? 0 : 1;
+  // M = 8 (c1: 39.1 vs 40.8 us); at M = 16 (c3) the tensor cores (1.06 ms)
+  // beat the blocked kernel (2.00 ms) and pair-per-thread (4.67 ms)
+  if (d->M > 8) return tc_ok ? 2 : 0;
+  return 1;
+}
+
+// complex64, M > 8: the projection on the tensor cores (k_back_tc);
+// FM_BACK=simt forces the SIMT k_back (A/B runs, tests)
+inline bool back_tc_mode() {
+  const char* e = getenv("FM_BACK");
+  return !(e && strcmp(e, "simt") == 0);
 }
 
 // FM_GSEG: segment-count tuning knob (A/B runs); read at every plan
@@ -174,7 +184,9 @@ inline int gseg_override() {
 //   fused  five statistics passes with on-chip lambda (FM_SCHEDULE=fused, §4a)
 //   bin    k_hstats + the per-bin kernel k_binw + k_trace (fm_bin.cuh, §4c):
 //          complex64, M <= 4, N in 2..4, K <= 8, H of a mixture in shared memory
-// FM_SCHEDULE=split|fused|bin forces one (bin only where it is eligible).
+// FM_SCHEDULE=split|fused|bin forces one (bin only where it is eligible); the
+// default is bin for eligible shapes with >= FM_BIN_MIN_BINS (bin, mixture) pairs.
+constexpr long long FM_BIN_MIN_BINS = 4096;  // measured: 8 mixtures x 513 bins already win (5177 vs 4309 it/s)
 inline bool bin_eligible(const fm_dims* d) {
   if (d->dtype != FM_F32 || d->dp || d->M > 4 || d->N < 2 || d->N > 4 || d->K > 8) return false;
   const long long hs = d->N * 8LL * d->T * 4LL;  // staged H (KK = 8 rows per source)
@@ -185,6 +197,10 @@ inline int schedule_of(const fm_dims* d) {
   if (e && strcmp(e, "fused") == 0) return FM_SCHED_FUSED;
   if (e && strcmp(e, "split") == 0) return FM_SCHED_SPLIT;
   if (e && strcmp(e, "bin") == 0) return bin_eligible(d) ? FM_SCHED_BIN : FM_SCHED_SPLIT;
+  // default: one warp per bin once the batch gives every SM a few CTAs of bins
+  // (config 2 shape: 8 mixtures 5177 vs 4309 iterations/s, 64: 809 vs 637,
+  // 256: 228 vs 163); the split schedule's (bin, frame-tile) CTAs otherwise
+  if (bin_eligible(d) && d->B * d->F >= FM_BIN_MIN_BINS) return FM_SCHED_BIN;
   return FM_SCHED_SPLIT;
 }
 inline bool use_fused(const fm_dims* d) { return schedule_of(d) == FM_SCHED_FUSED; }
@@ -222,10 +238,10 @@ inline int pass_stages_override() {
 // launches: part of the CUDA-graph cache key (fm_api.cu run_common).
 inline unsigned variant_key(const fm_dims* d) {
   return (unsigned)vacc_mode(d) | ((unsigned)(gseg_override() & 0xff) << 4) |
-         ((unsigned)(pass_ctas_override() & 0xffff) << 12) | ((unsigned)pass_stages_override() << 28) |
+         ((unsigned)(pass_ctas_override() & 0x3fff) << 12) | ((unsigned)pass_stages_override() << 26) |
          ((unsigned)use_fused(d) << 31) | ((unsigned)ip_warp_mode(d) << 3) |
          ((unsigned)use_bin(d) << 30) |
-         ((unsigned)small_m_mode() << 2);
+         ((unsigned)small_m_mode() << 2) | ((unsigned)back_tc_mode() << 29);
 }
 
 inline Plan make_plan(const fm_dims* d) {
@@ -657,7 +673,18 @@ int Impl<R>::back(const fm_dims* d, const fm_state* s, int tail_only, int record
       if (ppt == 2) launch_pdl(k_back<R, MM, 2>, grid, dim3(256), 0, st, a);
       else launch_pdl(k_back<R, MM, 1>, grid, dim3(256), 0, st, a);
     } else {
-      launch_pdl(k_back<R, MM, 1>, grid, dim3(256), 0, st, a);
+      bool done = false;
+      if constexpr (sizeof(R) == 4 && MM > 8) {
+        if (back_tc_mode()) {  // tensor-core projection; segments of whole 256-frame tiles
+          const long long ctas = 6LL * 4 * 148, fb = (long long)d->F * d->B;
+          long long ns = std::max<long long>(1, std::min<long long>(p.ntile, (ctas + fb - 1) / fb));
+          const int TRb = (int)((p.ntile + ns - 1) / ns) * 256;
+          const dim3 gridt((unsigned)((d->T + TRb - 1) / TRb), (unsigned)d->F, (unsigned)d->B);
+          launch_pdl(k_back_tc<MM>, gridt, dim3(128), 0, st, a, TRb, p.ntile);
+          done = true;
+        }
+      }
+      if (!done) launch_pdl(k_back<R, MM, 1>, grid, dim3(256), 0, st, a);
     }
     FM_CHECK_LAUNCH("k_back");
   });

@@ -23,13 +23,13 @@ def binsched(monkeypatch):
     monkeypatch.setenv("FM_SCHEDULE", "bin")
 
 
-def _schedule(F, T, M, N, K, prec="complex64"):
+def _schedule(F, T, M, N, K, prec="complex64", B=1):
     import ctypes
 
     from paper_1903_03237_b200 import _lib
     d = _lib.FmDims()
     d.dtype = 0 if prec == "complex64" else 1
-    d.B, d.F, d.T, d.M, d.N, d.K = 1, F, T, M, N, K
+    d.B, d.F, d.T, d.M, d.N, d.K = B, F, T, M, N, K
     d.normalize, d.ip_sweeps = 1, 1
     return _lib.SCHEDULES[_lib.load().fm_schedule(ctypes.byref(d))]
 
@@ -41,6 +41,17 @@ def test_schedule_selection():
     assert _schedule(513, 1024, 8, 4, 16) == "split"              # M > 4
     assert _schedule(64, 64, 4, 2, 12) == "split"                 # K > 8
     assert _schedule(64, 64, 4, 1, 4) == "split"                  # N < 2
+
+
+def test_default_schedule(monkeypatch):
+    """Without FM_SCHEDULE: per-bin once the batch holds >= 4096 (bin,
+    mixture) pairs (config 2), split below and wherever bin is ineligible."""
+    monkeypatch.delenv("FM_SCHEDULE")
+    assert _schedule(513, 512, 4, 3, 8, B=256) == "bin"
+    assert _schedule(513, 512, 4, 3, 8, B=8) == "bin"
+    assert _schedule(513, 512, 4, 3, 8, B=4) == "split"
+    assert _schedule(513, 512, 4, 3, 8) == "split"
+    assert _schedule(513, 1024, 8, 4, 16, B=64) == "split"
 
 
 def test_bin_config0_c64():
