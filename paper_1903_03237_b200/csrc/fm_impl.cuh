@@ -173,6 +173,11 @@ inline bool back_tc_mode() {
   return !(e && strcmp(e, "simt") == 0);
 }
 
+inline bool back_tc_forced() {  // FM_BACK=tc: also for M in 5..8 (A/B runs)
+  const char* e = getenv("FM_BACK");
+  return e && strcmp(e, "tc") == 0;
+}
+
 // FM_GSEG: segment-count tuning knob (A/B runs); read at every plan
 inline int gseg_override() {
   const char* e = getenv("FM_GSEG");
@@ -238,10 +243,11 @@ inline int pass_stages_override() {
 // launches: part of the CUDA-graph cache key (fm_api.cu run_common).
 inline unsigned variant_key(const fm_dims* d) {
   return (unsigned)vacc_mode(d) | ((unsigned)(gseg_override() & 0xff) << 4) |
-         ((unsigned)(pass_ctas_override() & 0x3fff) << 12) | ((unsigned)pass_stages_override() << 26) |
+         ((unsigned)(pass_ctas_override() & 0x1fff) << 12) | ((unsigned)pass_stages_override() << 26) |
          ((unsigned)use_fused(d) << 31) | ((unsigned)ip_warp_mode(d) << 3) |
          ((unsigned)use_bin(d) << 30) |
-         ((unsigned)small_m_mode() << 2) | ((unsigned)back_tc_mode() << 29);
+         ((unsigned)small_m_mode() << 2) | ((unsigned)back_tc_mode() << 29) |
+         ((unsigned)back_tc_forced() << 25);
 }
 
 inline Plan make_plan(const fm_dims* d) {
@@ -674,8 +680,8 @@ int Impl<R>::back(const fm_dims* d, const fm_state* s, int tail_only, int record
       else launch_pdl(k_back<R, MM, 1>, grid, dim3(256), 0, st, a);
     } else {
       bool done = false;
-      if constexpr (sizeof(R) == 4 && MM > 8) {
-        if (back_tc_mode()) {  // tensor-core projection; segments of whole 256-frame tiles
+      if constexpr (sizeof(R) == 4 && MM > 4) {
+        if (back_tc_mode() && (MM > 8 || back_tc_forced())) {  // tensor-core projection; segments of whole 256-frame tiles
           const long long ctas = 6LL * 4 * 148, fb = (long long)d->F * d->B;
           long long ns = std::max<long long>(1, std::min<long long>(p.ntile, (ctas + fb - 1) / fb));
           const int TRb = (int)((p.ntile + ns - 1) / ns) * 256;
