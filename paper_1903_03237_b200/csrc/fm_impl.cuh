@@ -564,6 +564,10 @@ int Impl<R>::vacc(const fm_dims* d, const fm_state* s, cudaStream_t st) {
     if constexpr (sizeof(R) == 4) {
       if constexpr (MM >= 10 && MM % 2 == 0) {
         if (mode == 2) {
+          if (reinterpret_cast<uintptr_t>(s->X) & 15) {  // the bulk copies of X blocks
+            set_error("k_vacc_tc: X must be 16-byte aligned");
+            return FM_EINVAL;
+          }
           const size_t smv = VtcCfg<MM>::SMEM;
           if (int rc = ensure_smem(k_vacc_tc<MM>, smv)) return rc;
           VaccArgs<float> at = *reinterpret_cast<VaccArgs<float>*>(&a);
