@@ -197,8 +197,15 @@ int fm_prologue(const fm_dims* d, const fm_state* s, void* stream);
  * assignable arrays, separate.py:178-184); the trace index continues. */
 int fm_refresh(const fm_dims* d, const fm_state* s, void* stream);
 
-/* Iteration schedules (fm_schedule). The environment variable
- * FM_SCHEDULE=split|fused|bin selects one (bin only where eligible). */
+/* Iteration schedules (fm_schedule). Default: the per-bin
+ * schedule where it is eligible and the batch holds >= 4096 (bin, mixture)
+ * pairs (BASELINE config 2), the split schedule otherwise. The environment
+ * variable FM_SCHEDULE=split|fused|bin forces one (bin only where eligible).
+ * Kernel variants inside a schedule are picked by shape: complex64
+ * with even M in 10..16 accumulates V_fm on the tensor cores (k_vacc_tc;
+ * FM_VACC=blk|simt|tc forces one) -- X must then be 16-byte aligned -- and
+ * complex64 with M > 8 projects on the tensor cores (k_back_tc; FM_BACK=simt
+ * forces the SIMT kernel). */
 #define FM_SCHED_SPLIT 0
 #define FM_SCHED_FUSED 1
 #define FM_SCHED_BIN 2
@@ -206,11 +213,12 @@ int fm_refresh(const fm_dims* d, const fm_state* s, void* stream);
 /* The schedule fm_iterate / fm_run use for these dims: FM_SCHED_*, or -1
  * for invalid dims. The per-bin schedule (FM_SCHED_BIN) is three launches
  * per iteration (k_hstats, k_binw, k_trace) for complex64 with M <= 4,
- * 2 <= N <= 4, K <= 8. */
+ * 2 <= N <= 4, K <= 8 and H of a mixture (N x 8 x T floats) within shared
+ * memory. */
 int fm_schedule(const fm_dims* d);
 
-/* One full iteration (separate.py:201-234) on one process. Split schedule
- * (default): ten launches (k_wstats, k_lambda, k_phi, k_hstats, k_lambda,
+/* One full iteration (separate.py:201-234) on one process. Split schedule:
+ * ten launches (k_wstats, k_lambda, k_phi, k_hstats, k_lambda,
  * k_gain, k_vacc, k_ip, k_back, k_trace). Fused schedule (FM_SCHEDULE=fused):
  * six (k_hpass, k_gpass, k_vacc, k_ip, k_bpass, k_trace), lambda formed on
  * chip and the W step of the NEXT iteration inside k_bpass (the state W after

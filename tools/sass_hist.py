@@ -3,7 +3,8 @@
 (cuobjdump -sass): usage sass_hist.py MANGLED_NAME_REGEX... Prints, per
 kernel, the instruction count and the opcodes that prove the pipe it uses
 (FFMA2 / DFMA on the FMA pipes; UTCHMMA/UTCQMMA/UTCMMA (tcgen05.mma), LDTM/STTM
-(tcgen05.ld/st), UTMALDG (TMA) on the tensor-core path)."""
+(tcgen05.ld/st), UTMALDG (TMA) / UBLKCP (cp.async.bulk), SYNCS (mbarrier) on the
+tensor-core path)."""
 import re
 import subprocess
 import sys
@@ -25,6 +26,6 @@ for blk in blocks[1:]:
             ops[m.group(2).split(".")[0]] += 1
     tot = sum(ops.values())
     key = [o for o in ("FFMA2", "FFMA", "DFMA", "FMUL", "LDS", "LDSM", "STS", "LDG", "STG", "LDGSTS",
-                       "UTCHMMA", "UTCQMMA", "UTCMMA", "UTCBAR", "LDTM", "STTM", "UTMALDG", "SHFL",
+                       "UTCHMMA", "UTCQMMA", "UTCMMA", "UTCBAR", "LDTM", "STTM", "UTMALDG", "UBLKCP", "SYNCS", "SHFL",
                        "MUFU", "BAR") if ops.get(o)]
     print(f"{dem}: {tot} instructions; " + ", ".join(f"{o} {ops[o]}" for o in key))
