@@ -305,6 +305,10 @@ def main():
 
     import ctypes
 
+    # NCCL logs (its "NCCL version ..." banner included) default to stdout, where
+    # the contract wants exactly one JSON line: send them to stderr
+    os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+
     import torch
     import torch.distributed as dist
 

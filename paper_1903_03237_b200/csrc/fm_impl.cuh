@@ -19,6 +19,7 @@
 #include "fm_dp_mh.cuh"
 #include "fm_vacc_tc.cuh"
 #include "fm_back_tc.cuh"
+#include "fm_lambda_tc.cuh"
 #include "fm_vacc_blk.cuh"
 #include "fm_init.cuh"
 #include "fm_stft.cuh"
@@ -173,6 +174,15 @@ inline bool back_tc_mode() {
   return !(e && strcmp(e, "simt") == 0);
 }
 
+// lambda = W H on the tensor cores (k_lambda_tc): complex64, K a multiple of 8 up
+// to 32, >= 2^24 lambda entries (config 3); FM_LAMBDA=simt|tc forces either
+inline bool lambda_tc_mode(const fm_dims* d, int n0) {
+  if (d->dtype != FM_F32 || d->K % 8 != 0 || d->K > 32) return false;
+  const char* e = getenv("FM_LAMBDA");
+  if (e && strcmp(e, "simt") == 0) return false;
+  if (e && strcmp(e, "tc") == 0) return true;
+  return d->B * (d->N - n0) * d->F * d->T >= (1LL << 24);
+}
 inline bool back_tc_forced() {  // FM_BACK=tc: also for M in 5..8 (A/B runs)
   const char* e = getenv("FM_BACK");
   return e && strcmp(e, "tc") == 0;
@@ -243,11 +253,11 @@ inline int pass_stages_override() {
 // launches: part of the CUDA-graph cache key (fm_api.cu run_common).
 inline unsigned variant_key(const fm_dims* d) {
   return (unsigned)vacc_mode(d) | ((unsigned)(gseg_override() & 0xff) << 4) |
-         ((unsigned)(pass_ctas_override() & 0x1fff) << 12) | ((unsigned)pass_stages_override() << 26) |
+         ((unsigned)(pass_ctas_override() & 0xfff) << 12) | ((unsigned)pass_stages_override() << 26) |
          ((unsigned)use_fused(d) << 31) | ((unsigned)ip_warp_mode(d) << 3) |
          ((unsigned)use_bin(d) << 30) |
          ((unsigned)small_m_mode() << 2) | ((unsigned)back_tc_mode() << 29) |
-         ((unsigned)back_tc_forced() << 25);
+         ((unsigned)back_tc_forced() << 25) | ((unsigned)lambda_tc_mode(d, d->dp ? 1 : 0) << 24);
 }
 
 inline Plan make_plan(const fm_dims* d) {
@@ -506,6 +516,18 @@ inline int ensure_smem(Kern k, size_t bytes) {
 template <typename R>
 int Impl<R>::lambda(const fm_dims* d, const R* W, const R* H, R* lam, cudaStream_t st) {
   const int n0 = d->dp ? 1 : 0;
+  if constexpr (sizeof(R) == 4) {
+    if (lambda_tc_mode(d, n0)) {  // tensor cores: large problems, K in {8, 16, 24, 32}
+      const long long tt = (d->T + 127) / 128, bn = d->B * (d->N - n0);
+      long long fg = std::max<long long>(1, (6LL * 4 * 148 + tt * bn - 1) / (tt * bn));
+      long long fpg = ((d->F + fg - 1) / fg + LTC_FT - 1) / LTC_FT * LTC_FT;
+      fg = (d->F + fpg - 1) / fpg;
+      launch_pdl(k_lambda_tc, dim3((unsigned)tt, (unsigned)fg, (unsigned)bn), dim3(128), 0, st, W, H,
+                 lam, (int)d->F, (int)d->T, (int)d->K, (int)d->N, n0, (int)fpg);
+      FM_CHECK_LAUNCH("k_lambda_tc");
+      return FM_OK;
+    }
+  }
   dim3 grid((unsigned)((d->T + 63) / 64), (unsigned)((d->F + 63) / 64),
             (unsigned)(d->B * (d->N - n0)));
   launch_pdl(k_lambda<R>, grid, dim3(256), 0, st, W, H, lam, (int)d->F, (int)d->T, (int)d->K,
