@@ -541,6 +541,24 @@ def main():
                                    "unit": "TFLOP/s", "frac": ach / fp32_peak,
                                    "alg_flops_per_launch": flops,
                                    "peak_kind": "nominal 148 SM x 128 FP32 lanes x 2 x max SM clock"}
+            tc_v = (cfg["precision"] == "complex64" and M >= 10 and M % 2 == 0
+                    and os.environ.get("FM_VACC") in (None, "tc"))
+            if tc_v:
+                # k_vacc_tc: the contraction D[j][m] = sum_t A[j][t] w[m][t] (M*M real rows,
+                # M weights) runs as 3xTF32 tcgen05 MMAs; the SIMT work left is the
+                # operand build. Against the TF32 tensor peak (half the measured bf16
+                # figure), counting the three TF32 products each fp32-class product costs.
+                pk = json.load(open(os.path.join(REPO, "MEASURED_PEAKS.json"))) \
+                    if os.path.exists(os.path.join(REPO, "MEASURED_PEAKS.json")) else {}
+                tf32_peak = float(pk.get("bf16_tflops", 1675.0)) / 2
+                gemm = 2 * M * M * M * FT
+                roofline["compute"] = {
+                    "bound": "tensor", "kind": "tf32 (3xTF32 split)",
+                    "achieved": 3 * gemm / (per_launch_ms / 1e3) / 1e12, "peak": tf32_peak,
+                    "unit": "TFLOP/s", "frac": 3 * gemm / (per_launch_ms / 1e3) / 1e12 / tf32_peak,
+                    "alg_flops_per_launch": gemm, "issued_flops_per_launch": 3 * gemm,
+                    "peak_kind": "measured bf16 cuBLAS peak / 2",
+                    "note": "shape-limited: N = M = 16 weight columns per MMA (M=128 x N=32|16 x K=8)"}
     # whole iteration against B_it = (4 b_r + 2 b_c) F T M per mixture
     b_it = 8 * rs * (F * T * M * (B_total if args.config == "c2" else Bl))
     it_s = ms_per_step / 1e3 / iters
