@@ -174,8 +174,19 @@ def logdet(Q_FMM):
     return io.out(out)
 
 
-def wiener_fast(lam_NFT, Q_FMM, g_NFM, X_FTM):
-    """separate.wiener_fast (separate.py:110-125): images (N,F,T,M)."""
+def check_wiener_status(st):
+    """Raise the reference's error for a singular diagonaliser (separate.py:116)."""
+    s = decode_status(st.item())
+    if s is not None:
+        raise SingularMatrixError(status_message(3, 0, s[3]))
+
+
+def wiener_fast(lam_NFT, Q_FMM, g_NFM, X_FTM, defer_status=False):
+    """separate.wiener_fast (separate.py:110-125): images (N,F,T,M).
+
+    ``defer_status=True`` (device inputs) skips the host read of the status
+    word and returns (images, status tensor) for ``check_wiener_status`` --
+    the caller overlaps its own work with the kernel."""
     io = _Io(lam_NFT, Q_FMM, g_NFM, X_FTM)
     torch = io.torch
     lam, Q, g, X = io.r(lam_NFT), io.c(Q_FMM), io.r(g_NFM), io.c(X_FTM)
@@ -186,7 +197,7 @@ def wiener_fast(lam_NFT, Q_FMM, g_NFM, X_FTM):
     _lib.check(_lib.load().fm_wiener_fast(io.dt, N, F, T, M, _lib.ptr(lam), _lib.ptr(Q),
                                           _lib.ptr(g), _lib.ptr(X), _lib.ptr(out), _lib.ptr(st),
                                           _lib.stream_ptr()), "fm_wiener_fast")
-    s = decode_status(st.item())
-    if s is not None:
-        raise SingularMatrixError(status_message(3, 0, s[3]))
+    if defer_status:
+        return io.out(out), st
+    check_wiener_status(st)
     return io.out(out)

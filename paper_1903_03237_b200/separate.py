@@ -452,17 +452,23 @@ class DeviceLoop:
         return SingularMatrixError(f"iteration {it}: {msg}" if prefix else msg)
 
     @_on_device
-    def images_batch(self, scale):
+    def images_batch(self, scale, defer_status=False):
         """separate.py:240-243 + the scale-back of :323, for every mixture:
-        one wiener_fast launch per mixture on the stream, no host sync."""
+        one wiener_fast launch per mixture on the stream. With
+        ``defer_status`` nothing reads back from the device: returns
+        (images, status tensors) and the caller runs
+        ``kernels.check_wiener_status`` on each once it has to wait anyway."""
         lam = self.lam_device()
-        out = []
+        out, sts = [], []
         for b in range(self.B):
-            img = K.wiener_fast(lam[b], self.Q[b], self.g[b], self.X_dev[b])
+            img = K.wiener_fast(lam[b], self.Q[b], self.g[b], self.X_dev[b], defer_status=defer_status)
+            if defer_status:
+                img, st = img
+                sts.append(st)
             if float(scale[b]) != 1.0:
                 img.mul_(float(scale[b]))
             out.append(img)
-        return out
+        return (out, sts) if defer_status else out
 
 
 # ---------------------------------------------------------------------------
@@ -554,7 +560,7 @@ def _prepare_observation(X, cfg, torch):
     return Xd, scale, floor.to(cfg.device)
 
 
-def _to_host(t):
+def _to_host(t, wait=True):
     """Device tensor -> host tensor in page-locked memory from torch's caching
     host allocator: one async DMA at full PCIe/C2C speed and no host-side copy
     (a plain .cpu() of a large tensor runs at pageable-DMA speed, and a copy
@@ -564,7 +570,8 @@ def _to_host(t):
     torch = _torch()
     out = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
     out.copy_(t.contiguous(), non_blocking=True)
-    torch.cuda.current_stream().synchronize()
+    if wait:
+        torch.cuda.current_stream().synchronize()
     return out
 
 
@@ -656,13 +663,20 @@ def _run(cfg, X_FTM, on_iteration, init, torch):
     err = loop.status_error()
     if err is not None:
         raise err
+    # images at the run's precision (complex64 runs return complex64), in pinned host
+    # memory: the Wiener kernels and the DMA are queued first, the host-side trace
+    # bookkeeping runs while they do, the one wait comes last
+    imgs, sts = loop.images_batch(scale, defer_status=True)
+    images_t = _to_host(imgs[0], wait=False)
     prev = start
     for e in ev:  # per-iteration device time (separate.py:307-312 analogue)
         time_trace.append(prev.elapsed_time(e) / 1e3)
         prev = e
     ll = loop.trace[:, 0].cpu().numpy().copy() if cfg.record_likelihood else np.zeros(0)
-    # images at the run's precision (complex64 runs return complex64), in pinned host memory
-    images = _to_host(loop.images_batch(scale)[0]).numpy()
+    torch.cuda.current_stream().synchronize()
+    for st in sts:
+        K.check_wiener_status(st)
+    images = images_t.numpy()
     res = SeparationResult(images_NFTM=images, likelihood_trace=np.asarray(ll),
                            time_trace=np.asarray(time_trace), method=cfg.method,
                            config=replace(cfg))
