@@ -1,9 +1,11 @@
-"""The complex64 V accumulations at M >= 12 -- tensor cores (k_vacc_tc,
-FM_VACC=tc) and the register-blocked SIMT default (k_vacc_blk) -- against the
-oracle: ragged frame blocks (T not a multiple of the 16-frame chunk or the
-128-frame staging block), a padded accumulator tile (M = 12: 144 real rows in
-two 128-lane tiles) and the full two-tile case (M = 16). complex64 tolerance
-1e-3 (BASELINE north_star), relative Frobenius per tensor and per-entry on the
+"""The complex64 kernels at M > 8 against the oracle. V accumulation: tensor
+cores (k_vacc_tc, the default for even M in 10..16, FM_VACC=tc), the
+register-blocked SIMT kernel (k_vacc_blk) and the pair-per-thread one --
+ragged frame blocks (T not a multiple of the 16-frame chunk or the 128-frame
+staging block, odd T: the scalar lambda path), padded lanes (M < 16), two
+segments (T = 2088). Projection (k_back_tc vs k_back) and lambda = W H
+(k_lambda_tc vs k_lambda) in every combination. complex64 tolerance 1e-3
+(BASELINE north_star), relative Frobenius per tensor and per-entry on the
 likelihood trace."""
 
 import numpy as np
@@ -58,3 +60,29 @@ def test_vacc_blocked_every_m(M, monkeypatch):
     assert np.max(np.abs(res.likelihood_trace - tr) / np.abs(tr)) <= 1e-3
     assert rel(res.images_NFTM, ref["images"]) <= 1e-3
     assert rel(res.loop.spatial.Q_FMM, ref["Q"]) <= 1e-3
+
+
+@pytest.mark.parametrize("back", ["tc", "simt"])
+@pytest.mark.parametrize("lam", ["tc", "simt"])
+@pytest.mark.parametrize("M,T,K", [(16, 300, 8), (12, 517, 16), (9, 130, 8), (13, 257, 32)])
+def test_projection_and_lambda_variants(M, T, K, back, lam, monkeypatch):
+    """The tensor-core projection (k_back_tc, complex64 M > 8: odd and even M,
+    K-padded to 32 real columns, ragged 128-frame tiles, several 256-frame
+    slots per segment) and lambda = W H (k_lambda_tc, K in {8, 16, 32}, ragged
+    bin tiles) against the SIMT kernels' oracle parity, in every combination."""
+    monkeypatch.setenv("FM_BACK", back)
+    monkeypatch.setenv("FM_LAMBDA", lam)
+    from paper_1903_03237_b200 import SeparatorConfig, run
+    F, N, seed, it = 37, 3, 21, 4
+    X = make_mixture(F, T, M, N, K, seed).astype(np.complex64)
+    Q0, g0, W0, H0 = baseline_init(F, T, M, N, K, seed)
+    ref = O.run_fastmnmf(X.astype(np.complex128), Q0, g0, W0, H0, it)
+    cfg = SeparatorConfig(method="fast-mnmf", n_sources=N, n_basis=K, n_iterations=it,
+                          precision="complex64")
+    res = run(cfg, X, init=(Q0, g0, W0, H0))
+    tr = ref["likelihood_trace"]
+    assert np.max(np.abs(res.likelihood_trace - tr) / np.abs(tr)) <= 1e-3
+    assert rel(res.images_NFTM, ref["images"]) <= 1e-3
+    assert rel(res.loop.spatial.Q_FMM, ref["Q"]) <= 1e-3
+    assert rel(res.loop.source.W_NFK, ref["W"]) <= 1e-3
+    assert rel(res.loop.source.H_NKT, ref["H"]) <= 1e-3
