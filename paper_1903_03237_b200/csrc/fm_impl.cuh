@@ -21,6 +21,7 @@
 #include "fm_back_tc.cuh"
 #include "fm_lambda_tc.cuh"
 #include "fm_vacc_blk.cuh"
+#include "fm_vacc_p.cuh"
 #include "fm_init.cuh"
 #include "fm_stft.cuh"
 #include "fm_fullrank.cuh"
@@ -160,11 +161,24 @@ inline int vacc_mode(const fm_dims* d) {
   if (e && strcmp(e, "simt") == 0) return 1;
   if (e && strcmp(e, "tc") == 0) return tc_ok ? 2 : 1;
   if (e && strcmp(e, "blk") == 0) return 0;
+  const bool p_ok = d->dtype == FM_F32 && d->M >= 5 && d->M <= 8;
+  if (e && strcmp(e, "p") == 0) return p_ok ? 3 : 1;
   // measured on B200: pair-per-thread wins at M = 4 (c2: 1.13 vs 1.89 ms) and
   // M = 8 (c1: 39.1 vs 40.8 us); at M = 16 (c3) the tensor cores (1.06 ms)
   // beat the blocked kernel (2.00 ms) and pair-per-thread (4.67 ms)
   if (d->M > 8) return tc_ok ? 2 : 0;
   return 1;
+}
+
+// k_vacc_p knobs (A/B runs): frames per chunk (128 | 256) and CTAs per SM
+inline int vp_tb() {
+  const char* e = getenv("FM_VP_TB");
+  return (e && atoi(e) == 128) ? 128 : 256;
+}
+inline int vp_ctas_per_sm() {
+  const char* e = getenv("FM_VP_CTAS");
+  const int v = e ? atoi(e) : 0;
+  return (v >= 1 && v <= 8) ? v : 0;
 }
 
 // complex64, M > 8: the projection on the tensor cores (k_back_tc);
@@ -314,6 +328,10 @@ inline Plan make_plan(const fm_dims* d) {
     const long long vtr = (blocks + vs - 1) / vs * 128;
     p.VTR = (int)vtr;
     p.vnseg = (int)((T + vtr - 1) / vtr);
+  }
+  if (d->dtype == FM_F32 && vacc_mode(d) == 3) {  // k_vacc_p: one chunk per item
+    p.VTR = vp_tb();
+    p.vnseg = (int)((T + p.VTR - 1) / p.VTR);
   }
   const size_t vpart = (size_t)B * F * p.vnseg * M * (M * (M + 1) / 2) * 2;
   // ---- fused passes: bins per CTA (8 warps; fewer where fp64 rows overflow
@@ -597,6 +615,30 @@ int Impl<R>::vacc(const fm_dims* d, const fm_state* s, cudaStream_t st) {
           launch_pdl(k_vacc_tc<MM>, dim3((unsigned)p.vnseg, (unsigned)d->F, (unsigned)d->B),
                      dim3(VtcCfg<MM>::BS), smv, st, at);
           FM_CHECK_LAUNCH("k_vacc_tc");
+          return FM_OK;
+        }
+      }
+      if constexpr (MM >= 5 && MM <= 8) {
+        if (mode == 3) {
+          VaccArgs<float> ap = *reinterpret_cast<VaccArgs<float>*>(&a);
+          ap.TR = p.VTR;
+          const long long items = (long long)d->B * d->F * p.vnseg;
+          if (items >= (1ll << 31) || d->B * d->F >= (1ll << 31)) {
+            set_error("k_vacc_p: too many (bin, chunk) items");
+            return FM_EINVAL;
+          }
+          auto go = [&](auto kern, size_t smv, int minb) -> int {
+            if (int rc = ensure_smem(kern, smv)) return rc;
+            const int per_sm = vp_ctas_per_sm() ? vp_ctas_per_sm() : minb;
+            const long long G = std::min<long long>(items, 148LL * per_sm);
+            launch_pdl(kern, dim3((unsigned)G), dim3(256), smv, st, ap, p.vnseg, (int)items);
+            return FM_OK;
+          };
+          int rc;
+          if (p.VTR == 128) rc = go(k_vacc_p<MM, 128>, VpCfg<MM, 128>::SMEM, VpCfg<MM, 128>::MINB);
+          else rc = go(k_vacc_p<MM, 256>, VpCfg<MM, 256>::SMEM, VpCfg<MM, 256>::MINB);
+          if (rc) return rc;
+          FM_CHECK_LAUNCH("k_vacc_p");
           return FM_OK;
         }
       }

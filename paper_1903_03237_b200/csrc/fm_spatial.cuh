@@ -70,7 +70,13 @@ template <typename R, int M> struct GaCfg {
   // source pairs per accumulating thread (fp32, MQ = 4, even N): 2x the slices
   static constexpr bool PAIRS = sizeof(R) == 4 && MQ == 4;
   static constexpr int RED = (PAIRS ? 1024 : 512) * MQ;  // >= slices x N x M x 2 partial sums
-  static constexpr bool ALIAS = RED <= 2 * TB * M;  // reduction reuses the staged rows
+  // staged row stride: fp32 rows of M = 8 floats are padded by 4 (an odd
+  // number of 16-byte words) so the frame-per-thread 16-byte stores
+  // do not collide; the lambda rows by 8 so the (source, slice) loads of a
+  // warp fall into distinct banks
+  static constexpr int RS = M + ((sizeof(R) == 4 && M == 8) ? 4 : 0);
+  static constexpr int LS = TB + ((sizeof(R) == 4) ? 8 : 1);
+  static constexpr bool ALIAS = RED <= 2 * TB * RS;  // reduction reuses the staged rows
 };
 
 // gain statistics (separate.py:217; _kernels.py:244-250)
@@ -78,13 +84,13 @@ template <typename R, int M>
 __global__ void __launch_bounds__(256) k_gain(GainArgs<R> a) {
   pdl_entry();
   using Cf = GaCfg<R, M>;
-  constexpr int TB = Cf::TB, MQ = Cf::MQ;
-  __shared__ __align__(16) R lams[NMAX * (TB + 1)];
-  __shared__ __align__(16) R stage[2 * TB * M];  // [TB][M] 1/y | [TB][M] x~/y^2
+  constexpr int TB = Cf::TB, MQ = Cf::MQ, RS = Cf::RS, LS = Cf::LS;
+  __shared__ __align__(16) R lams[NMAX * LS];
+  __shared__ __align__(16) R stage[2 * TB * RS];  // [TB][M] 1/y | [TB][M] x~/y^2
   __shared__ __align__(16) R gs[NMAX * M];
   __shared__ __align__(16) R redx[Cf::ALIAS ? 1 : Cf::RED];
   R* iys = stage;
-  R* xrs = stage + TB * M;
+  R* xrs = stage + TB * RS;
   R* redb = Cf::ALIAS ? stage : redx;
   const int seg = blockIdx.x, f = blockIdx.y, b = blockIdx.z, nseg = gridDim.x;
   const int tid = threadIdx.x;
@@ -140,26 +146,26 @@ __global__ void __launch_bounds__(256) k_gain(GainArgs<R> a) {
         if (!tv) iy[m] = R(0);
         xr[m] = x[m] * iy[m] * iy[m];
       }
-      RowIO<R, M>::store(iys + tid * M, iy);
-      RowIO<R, M>::store(xrs + tid * M, xr);
+      RowIO<R, M>::store(iys + tid * RS, iy);
+      RowIO<R, M>::store(xrs + tid * RS, xr);
 #pragma unroll
       for (int n = 0; n < NMAX; ++n) {
         if (n >= N) break;
-        lams[n * (TB + 1) + tid] = l[n];
+        lams[n * LS + tid] = l[n];
       }
     }
     __syncthreads();
     if (s1 < S) {
       if (NP == 2) {
         for (int tl = s1; tl < TB; tl += S) {
-          const R lv0 = lams[n1 * (TB + 1) + tl], lv1 = lams[(n1 + 1) * (TB + 1) + tl];
+          const R lv0 = lams[n1 * LS + tl], lv1 = lams[(n1 + 1) * LS + tl];
           R xv[MQ], iv[MQ];
           if constexpr (MQ == 4) {
-            lds4(xrs + tl * M + m0, xv);
-            lds4(iys + tl * M + m0, iv);
+            lds4(xrs + tl * RS + m0, xv);
+            lds4(iys + tl * RS + m0, iv);
           } else {
-            xv[0] = xrs[tl * M + m0];
-            iv[0] = iys[tl * M + m0];
+            xv[0] = xrs[tl * RS + m0];
+            iv[0] = iys[tl * RS + m0];
           }
 #pragma unroll
           for (int k = 0; k < MQ; ++k) {
@@ -171,14 +177,14 @@ __global__ void __launch_bounds__(256) k_gain(GainArgs<R> a) {
         }
       } else {
         for (int tl = s1; tl < TB; tl += S) {
-          const R lv = lams[n1 * (TB + 1) + tl];
+          const R lv = lams[n1 * LS + tl];
           R xv[MQ], iv[MQ];
           if constexpr (MQ == 4) {
-            lds4(xrs + tl * M + m0, xv);
-            lds4(iys + tl * M + m0, iv);
+            lds4(xrs + tl * RS + m0, xv);
+            lds4(iys + tl * RS + m0, iv);
           } else {
-            xv[0] = xrs[tl * M + m0];
-            iv[0] = iys[tl * M + m0];
+            xv[0] = xrs[tl * RS + m0];
+            iv[0] = iys[tl * RS + m0];
           }
 #pragma unroll
           for (int k = 0; k < MQ; ++k) {
@@ -219,10 +225,17 @@ template <typename R, int M> struct VaCfg {
   static constexpr int BS = (M <= 8) ? 256 : 512;
   static constexpr int P = M * (M + 1) / 2;
   static constexpr int S2 = BS / P;
+  // staged row strides (elements). fp32 with M % 4 == 0 pads the 1/y row to
+  // M + 4 floats and the x row to M + 2 complex: 3 and 5 (odd) 16-byte words,
+  // so the frame-per-thread 16-byte stores of phase A are conflict-free
+  // (unpadded 32- / 64-byte rows: 8 and 16 wavefronts per store instead of 4,
+  // a quarter of the kernel's shared-memory wavefronts at config 1)
+  static constexpr bool PAD = sizeof(R) == 4 && M % 4 == 0;
+  static constexpr int IYS = M + (PAD ? 4 : 0), XCS = M + (PAD ? 2 : 0);
   // frames per chunk: the staged (x, 1/y) rows must fit ~36 KB of static smem
-  static constexpr int ROWB = M * 3 * (int)sizeof(R);
+  static constexpr int ROWB = (IYS + 2 * XCS) * (int)sizeof(R);
   static constexpr int TB = (256 * ROWB <= 36864) ? 256 : (128 * ROWB <= 36864) ? 128 : 64;
-  static constexpr int STAGEB = TB * M * (int)(sizeof(R) + 2 * sizeof(R));
+  static constexpr int STAGEB = TB * ROWB;
   // fp32, M = 6..8: cap registers for 3 CTAs (24 warps) per SM -- the pair loop is
   // shared-load latency bound, not issue bound
   static constexpr int MINB = (sizeof(R) == 4 && M >= 6 && M <= 8) ? 3 : 1;
@@ -249,11 +262,11 @@ __global__ void __launch_bounds__(VaCfg<R, M>::BS, VaCfg<R, M>::MINB) k_vacc(Vac
   pdl_entry();
   using C = cplx<R>;
   using Cf = VaCfg<R, M>;
-  constexpr int BS = Cf::BS, TB = Cf::TB, P = Cf::P, S2 = Cf::S2;
+  constexpr int BS = Cf::BS, TB = Cf::TB, P = Cf::P, S2 = Cf::S2, IYS = Cf::IYS, XCS = Cf::XCS;
   constexpr int BUFB = (Cf::STAGEB > M * P * (int)sizeof(C)) ? Cf::STAGEB : M * P * (int)sizeof(C);
   __shared__ __align__(16) unsigned char buf[BUFB];
   R* iys = reinterpret_cast<R*>(buf);
-  C* Xc = reinterpret_cast<C*>(buf + TB * M * sizeof(R));
+  C* Xc = reinterpret_cast<C*>(buf + TB * IYS * sizeof(R));
   __shared__ __align__(16) R gs[NMAX * M];
   __shared__ int pairs[2 * P];
   const int seg = blockIdx.x, f = blockIdx.y, b = blockIdx.z, nseg = gridDim.x;
@@ -308,6 +321,10 @@ __global__ void __launch_bounds__(VaCfg<R, M>::BS, VaCfg<R, M>::MINB) k_vacc(Vac
   C v[M];
 #pragma unroll
   for (int m = 0; m < M; ++m) v[m] = cmake<C>(0.0, 0.0);
+  constexpr bool PACKW = sizeof(R) == 4 && M % 4 == 0;
+  float2 ar[PACKW ? M / 2 : 1], ai[PACKW ? M / 2 : 1];
+#pragma unroll
+  for (int h = 0; h < (PACKW ? M / 2 : 1); ++h) ar[h] = ai[h] = make_float2(0.f, 0.f);
   for (int c0 = ta; c0 < tb; c0 += TB) {
     if (tid < TB) {
       const bool tv = c0 + tid < tb;
@@ -323,18 +340,54 @@ __global__ void __launch_bounds__(VaCfg<R, M>::BS, VaCfg<R, M>::MINB) k_vacc(Vac
 #pragma unroll
       for (int m = 0; m < M; ++m)
         if (!tv) iy[m] = R(0);
-      RowIO<R, M>::store(iys + tid * M, iy);
-      CRowIO<R, M>::store(Xc + tid * M, xv);
+      RowIO<R, M>::store(iys + tid * IYS, iy);
+      CRowIO<R, M>::store(Xc + tid * XCS, xv);
     }
     __syncthreads();
+    if constexpr (PACKW) {
+      // fp32, M % 4 == 0: the accumulators pack two WEIGHTS per FFMA2
+      // (re and im parts apart), so the 1/y pairs are the 16-B shared loads'
+      // own register pairs and only (p.x, p.x), (p.y, p.y) are formed per
+      // frame -- the (1/y, 1/y) operand of the re/im packing costs a MOV per
+      // FFMA2; two frames per trip, their FFMA2 groups not interleaved
+      if (act) {
+        auto frame = [&](const C xi, const C xj, const float (&iy)[M]) {
+          const float px = xi.x * xj.x + xi.y * xj.y;  // x_i conj(x_j)
+          const float py = xi.y * xj.x - xi.x * xj.y;
+          const float2 pxx = make_float2(px, px), pyy = make_float2(py, py);
+#pragma unroll
+          for (int h = 0; h < M / 2; ++h) {
+            const float2 w = make_float2(iy[2 * h], iy[2 * h + 1]);
+            ar[h] = fma2(w, pxx, ar[h]);
+            ai[h] = fma2(w, pyy, ai[h]);
+          }
+        };
+        int tl = s2;
+        for (; tl + S2 < TB; tl += 2 * S2) {
+          const C xi0 = Xc[tl * XCS + pi], xj0 = Xc[tl * XCS + pj];
+          const C xi1 = Xc[(tl + S2) * XCS + pi], xj1 = Xc[(tl + S2) * XCS + pj];
+          float iy0[M], iy1[M];
+          RowIO<float, M>::load(reinterpret_cast<const float*>(iys) + tl * IYS, iy0);
+          RowIO<float, M>::load(reinterpret_cast<const float*>(iys) + (tl + S2) * IYS, iy1);
+          frame(xi0, xj0, iy0);
+          frame(xi1, xj1, iy1);
+        }
+        if (tl < TB) {
+          const C xi = Xc[tl * XCS + pi], xj = Xc[tl * XCS + pj];
+          float iy[M];
+          RowIO<float, M>::load(reinterpret_cast<const float*>(iys) + tl * IYS, iy);
+          frame(xi, xj, iy);
+        }
+      }
+    } else
     if (act) {
       int tl = s2;
       for (; tl + S2 < TB; tl += 2 * S2) {
-        const C xi0 = Xc[tl * M + pi], xj0 = Xc[tl * M + pj];
-        const C xi1 = Xc[(tl + S2) * M + pi], xj1 = Xc[(tl + S2) * M + pj];
+        const C xi0 = Xc[tl * XCS + pi], xj0 = Xc[tl * XCS + pj];
+        const C xi1 = Xc[(tl + S2) * XCS + pi], xj1 = Xc[(tl + S2) * XCS + pj];
         R iy0[M], iy1[M];
-        RowIO<R, M>::load(iys + tl * M, iy0);
-        RowIO<R, M>::load(iys + (tl + S2) * M, iy1);
+        RowIO<R, M>::load(iys + tl * IYS, iy0);
+        RowIO<R, M>::load(iys + (tl + S2) * IYS, iy1);
         C p0, p1;  // x_i conj(x_j)
         p0.x = xi0.x * xj0.x + xi0.y * xj0.y;
         p0.y = xi0.y * xj0.x - xi0.x * xj0.y;
@@ -347,17 +400,24 @@ __global__ void __launch_bounds__(VaCfg<R, M>::BS, VaCfg<R, M>::MINB) k_vacc(Vac
         }
       }
       if (tl < TB) {
-        const C xi = Xc[tl * M + pi], xj = Xc[tl * M + pj];
+        const C xi = Xc[tl * XCS + pi], xj = Xc[tl * XCS + pj];
         C pr;
         pr.x = xi.x * xj.x + xi.y * xj.y;
         pr.y = xi.y * xj.x - xi.x * xj.y;
         R iy[M];
-        RowIO<R, M>::load(iys + tl * M, iy);
+        RowIO<R, M>::load(iys + tl * IYS, iy);
 #pragma unroll
         for (int m = 0; m < M; ++m) v[m] = fma2(cmake<C>(iy[m], iy[m]), pr, v[m]);
       }
     }
     __syncthreads();
+  }
+  if constexpr (PACKW) {
+#pragma unroll
+    for (int h = 0; h < M / 2; ++h) {
+      v[2 * h] = cmake<C>(ar[h].x, ai[h].x);
+      v[2 * h + 1] = cmake<C>(ar[h].y, ai[h].y);
+    }
   }
   // fixed-order slice reduction (staging area reused), then the segment partial
   C* red = reinterpret_cast<C*>(buf);

@@ -86,3 +86,28 @@ def test_projection_and_lambda_variants(M, T, K, back, lam, monkeypatch):
     assert rel(res.loop.spatial.Q_FMM, ref["Q"]) <= 1e-3
     assert rel(res.loop.source.W_NFK, ref["W"]) <= 1e-3
     assert rel(res.loop.source.H_NKT, ref["H"]) <= 1e-3
+
+
+@pytest.mark.parametrize("tb", ["256", "128"])
+@pytest.mark.parametrize("M,F,T,N", [(8, 37, 1024, 4), (8, 5, 300, 3), (7, 150, 517, 2), (6, 460, 130, 3),
+                                     (5, 3, 1300, 2), (8, 700, 256, 4)])
+def test_vacc_persistent_vs_oracle(M, F, T, N, tb, monkeypatch):
+    """k_vacc_p (persistent CTAs over (bin, chunk) items, complex64 M = 5..8):
+    runs that start and end inside a bin, ragged last chunks, fewer items than
+    CTAs (F = 3, 5), more items than CTAs (F = 460, 700), one chunk per bin;
+    fused run against the oracle."""
+    monkeypatch.setenv("FM_VACC", "p")
+    monkeypatch.setenv("FM_VP_TB", tb)
+    from paper_1903_03237_b200 import SeparatorConfig, run
+    K, seed, it = 4, 300 + M + F, 3
+    X = make_mixture(F, T, M, N, K, seed).astype(np.complex64)
+    Q0, g0, W0, H0 = baseline_init(F, T, M, N, K, seed)
+    ref = O.run_fastmnmf(X.astype(np.complex128), Q0, g0, W0, H0, it)
+    cfg = SeparatorConfig(method="fast-mnmf", n_sources=N, n_basis=K, n_iterations=it,
+                          precision="complex64")
+    res = run(cfg, X, init=(Q0, g0, W0, H0))
+    tr = ref["likelihood_trace"]
+    assert np.max(np.abs(res.likelihood_trace - tr) / np.abs(tr)) <= 1e-3
+    assert rel(res.images_NFTM, ref["images"]) <= 1e-3
+    assert rel(res.loop.spatial.Q_FMM, ref["Q"]) <= 1e-3
+    assert rel(res.loop.spatial.g_NFM, ref["g"]) <= 1e-3
