@@ -414,17 +414,20 @@ __global__ void __launch_bounds__(256) k_phi(const R* __restrict__ lam, const R*
   const int f = blockIdx.y, b = blockIdx.z, tid = threadIdx.x;
   const int t = blockIdx.x * 256 + tid;
   const size_t FT = (size_t)F * T;
-  for (int e = tid; e < N * M; e += 256)
-    gs[e] = g[(size_t)b * N * F * M + (size_t)(e / M) * F * M + (size_t)f * M + (e % M)];
-  __syncthreads();
-  if (t >= T) return;
+  // the frame's own loads go out before the gains are staged, so a CTA waits
+  // for one global round trip, not two (gains -> barrier -> lambda, x~)
+  const int tc = t < T ? t : T - 1;
   const R fl = floorp[b];
-  const R* lb = lam + (size_t)b * N * FT + (size_t)f * T + t;
+  const R* lb = lam + (size_t)b * N * FT + (size_t)f * T + tc;
   R l[NMAX];
 #pragma unroll
   for (int n = 0; n < NMAX; ++n) l[n] = n < N ? lb[(size_t)n * FT] : R(0);
   R xtv[M], iy[M], y[M];
-  RowIO<R, M>::load(xt + (((size_t)b * F + f) * T + t) * M, xtv);
+  RowIO<R, M>::load(xt + (((size_t)b * F + f) * T + tc) * M, xtv);
+  for (int e = tid; e < N * M; e += 256)
+    gs[e] = g[(size_t)b * N * F * M + (size_t)(e / M) * F * M + (size_t)f * M + (e % M)];
+  __syncthreads();
+  if (t >= T) return;
   model_power<R, M>(l, gs, N, fl, iy, y);
   phi_point<R, M>(xtv, iy, gs, N, phi + (size_t)b * 2 * N * FT, FT, (size_t)f * T + t);
 }

@@ -97,8 +97,6 @@ __global__ void __launch_bounds__(256) k_gain(GainArgs<R> a) {
   const int N = a.N, T = a.T, F = a.F;
   const size_t FT = (size_t)F * T;
   const int ta = seg * a.TR, tb = min(T, ta + a.TR);
-  for (int e = tid; e < N * M; e += 256)
-    gs[e] = a.g[(size_t)b * N * F * M + (size_t)(e / M) * F * M + (size_t)f * M + (e % M)];
   const R fl = a.floorp[b];
   const R* lamb = a.lam + (size_t)b * N * FT + (size_t)f * T;
   const R* xtb = a.xt + ((size_t)b * F + f) * T * M;
@@ -114,7 +112,9 @@ __global__ void __launch_bounds__(256) k_gain(GainArgs<R> a) {
     }
     RowIO<R, M>::load(xtb + (size_t)tc * M, xp);
   };
-  if (tid < TB) fetch(ta);
+  if (tid < TB) fetch(ta);  // in flight before the gains are staged (one round trip, not two)
+  for (int e = tid; e < N * M; e += 256)
+    gs[e] = a.g[(size_t)b * N * F * M + (size_t)(e / M) * F * M + (size_t)f * M + (e % M)];
   // accumulate mapping: thread = (NP sources from n1, MQ consecutive
   // channels, slice); with MQ = 4 and N even a thread takes a source pair, so
   // one pair of 16-B loads of x~/y^2 and 1/y feeds 16 FMAs (c3: the loop was
@@ -274,6 +274,23 @@ __global__ void __launch_bounds__(VaCfg<R, M>::BS, VaCfg<R, M>::MINB) k_vacc(Vac
   const int N = a.N, T = a.T, F = a.F;
   const size_t FT = (size_t)F * T;
   const int ta = seg * a.TR, tb = min(T, ta + a.TR);
+  const R fl = a.floorp[b];
+  const R* lamb = a.lam + (size_t)b * N * FT + (size_t)f * T;
+  const C* Xb = a.X + ((size_t)b * F + f) * T * M;
+  R lp[NMAX];
+  C xp[M];
+  auto fetch = [&](int c0) {
+    const int t = c0 + tid;
+    const int tc = t < tb ? t : tb - 1;
+#pragma unroll
+    for (int n = 0; n < NMAX; ++n) {
+      lp[n] = R(0);
+      if (n >= N) break;
+      lp[n] = lamb[(size_t)n * FT + tc];
+    }
+    CRowIO<R, M>::load(Xb + (size_t)tc * M, xp);
+  };
+  if (tid < TB) fetch(ta);  // in flight while the gains are finished (one round trip, not two)
   // finish the gain MU from the k_gain segment partials (fixed order)
   for (int e = tid; e < N * M; e += BS) {
     const int n = e / M, m = e % M;
@@ -297,23 +314,6 @@ __global__ void __launch_bounds__(VaCfg<R, M>::BS, VaCfg<R, M>::MINB) k_vacc(Vac
     pairs[2 * tid] = i;
     pairs[2 * tid + 1] = i + r;
   }
-  const R fl = a.floorp[b];
-  const R* lamb = a.lam + (size_t)b * N * FT + (size_t)f * T;
-  const C* Xb = a.X + ((size_t)b * F + f) * T * M;
-  R lp[NMAX];
-  C xp[M];
-  auto fetch = [&](int c0) {
-    const int t = c0 + tid;
-    const int tc = t < tb ? t : tb - 1;
-#pragma unroll
-    for (int n = 0; n < NMAX; ++n) {
-      lp[n] = R(0);
-      if (n >= N) break;
-      lp[n] = lamb[(size_t)n * FT + tc];
-    }
-    CRowIO<R, M>::load(Xb + (size_t)tc * M, xp);
-  };
-  if (tid < TB) fetch(ta);
   __syncthreads();
   const int p = tid % P, s2 = tid / P;
   const bool act = s2 < S2;
@@ -842,10 +842,15 @@ __global__ void __launch_bounds__(256, (M > 8 ? 2 : 3)) k_back(BackArgs<R> a) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int N = a.N, T = a.T, F = a.F;
   const size_t FT = (size_t)F * T;
-  for (int e = tid; e < M * M; e += 256) Qr[e] = a.Q[((size_t)b * F + f) * M * M + e];
-  for (int e = tid; e < N * M; e += 256)
-    gs[e] = a.g[(size_t)b * N * F * M + (size_t)(e / M) * F * M + (size_t)f * M + (e % M)];
-  if (tid < NMAX) cs[tid] = a.cs ? a.cs[((size_t)b * F + f) * NMAX + tid] : R(1);
+  // Q, g and c go to registers first and to shared memory only after the
+  // frame loads below are in flight: one global round trip before the barrier
+  // instead of two (M * M <= 256 and N * M <= 256: one element per thread)
+  C qreg = cmake<C>(0.0, 0.0);
+  R greg = R(0), creg = R(1);
+  if (tid < M * M) qreg = a.Q[((size_t)b * F + f) * M * M + tid];
+  if (tid < N * M)
+    greg = a.g[(size_t)b * N * F * M + (size_t)(tid / M) * F * M + (size_t)f * M + (tid % M)];
+  if (tid < NMAX && a.cs) creg = a.cs[((size_t)b * F + f) * NMAX + tid];
   double ll = 0.0;
   C xv[PPT][M];
   R l[PPT][NMAX];
@@ -863,6 +868,9 @@ __global__ void __launch_bounds__(256, (M > 8 ? 2 : 3)) k_back(BackArgs<R> a) {
       }
     }
   }
+  if (tid < M * M) Qr[tid] = qreg;
+  if (tid < N * M) gs[tid] = greg;
+  if (tid < NMAX) cs[tid] = creg;
   __syncthreads();
   const R fl = a.floorp[b];
 #pragma unroll
