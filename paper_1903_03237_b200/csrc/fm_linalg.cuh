@@ -240,7 +240,10 @@ __device__ bool warp_inv_pivot(C2* A, int lane, double* logabs) {
   using Rc = decltype(C2().x);
   constexpr int W2 = 2 * M;
   constexpr int NE = (M * W2 + 31) / 32;
-  double la = 0.0;
+  // log|det| = 1/2 log prod |pivot|^2: the product is carried in fp64 and one
+  // log taken when it leaves [1e-150, 1e150] or at the end -- a double log per
+  // elimination step sat on the warp's serial chain
+  double la = 0.0, pprod = 1.0;
   for (int k = 0; k < M; ++k) {
     Rc v = Rc(-1);
     int idx = lane;
@@ -267,7 +270,11 @@ __device__ bool warp_inv_pivot(C2* A, int lane, double* logabs) {
     }
     __syncwarp();
     const C2 piv = A[k * W2 + k];
-    la += 0.5 * log((double)piv.x * piv.x + (double)piv.y * piv.y);
+    pprod *= (double)piv.x * piv.x + (double)piv.y * piv.y;
+    if (pprod > 1e150 || pprod < 1e-150) {
+      la += 0.5 * log(pprod);
+      pprod = 1.0;
+    }
     const C2 rp = crcp(piv);
     C2 nv[NE];
 #pragma unroll
@@ -287,6 +294,7 @@ __device__ bool warp_inv_pivot(C2* A, int lane, double* logabs) {
     }
     __syncwarp();
   }
+  la += 0.5 * log(pprod);
   *logabs = la;
   return true;
 }

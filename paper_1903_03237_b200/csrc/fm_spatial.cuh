@@ -762,10 +762,16 @@ __global__ void __launch_bounds__(IpCfg<M>::BS) k_ip(IpArgs<R> a) {
       const double r = rown[e % M];
       gs[e] = (R)((double)gs[e] / (r * r));
     }
-    if (tid == 0) {
-      double s = 0.0;
-      for (int m = 0; m < M; ++m) s += log(rown[m]);
-      misc[1] -= s;
+    if (tid == 0) {  // sum_m log ||row m||: one log per range-guarded product
+      double s = 0.0, pr = 1.0;
+      for (int m = 0; m < M; ++m) {
+        pr *= rown[m];
+        if (pr > 1e150 || pr < 1e-150) {
+          s += log(pr);
+          pr = 1.0;
+        }
+      }
+      misc[1] -= s + log(pr);
     }
     __syncthreads();
     if (tid < N) {
