@@ -83,8 +83,16 @@ __device__ __forceinline__ float2 cmul(float2 a, float2 b) {
 __device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
 __device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
 __device__ __forceinline__ float cabs1(float2 a) { return fabsf(a.x) + fabsf(a.y); }
+// 1/x for a normal positive fp32 x: MUFU.RCP plus one Newton step (<= 1 ulp)
+// -- the IEEE division expands to ~10 instructions with a slow-path call and
+// sat on every Gauss-Jordan step of the fp32 inverses
+__device__ __forceinline__ float frcp_nr(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return fmaf(r, fmaf(-x, r, 1.0f), r);
+}
 __device__ __forceinline__ float2 crcp(float2 p) {
-  const float inv = 1.0f / (p.x * p.x + p.y * p.y);
+  const float inv = frcp_nr(p.x * p.x + p.y * p.y);
   return make_float2(p.x * inv, -p.y * inv);
 }
 __device__ __forceinline__ float drsqrt(float x) { return rsqrtf(x); }

@@ -202,7 +202,8 @@ __device__ bool warp_inv_hpd_f32(float2* A, int lane) {
     const float2 p = A[k * M + k];
     if (!(p.x > 0.0f) || !isfinite(p.x)) return false;
     // HPD: the pivot is real; 1/Re p (no |p|^2, which halves the fp32 range)
-    const float2 rp = make_float2(1.0f / p.x, 0.0f);
+    const float rpx = frcp_nr(p.x);
+    const float2 rp = make_float2(rpx, 0.0f);
     float2 nv[NE];
 #pragma unroll
     for (int r = 0; r < NE; ++r) {
@@ -210,8 +211,8 @@ __device__ bool warp_inv_hpd_f32(float2* A, int lane) {
       if (e < M * M) {
         const int i = e / M, j = e % M;
         const float2 aik = A[i * M + k], akj = A[k * M + j], aij = A[e];
-        const float2 akjr = make_float2(akj.x * rp.x - akj.y * rp.y, akj.x * rp.y + akj.y * rp.x);
-        const float2 aikr = make_float2(aik.x * rp.x - aik.y * rp.y, aik.x * rp.y + aik.y * rp.x);
+        const float2 akjr = make_float2(akj.x * rpx, akj.y * rpx);  // the pivot is real
+        const float2 aikr = make_float2(aik.x * rpx, aik.y * rpx);
         const float2 other = make_float2(aij.x - (aik.x * akjr.x - aik.y * akjr.y),
                                          aij.y - (aik.x * akjr.y + aik.y * akjr.x));
         const bool rk = i == k, ck = j == k;

@@ -225,14 +225,28 @@ __global__ void __launch_bounds__(256) k_hstats(const R* __restrict__ phi, const
   const R* P2 = P1 + (size_t)N * FTs;
   const R* Wn = W + (size_t)bn * F * K;
   const bool async = sizeof(R) == 4 && (T % 4) == 0;
+  const bool asyncw = sizeof(R) == 4 && (K % 4) == 0 && (LDW % 4) == 0 && (KB % 4) == 0 &&
+                      (reinterpret_cast<uintptr_t>(W) & 15) == 0;
   auto stage = [&](int st) { return stage0 + st * Cf::STAGE; };
   auto load = [&](int st, int c0) {
     R* ws = stage(st);
     R* p1s = ws + FCH * LDW;
     R* p2s = p1s + FCH * LDP;
-    for (int e = tid; e < FCH * KB; e += 256) {
-      const int fl = e / KB, k = e % KB, f = c0 + fl;
-      ws[fl * LDW + k] = (f < F && k < K) ? Wn[(size_t)f * K + k] : R(0);
+    if (asyncw) {
+      // W rows by 16-byte cp.async like the phi tiles: the plain load -> store
+      // staging made every thread wait out a global round trip per chunk
+      // (a third of the kernel's stall samples at config 1)
+      constexpr int QW = KB / 4;
+      for (int e = tid; e < FCH * QW; e += 256) {
+        const int fl = e / QW, q = e % QW, f = c0 + fl;
+        const bool v = f < F && 4 * q < K;
+        cp_async16(ws + fl * LDW + 4 * q, Wn + (v ? (size_t)f * K + 4 * q : 0), v);
+      }
+    } else {
+      for (int e = tid; e < FCH * KB; e += 256) {
+        const int fl = e / KB, k = e % KB, f = c0 + fl;
+        ws[fl * LDW + k] = (f < F && k < K) ? Wn[(size_t)f * K + k] : R(0);
+      }
     }
     if (async) {
       constexpr int Q = TT / 4;
