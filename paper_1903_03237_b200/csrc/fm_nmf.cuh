@@ -402,6 +402,8 @@ __device__ __forceinline__ void phi_point(const R (&xtv)[M], const R (&iy)[M], c
   R r[M];
 #pragma unroll
   for (int m = 0; m < M; ++m) r[m] = xtv[m] * iy[m] * iy[m];
+  R* q1 = phi + off;
+  R* q2 = q1 + (size_t)N * FT;
 #pragma unroll
   for (int n = 0; n < NMAX; ++n) {
     if (n >= N) break;
@@ -413,8 +415,10 @@ __device__ __forceinline__ void phi_point(const R (&xtv)[M], const R (&iy)[M], c
       p1 += g[m] * r[m];
       p2 += g[m] * iy[m];
     }
-    phi[(size_t)n * FT + off] = p1;
-    phi[(size_t)(N + n) * FT + off] = p2;
+    q1[0] = p1;
+    q2[0] = p2;
+    q1 += FT;  // pointer steps instead of a 64-bit multiply per store
+    q2 += FT;
   }
 }
 

@@ -123,8 +123,18 @@ __global__ void __launch_bounds__(256) k_gain(GainArgs<R> a) {
   // (only when enough items remain that the slice reduction stays short:
   // c3 k_gain 489 -> 418 us; c1, 4 pair items, 18.4 -> 20.5 us, so not there)
   const int NP = (Cf::PAIRS && (N % 2) == 0 && (N / 2) * Q >= 8) ? 2 : 1;
-  const int E = (N / NP) * Q, S = 256 / E;
-  const int e1 = tid % E, s1 = tid / E;
+  const int E = (N / NP) * Q;
+  int S, e1, s1;
+  if ((E & (E - 1)) == 0) {  // power of two (the BASELINE shapes): shifts, no integer divisions
+    const int sh = __ffs(E) - 1;
+    S = 256 >> sh;
+    e1 = tid & (E - 1);
+    s1 = tid >> sh;
+  } else {
+    S = 256 / E;
+    e1 = tid % E;
+    s1 = tid / E;
+  }
   const int n1 = (e1 / Q) * NP, m0 = (e1 % Q) * MQ;
   R num[2][MQ], den[2][MQ];
 #pragma unroll
