@@ -548,6 +548,17 @@ __global__ void __launch_bounds__(IpCfg<M>::BS) k_ip(IpArgs<R> a) {
   const R* Wsg = a.Wsrc + (size_t)b * (N - a.n0) * F * K + (size_t)f * K;
   const unsigned it = *a.iter;
   const long long fglob = a.f_offset + f;
+  // Q and the updated gains go to registers before the V partials are summed
+  // (their loads are in flight during that loop: one global round trip before
+  // the first barrier, not two)
+  constexpr bool PRE = M * M <= BS && NMAX * M <= BS;
+  C qreg = cmake<C>(0.0, 0.0);
+  R gnreg = R(0);
+  if constexpr (PRE) {
+    if (tid < M * M) qreg = Qg[tid];
+    if (tid < N * M)
+      gnreg = a.gnew[(size_t)b * N * F * M + (size_t)(tid / M) * F * M + (size_t)f * M + (tid % M)];
+  }
   {  // V_f = (1/T) sum over the segment partials (fixed order, fp64), mirrored
     constexpr int P = M * (M + 1) / 2;
     const C* vp = a.Vpart + ((size_t)b * F + f) * a.nseg * M * P;
@@ -571,9 +582,14 @@ __global__ void __launch_bounds__(IpCfg<M>::BS) k_ip(IpArgs<R> a) {
       if (i != j) Vd[((size_t)m * M + j) * M + i] = make_double2(d.x, -d.y);
     }
   }
-  for (int e = tid; e < M * M; e += BS) Qd[e] = to_c2(Qg[e], C2());
-  for (int e = tid; e < N * M; e += BS)
-    gs[e] = a.gnew[(size_t)b * N * F * M + (size_t)(e / M) * F * M + (size_t)f * M + (e % M)];
+  if constexpr (PRE) {
+    if (tid < M * M) Qd[tid] = to_c2(qreg, C2());
+    if (tid < N * M) gs[tid] = gnreg;
+  } else {
+    for (int e = tid; e < M * M; e += BS) Qd[e] = to_c2(Qg[e], C2());
+    for (int e = tid; e < N * M; e += BS)
+      gs[e] = a.gnew[(size_t)b * N * F * M + (size_t)(e / M) * F * M + (size_t)f * M + (e % M)];
+  }
   if (tid < NMAX) cs[tid] = R(1);
   if (tid == 0) flags[0] = flags[1] = 0;
   __syncthreads();
