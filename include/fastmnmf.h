@@ -202,10 +202,12 @@ int fm_refresh(const fm_dims* d, const fm_state* s, void* stream);
  * pairs (BASELINE config 2), the split schedule otherwise. The environment
  * variable FM_SCHEDULE=split|fused|bin forces one (bin only where eligible).
  * Kernel variants inside a schedule are picked by shape: complex64
- * with even M in 10..16 accumulates V_fm on the tensor cores (k_vacc_tc;
- * FM_VACC=blk|simt|tc forces one) -- X must then be 16-byte aligned -- and
- * complex64 with M > 8 projects on the tensor cores (k_back_tc; FM_BACK=simt
- * forces the SIMT kernel). */
+ * with even M in 10..16 accumulates V_fm on the tensor cores (k_vacc_tc; X
+ * must then be 16-byte aligned) and complex64 with M > 8 projects on the
+ * tensor cores (k_back_tc; FM_BACK=simt forces the SIMT kernel).
+ * FM_VACC=blk|simt|tc|p forces a V kernel (p: the persistent k_vacc_p,
+ * complex64 M = 5..8, opt-in). FM_UNROLL=n captures n iterations per CUDA
+ * graph in fm_run (default 1; measured slower at config 1, DESIGN 8a). */
 #define FM_SCHED_SPLIT 0
 #define FM_SCHED_FUSED 1
 #define FM_SCHED_BIN 2

@@ -91,3 +91,31 @@ def test_fused_state_assignment_refreshes():
     ll_b = b.iterate()
     assert abs(ll_a - ll_b) <= 1e-12 * abs(ll_b)
     np.testing.assert_allclose(a.source.W_NFK, b.source.W_NFK, rtol=1e-12)
+
+
+@pytest.mark.parametrize("unroll", ["4", "16"])
+def test_unrolled_graph_matches_single(unroll, monkeypatch):
+    """FM_UNROLL: several iterations captured per CUDA graph (plus single-
+    iteration graphs for the remainder) give bit-identical state and trace to
+    one graph per iteration."""
+    from paper_1903_03237_b200.separate import DeviceLoop
+    import torch
+    F, T, M, N, K, seed, it = 19, 96, 4, 2, 4, 5, 10
+    X = make_mixture(F, T, M, N, K, seed)
+    Q0, g0, W0, H0 = baseline_init(F, T, M, N, K, seed)
+    dev = torch.device("cuda", 0)
+    Xd = torch.from_numpy(X).to(dev)[None].contiguous()
+    fl = torch.tensor([1e-12 * float((np.abs(X) ** 2).max())], dtype=torch.float64)
+    t = lambda a: torch.from_numpy(np.asarray(a))[None]
+    out = []
+    for u in ("1", unroll):
+        monkeypatch.setenv("FM_UNROLL", u)
+        lp = DeviceLoop(Xd, t(Q0), t(g0), t(W0), t(H0), fl, True, 1, n_trace=it)
+        lp.prologue()
+        lp.run(it, use_graph=True)
+        torch.cuda.synchronize()
+        assert lp.status_error() is None
+        out.append((lp.trace[:, 0].cpu().numpy().copy(), lp.source.W_NFK.copy(), lp.spatial.Q_FMM.copy()))
+    np.testing.assert_array_equal(out[0][0], out[1][0])
+    np.testing.assert_array_equal(out[0][1], out[1][1])
+    np.testing.assert_array_equal(out[0][2], out[1][2])
