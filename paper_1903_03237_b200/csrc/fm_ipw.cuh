@@ -234,15 +234,9 @@ __device__ __forceinline__ void ipw_core(unsigned char* sm, int lane, int N, int
       const double r = rown[e % M];
       gs[e] = (R)((double)gs[e] / (r * r));
     }
-    double ls = 0.0, pr = 1.0;  // sum_m log ||row m||: one log per range-guarded product
-    for (int m = 0; m < M; ++m) {
-      pr *= rown[m];
-      if (pr > 1e150 || pr < 1e-150) {
-        ls += log(pr);
-        pr = 1.0;
-      }
-    }
-    ldet -= ls + log(pr);
+    double ls = 0.0;
+    for (int m = 0; m < M; ++m) ls += log(rown[m]);
+    ldet -= ls;
     __syncwarp();
     if (lane < N) {
       R s = 0;

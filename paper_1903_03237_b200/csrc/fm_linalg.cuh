@@ -236,14 +236,17 @@ __device__ bool warp_inv_hpd_f32(float2* A, int lane) {
 // the augmented [Q | I] (M x 2M, row-major) by one warp; on success the
 // right half holds Q^-1 and *logabs = sum_k log|pivot_k| = log|det Q|
 // (the LU pivots; slogdet, separate.py:238).
-template <int M, typename C2>
+template <int M, typename C2, bool PRODLOG = false>
 __device__ bool warp_inv_pivot(C2* A, int lane, double* logabs) {
   using Rc = decltype(C2().x);
   constexpr int W2 = 2 * M;
   constexpr int NE = (M * W2 + 31) / 32;
-  // log|det| = 1/2 log prod |pivot|^2: the product is carried in fp64 and one
-  // log taken when it leaves [1e-150, 1e150] or at the end -- a double log per
-  // elimination step sat on the warp's serial chain
+  // PRODLOG (k_ip): log|det| = 1/2 log prod |pivot|^2, the product carried in
+  // fp64 and one log taken when it leaves [1e-150, 1e150] or at the end -- a
+  // double log per elimination step sat on warp 0's serial chain (c1 k_ip 22.5
+  // -> 20.5 us). The warp-per-bin callers (ipw_core: k_ip_w, k_binw) keep the
+  // log per step: with every warp on its own bin the logs overlap other warps'
+  // work, and the guarded form measured slower there (c2 k_binw 4.03 -> 4.23 ms)
   double la = 0.0, pprod = 1.0;
   for (int k = 0; k < M; ++k) {
     Rc v = Rc(-1);
@@ -271,10 +274,14 @@ __device__ bool warp_inv_pivot(C2* A, int lane, double* logabs) {
     }
     __syncwarp();
     const C2 piv = A[k * W2 + k];
-    pprod *= (double)piv.x * piv.x + (double)piv.y * piv.y;
-    if (pprod > 1e150 || pprod < 1e-150) {
-      la += 0.5 * log(pprod);
-      pprod = 1.0;
+    if constexpr (PRODLOG) {
+      pprod *= (double)piv.x * piv.x + (double)piv.y * piv.y;
+      if (pprod > 1e150 || pprod < 1e-150) {
+        la += 0.5 * log(pprod);
+        pprod = 1.0;
+      }
+    } else {
+      la += 0.5 * log((double)piv.x * piv.x + (double)piv.y * piv.y);
     }
     const C2 rp = crcp(piv);
     C2 nv[NE];
@@ -295,7 +302,7 @@ __device__ bool warp_inv_pivot(C2* A, int lane, double* logabs) {
     }
     __syncwarp();
   }
-  la += 0.5 * log(pprod);
+  if constexpr (PRODLOG) la += 0.5 * log(pprod);
   *logabs = la;
   return true;
 }

@@ -402,8 +402,6 @@ __device__ __forceinline__ void phi_point(const R (&xtv)[M], const R (&iy)[M], c
   R r[M];
 #pragma unroll
   for (int m = 0; m < M; ++m) r[m] = xtv[m] * iy[m] * iy[m];
-  R* q1 = phi + off;
-  R* q2 = q1 + (size_t)N * FT;
 #pragma unroll
   for (int n = 0; n < NMAX; ++n) {
     if (n >= N) break;
@@ -415,10 +413,8 @@ __device__ __forceinline__ void phi_point(const R (&xtv)[M], const R (&iy)[M], c
       p1 += g[m] * r[m];
       p2 += g[m] * iy[m];
     }
-    q1[0] = p1;
-    q2[0] = p2;
-    q1 += FT;  // pointer steps instead of a 64-bit multiply per store
-    q2 += FT;
+    phi[(size_t)n * FT + off] = p1;
+    phi[(size_t)(N + n) * FT + off] = p2;
   }
 }
 
@@ -432,22 +428,40 @@ __global__ void __launch_bounds__(256) k_phi(const R* __restrict__ lam, const R*
   const int f = blockIdx.y, b = blockIdx.z, tid = threadIdx.x;
   const int t = blockIdx.x * 256 + tid;
   const size_t FT = (size_t)F * T;
-  // the frame's own loads go out before the gains are staged, so a CTA waits
-  // for one global round trip, not two (gains -> barrier -> lambda, x~)
-  const int tc = t < T ? t : T - 1;
-  const R fl = floorp[b];
-  const R* lb = lam + (size_t)b * N * FT + (size_t)f * T + tc;
-  R l[NMAX];
+  // M <= 8: the frame's own loads go out before the gains are staged, so a CTA
+  // waits for one global round trip, not two (gains -> barrier -> lambda, x~;
+  // c1 k_phi). At M = 16 the values held across the barrier cost more than the
+  // round trip (c3: 248 -> 256 us), so the loads stay behind it there.
+  if constexpr (M <= 8) {
+    const int tc = t < T ? t : T - 1;
+    const R fl = floorp[b];
+    const R* lb = lam + (size_t)b * N * FT + (size_t)f * T + tc;
+    R l[NMAX];
 #pragma unroll
-  for (int n = 0; n < NMAX; ++n) l[n] = n < N ? lb[(size_t)n * FT] : R(0);
-  R xtv[M], iy[M], y[M];
-  RowIO<R, M>::load(xt + (((size_t)b * F + f) * T + tc) * M, xtv);
-  for (int e = tid; e < N * M; e += 256)
-    gs[e] = g[(size_t)b * N * F * M + (size_t)(e / M) * F * M + (size_t)f * M + (e % M)];
-  __syncthreads();
-  if (t >= T) return;
-  model_power<R, M>(l, gs, N, fl, iy, y);
-  phi_point<R, M>(xtv, iy, gs, N, phi + (size_t)b * 2 * N * FT, FT, (size_t)f * T + t);
+    for (int n = 0; n < NMAX; ++n) l[n] = n < N ? lb[(size_t)n * FT] : R(0);
+    R xtv[M], iy[M], y[M];
+    RowIO<R, M>::load(xt + (((size_t)b * F + f) * T + tc) * M, xtv);
+    for (int e = tid; e < N * M; e += 256)
+      gs[e] = g[(size_t)b * N * F * M + (size_t)(e / M) * F * M + (size_t)f * M + (e % M)];
+    __syncthreads();
+    if (t >= T) return;
+    model_power<R, M>(l, gs, N, fl, iy, y);
+    phi_point<R, M>(xtv, iy, gs, N, phi + (size_t)b * 2 * N * FT, FT, (size_t)f * T + t);
+  } else {
+    for (int e = tid; e < N * M; e += 256)
+      gs[e] = g[(size_t)b * N * F * M + (size_t)(e / M) * F * M + (size_t)f * M + (e % M)];
+    __syncthreads();
+    if (t >= T) return;
+    const R fl = floorp[b];
+    const R* lb = lam + (size_t)b * N * FT + (size_t)f * T + t;
+    R l[NMAX];
+#pragma unroll
+    for (int n = 0; n < NMAX; ++n) l[n] = n < N ? lb[(size_t)n * FT] : R(0);
+    R xtv[M], iy[M], y[M];
+    RowIO<R, M>::load(xt + (((size_t)b * F + f) * T + t) * M, xtv);
+    model_power<R, M>(l, gs, N, fl, iy, y);
+    phi_point<R, M>(xtv, iy, gs, N, phi + (size_t)b * 2 * N * FT, FT, (size_t)f * T + t);
+  }
 }
 
 }  // namespace fm

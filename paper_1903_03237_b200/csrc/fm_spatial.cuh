@@ -75,7 +75,7 @@ template <typename R, int M> struct GaCfg {
   // do not collide; the lambda rows by 8 so the (source, slice) loads of a
   // warp fall into distinct banks
   static constexpr int RS = M + ((sizeof(R) == 4 && M == 8) ? 4 : 0);
-  static constexpr int LS = TB + ((sizeof(R) == 4) ? 8 : 1);
+  static constexpr int LS = TB + ((sizeof(R) == 4 && M <= 8) ? 8 : 1);
   static constexpr bool ALIAS = RED <= 2 * TB * RS;  // reduction reuses the staged rows
 };
 
@@ -112,9 +112,13 @@ __global__ void __launch_bounds__(256) k_gain(GainArgs<R> a) {
     }
     RowIO<R, M>::load(xtb + (size_t)tc * M, xp);
   };
-  if (tid < TB) fetch(ta);  // in flight before the gains are staged (one round trip, not two)
+  // M <= 8: the first chunk is in flight before the gains are staged (one
+  // round trip, not two); M = 16 keeps the fetch behind them (c3: the 24
+  // prefetched values held across the staging cost more than they save)
+  if (M <= 8 && tid < TB) fetch(ta);
   for (int e = tid; e < N * M; e += 256)
     gs[e] = a.g[(size_t)b * N * F * M + (size_t)(e / M) * F * M + (size_t)f * M + (e % M)];
+  if (M > 8 && tid < TB) fetch(ta);
   // accumulate mapping: thread = (NP sources from n1, MQ consecutive
   // channels, slice); with MQ = 4 and N even a thread takes a source pair, so
   // one pair of 16-B loads of x~/y^2 and 1/y feeds 16 FMAs (c3: the loop was
@@ -123,18 +127,8 @@ __global__ void __launch_bounds__(256) k_gain(GainArgs<R> a) {
   // (only when enough items remain that the slice reduction stays short:
   // c3 k_gain 489 -> 418 us; c1, 4 pair items, 18.4 -> 20.5 us, so not there)
   const int NP = (Cf::PAIRS && (N % 2) == 0 && (N / 2) * Q >= 8) ? 2 : 1;
-  const int E = (N / NP) * Q;
-  int S, e1, s1;
-  if ((E & (E - 1)) == 0) {  // power of two (the BASELINE shapes): shifts, no integer divisions
-    const int sh = __ffs(E) - 1;
-    S = 256 >> sh;
-    e1 = tid & (E - 1);
-    s1 = tid >> sh;
-  } else {
-    S = 256 / E;
-    e1 = tid % E;
-    s1 = tid / E;
-  }
+  const int E = (N / NP) * Q, S = 256 / E;
+  const int e1 = tid % E, s1 = tid / E;
   const int n1 = (e1 / Q) * NP, m0 = (e1 % Q) * MQ;
   R num[2][MQ], den[2][MQ];
 #pragma unroll
@@ -603,7 +597,7 @@ __global__ void __launch_bounds__(IpCfg<M>::BS) k_ip(IpArgs<R> a) {
       }
       __syncwarp();
       double la = 0.0;
-      const bool ok = warp_inv_pivot<M>(Ai, lane, &la);
+      const bool ok = warp_inv_pivot<M, C2, true>(Ai, lane, &la);
       if (lane == 0) {
         misc[0] = la;
         flags[0] = ok ? 0 : 1;
