@@ -42,7 +42,7 @@ static int check_m(int64_t M) {
 // per device. A small LRU keeps a few problems alive at once.
 struct GraphEntry {
   int dev = -1;
-  unsigned variant = 0;
+  unsigned long long variant = 0;
   int unroll = 1;  // iterations captured in the graph
   bool dp = false;
   fm_dims d;
@@ -402,7 +402,7 @@ static int graph_unroll(const fm_dims* d, int n_iterations) {
 
 // The cached graph of `unroll` consecutive iterations (captured on a miss).
 static int graph_for(const fm_dims* d, const fm_state* s, const fm_dp* p, int unroll, int dev,
-                     unsigned variant, cudaGraphExec_t* out) {
+                     unsigned long long variant, cudaGraphExec_t* out) {
   auto one = [&](void* strm) { return p ? fm_iterate_dp(d, s, p, strm) : fm_iterate(d, s, strm); };
   GraphEntry* hit = nullptr;
   for (auto& e : g_graphs) {
@@ -462,7 +462,7 @@ static int run_common(const fm_dims* d, const fm_state* s, const fm_dp* p, int n
   int dev = 0;
   FM_CUDA(cudaGetDevice(&dev));
   if (dev < 0 || dev >= MAX_DEV) { set_error("device %d", dev); return FM_EINVAL; }
-  const unsigned variant = variant_key(d);
+  const unsigned long long variant = variant_key(d);
   const int U = graph_unroll(d, n_iterations);
   std::lock_guard<std::mutex> lk(g_graph_mu);
   cudaGraphExec_t ex = nullptr;

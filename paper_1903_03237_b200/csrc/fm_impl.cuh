@@ -265,13 +265,16 @@ inline int pass_stages_override() {
 
 // Everything outside fm_dims that changes which kernels an iteration
 // launches: part of the CUDA-graph cache key (fm_api.cu run_common).
-inline unsigned variant_key(const fm_dims* d) {
-  return (unsigned)vacc_mode(d) | ((unsigned)(gseg_override() & 0xff) << 4) |
+inline unsigned long long variant_key(const fm_dims* d) {
+  const unsigned lo = (unsigned)vacc_mode(d) | ((unsigned)(gseg_override() & 0xff) << 4) |
          ((unsigned)(pass_ctas_override() & 0xfff) << 12) | ((unsigned)pass_stages_override() << 26) |
          ((unsigned)use_fused(d) << 31) | ((unsigned)ip_warp_mode(d) << 3) |
          ((unsigned)use_bin(d) << 30) |
          ((unsigned)small_m_mode() << 2) | ((unsigned)back_tc_mode() << 29) |
          ((unsigned)back_tc_forced() << 25) | ((unsigned)lambda_tc_mode(d, d->dp ? 1 : 0) << 24);
+  // k_vacc_p knobs (chunk size, CTAs per SM) above the 32 selection bits
+  return (unsigned long long)lo | ((unsigned long long)(vp_tb() == 128) << 32) |
+         ((unsigned long long)vp_ctas_per_sm() << 33);
 }
 
 inline Plan make_plan(const fm_dims* d) {
