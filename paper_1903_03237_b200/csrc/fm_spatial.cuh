@@ -856,7 +856,7 @@ template <typename R> struct BackArgs {
 inline int back_ppt(long long M, long long T) { return (M <= 4 && T >= 512) ? 2 : 1; }
 
 template <typename R, int M, int PPT>
-__global__ void __launch_bounds__(256, (M > 8 ? 2 : 3)) k_back(BackArgs<R> a) {
+__global__ void __launch_bounds__(256, (M > 8 ? 2 : (M == 8 && sizeof(R) == 4 ? 4 : 3))) k_back(BackArgs<R> a) {
   pdl_entry();
   using C = cplx<R>;
   __shared__ __align__(16) C Qr[M * M];
